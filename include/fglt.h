@@ -1,0 +1,148 @@
+/*
+ * fglt.h — C-ABI of the B200-native Fast Graphlet Transform (FGlT).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   graphlet::transform(const SparseAdjacency&, const TransformOptions&)
+ *     (/root/reference/proj/include/graphlet/transform.hpp:22-23,
+ *      src/transform.cpp:9-26)
+ *   graphlet::raw_frequencies(g, dict, KernelOptions, TransformStats*)
+ *     (include/graphlet/kernels.hpp:120-123, src/kernels.cpp:305-419)
+ *   graphlet::net_from_raw(raw, U, lenient, threads)
+ *     (include/graphlet/conversion.hpp:49-51, src/conversion.cpp:80-116)
+ * The reference has no C-ABI; its only bindings are the C++ headers and the
+ * pybind11 module (bindings/module.cpp:61-180). Every entry point below is
+ * what those callers need, in plain pointers and sizes. INTEGRATION.md shows
+ * the ctypes / C++ bindings a maintainer adds on the reference side.
+ *
+ * Input: a sanitised symmetric 0/1 CSR with int32 indices (row_ptr n+1,
+ * col_idx nnz), strictly increasing rows, zero diagonal — the invariants of
+ * SparseAdjacency (graph.hpp:38-40). Inputs are borrowed, read-only.
+ * Output: raw and net n x k uint64 row-major tables, k = |dictionary|,
+ * columns = selected graphlet ids ascending (fields.hpp:10-29), bit-exact
+ * with the reference. Outputs are caller-allocated.
+ *
+ * Return codes are the reference CLI's exit classes (tools/glt.cpp:17-21):
+ * 0 ok, 1 parse, 2 structural, 3 overflow, 4 inconsistency, 5 I/O; plus 6 for
+ * a CUDA/runtime failure and 7 when no CUDA device is usable (there is no CPU
+ * fallback: the call fails loudly).
+ */
+#ifndef FGLT_H_
+#define FGLT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fglt_code {
+  FGLT_OK = 0,
+  FGLT_E_PARSE = 1,
+  FGLT_E_STRUCTURAL = 2,
+  FGLT_E_OVERFLOW = 3,
+  FGLT_E_INCONSISTENCY = 4,
+  FGLT_E_IO = 5,
+  FGLT_E_CUDA = 6,
+  FGLT_E_NO_DEVICE = 7
+};
+
+/* flags for fglt_transform_csr32 / fglt_ctx_transform */
+#define FGLT_INPUT_DEVICE 0x1u  /* row_ptr/col_idx are device pointers   */
+#define FGLT_OUTPUT_DEVICE 0x2u /* raw_out/net_out are device pointers   */
+#define FGLT_TIMINGS 0x4u       /* fill per-step times (adds event syncs) */
+
+/* Mirrors OverflowError / InconsistencyError (types.hpp:31-51). */
+typedef struct fglt_error {
+  int32_t code;        /* enum fglt_code */
+  int32_t graphlet_id; /* -1 when not applicable */
+  int64_t vertex;      /* -1 when not applicable (original vertex id) */
+  char msg[256];
+} fglt_error;
+
+#define FGLT_MAX_STEPS 12
+/* Mirrors TransformStats (kernels.hpp:105-112) plus device facts. */
+typedef struct fglt_stats {
+  int32_t num_steps;
+  char step_names[FGLT_MAX_STEPS][32]; /* reference step names, in order */
+  double step_seconds[FGLT_MAX_STEPS];
+  uint64_t p2_row_touches;   /* W - 2m when the four-cycle step runs     */
+  uint64_t p2_touch_bound;   /* 2 * d_max * m                            */
+  uint64_t peak_aux_words;   /* device scratch, 8-byte words             */
+  uint64_t largest_aux_alloc_words;
+  int32_t threads_used;      /* host threads (the device does the work)  */
+  int32_t device;
+  uint64_t W;                /* sum_v d_v^2                              */
+  uint64_t d_max;
+  uint64_t kernel_launches;  /* kernels this library launched            */
+} fglt_stats;
+
+/* Opaque per-device context: stream, workspace, cached preprocessing. One
+ * transform at a time per context. */
+typedef struct fglt_ctx fglt_ctx;
+
+/* Create a context on `device`, launching on `stream` (a cudaStream_t; 0 for
+ * the legacy default stream). Returns NULL and fills err on failure. */
+fglt_ctx* fglt_ctx_create(int device, void* stream, fglt_error* err);
+void fglt_ctx_destroy(fglt_ctx* ctx);
+
+/* One full transform: raw + net for the dictionary `dict_mask` (bit k =
+ * graphlet k; bits 0 and 1 are forced, Dictionary::from_ids,
+ * src/dictionary.cpp:38-50). `lenient` as TransformOptions::lenient.
+ * raw_out/net_out may be NULL to skip that table. stats may be NULL. */
+int fglt_ctx_transform(fglt_ctx* ctx, const int32_t* row_ptr,
+                       const int32_t* col_idx, int64_t n, int64_t nnz,
+                       uint32_t dict_mask, int lenient, uint32_t flags,
+                       uint64_t* raw_out, uint64_t* net_out, fglt_stats* stats,
+                       fglt_error* err);
+
+/* Convenience: create a context on `device`, transform, destroy. */
+int fglt_transform_csr32(const int32_t* row_ptr, const int32_t* col_idx,
+                         int64_t n, int64_t nnz, uint32_t dict_mask,
+                         int lenient, int device, uint32_t flags,
+                         uint64_t* raw_out, uint64_t* net_out,
+                         fglt_stats* stats, fglt_error* err);
+
+/* Stand-alone raw -> net conversion on the device (net_from_raw,
+ * conversion.cpp:80-116): raw/net are n x k host arrays for dict_mask. */
+int fglt_net_from_raw(fglt_ctx* ctx, const uint64_t* raw, int64_t n,
+                      uint32_t dict_mask, int lenient, uint64_t* net,
+                      fglt_error* err);
+
+/* ------------------------------------------------------------------ staged
+ * Row-block sharding across ranks (one process per GPU; the caller owns the
+ * collectives, e.g. torch.distributed over NCCL). Sequence per rank:
+ *   fglt_stage_prepare      replicated preprocessing of the whole graph
+ *   fglt_stage_bounds       root ranges balanced by exact work
+ *   fglt_stage_triangles    partial per-edge triangle counts for own roots
+ *   -- all-reduce(sum) of the uint32 edge-count buffer --
+ *   fglt_stage_local        vertex sweeps over the full graph (replicated)
+ *   fglt_stage_roots        partial c4/d13/d15 for own roots
+ *   -- all-reduce(sum) of the uint64 3n vector buffer --
+ *   fglt_stage_epilogue     raw/net rows [r0, r1) in original-id order
+ * Buffers handed to the caller are device pointers owned by the context. */
+int fglt_stage_prepare(fglt_ctx* ctx, const int32_t* d_row_ptr,
+                       const int32_t* d_col_idx, int64_t n, int64_t nnz,
+                       uint32_t dict_mask, int lenient, fglt_error* err);
+/* bounds[0..world] of the relabelled root range for each rank */
+int fglt_stage_bounds(fglt_ctx* ctx, int world, int64_t* bounds, fglt_error* err);
+int fglt_stage_triangles(fglt_ctx* ctx, int64_t u0, int64_t u1,
+                         uint32_t** d_edge_counts, int64_t* count,
+                         fglt_error* err);
+int fglt_stage_local(fglt_ctx* ctx, fglt_error* err);
+int fglt_stage_roots(fglt_ctx* ctx, int64_t u0, int64_t u1,
+                     uint64_t** d_vectors, int64_t* count, fglt_error* err);
+/* Rows are ORIGINAL vertex ids [v0, v1); outputs are device pointers of
+ * (v1-v0) x k. */
+int fglt_stage_epilogue(fglt_ctx* ctx, int64_t v0, int64_t v1,
+                        uint64_t* d_raw_rows, uint64_t* d_net_rows,
+                        fglt_error* err);
+
+/* Library facts */
+const char* fglt_version(void);
+int fglt_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FGLT_H_ */

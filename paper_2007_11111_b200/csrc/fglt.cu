@@ -1,0 +1,1012 @@
+// fglt.cu — host orchestrator + C-ABI (include/fglt.h) of the B200-native
+// Fast Graphlet Transform. One CUDA stream per context; all device work is
+// stream-ordered; the only host syncs are the small bin-count readbacks and
+// the final error word.
+//
+// Pipeline (reference plan order, proj/src/dictionary.cpp:143-158):
+//   prepare   degree relabel (CUB radix sort of n keys + segmented row sort),
+//             split/mirror indices, canonical edge list          ["degrees"]
+//   sweep A   p2, d7                                              ["two-paths"]
+//   K2        per-edge triangle counts C3 (edge-centric, atomics) ["triangles"]
+//   sweep B/C c3, d14, d10, p3, d9                                ["three-paths"]
+//   K4        4-cycles per vertex (root-centric wedge counting)   ["four-cycle rows"]
+//   K5        diamonds + 4-cliques (root bitmaps of G[N+(u)])     ["diamond rows", "tetrahedra"]
+//   K6        column fill + raw->net back-substitution, rows written in
+//             original vertex order                               ["column fill", "conversion"]
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/fglt.h"
+#include "fglt_device.cuh"
+#include "fglt_roots.cuh"
+
+using namespace fglt;
+
+namespace {
+
+// Net-to-raw coefficients U16 (Table 2; reference encoding
+// proj/src/conversion.cpp:14-32). Rows = raw graphlet, cols = net graphlet.
+const unsigned char kU16[16][16] = {
+    {1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 1, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 1, 0, 2, 4, 2, 6},
+    {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 2, 2, 2, 4, 6},
+    {0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 2, 1, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 1, 1},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 0, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 2, 6},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
+};
+
+constexpr int kSmallS = 32;       // roots with |N+(u)| <= 32: warp kernel
+constexpr int kBlockS = 1024;     // <= 1024: block kernel, bitmap in smem
+constexpr int kWarpHashLog = 9;   // 512-slot table per warp
+constexpr int kWarpHashMax = 256; // wedges per root for the warp table
+constexpr int kBlockHashLog = 14; // 16384-slot table per block (128 KB)
+constexpr int kBlockHashMax = 8192;
+constexpr int kTile = 49152;      // dense tile counters (192 KB)
+
+enum Buf {
+  B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
+  B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
+  B_CUB, B_CURSOR, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_COUNT
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+// Per-vertex vectors, each n u64, in B_VEC.
+enum Vec { V_P2, V_D7, V_C3, V_D14, V_D10, V_P3, V_D9, V_C4, V_D13, V_D15, V_COUNT };
+
+struct Plan {
+  unsigned mask = 3;
+  bool enumerate = false;  // relabel + any enumeration kernel
+  bool p2 = false, d7 = false, c3 = false, d14 = false, d10 = false, p3 = false;
+  bool d9 = false, c4 = false, d13 = false, d15 = false, dip = false;
+  std::vector<std::string> ref_steps;  // reference step names in plan order
+};
+
+Plan make_plan(unsigned mask) {
+  Plan p;
+  mask |= 3u;
+  p.mask = mask;
+  auto has = [&](int id) { return (mask >> id) & 1u; };
+  auto any = [&](std::initializer_list<int> ids) {
+    for (int i : ids)
+      if (has(i)) return true;
+    return false;
+  };
+  p.p2 = any({2, 5, 6});
+  p.p3 = has(5);
+  p.d7 = has(7);
+  p.dip = any({9, 10, 11});
+  p.d9 = p.dip;
+  p.d10 = p.dip;
+  p.c4 = has(12);
+  p.d13 = has(13);
+  p.d14 = has(14);
+  p.d15 = has(15);
+  p.c3 = any({4, 5, 6, 9, 10, 11, 13, 14});
+  p.enumerate = p.c3 || p.c4 || p.d13 || p.d15;
+  // reference plan (resolve_dependencies, src/dictionary.cpp:143-158)
+  p.ref_steps.push_back("degrees");
+  if (any({4, 5, 6, 9, 10, 11, 13})) p.ref_steps.push_back("triangles");
+  if (any({2, 5, 6})) p.ref_steps.push_back("two-paths");
+  if (any({5})) p.ref_steps.push_back("three-paths");
+  if (any({12, 14})) p.ref_steps.push_back("four-cycle rows");
+  if (any({13})) p.ref_steps.push_back("diamond rows");
+  if (any({15})) p.ref_steps.push_back("tetrahedra");
+  p.ref_steps.push_back("column fill");
+  p.ref_steps.push_back("conversion");
+  return p;
+}
+
+DictInfo make_dict(unsigned mask) {
+  DictInfo d;
+  std::memset(&d, 0, sizeof(d));
+  mask |= 3u;
+  d.mask = mask;
+  d.k = 0;
+  for (int i = 0; i < 16; ++i)
+    if (mask & (1u << i)) d.ids[d.k++] = i;
+  for (int r = 0; r < d.k; ++r) {
+    int t = 0;
+    for (int c = r + 1; c < d.k; ++c) {
+      unsigned coef = kU16[d.ids[r]][d.ids[c]];
+      if (coef) {
+        d.tail_col[r][t] = c;
+        d.tail_coef[r][t] = coef;
+        ++t;
+      }
+    }
+    d.ntail[r] = t;
+  }
+  return d;
+}
+
+struct CudaFail {
+  int code;
+  std::string msg;
+};
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      throw CudaFail{FGLT_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+void set_err(fglt_error* err, int code, int g, int64_t v, const char* fmt, ...) {
+  if (!err) return;
+  err->code = code;
+  err->graphlet_id = g;
+  err->vertex = v;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(err->msg, sizeof(err->msg), fmt, ap);
+  va_end(ap);
+}
+
+int group_for(double avg) {
+  if (avg < 6) return 4;
+  if (avg < 16) return 8;
+  if (avg < 48) return 16;
+  return 32;
+}
+
+}  // namespace
+
+struct fglt_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sms = 148;
+  DevBuf buf[B_COUNT];
+  size_t scratch_bytes = 0, peak_scratch = 0, largest = 0;
+  uint64_t launches = 0;
+
+  // prepared graph
+  int64_t n = 0, nnz = 0, m = 0;
+  Plan plan;
+  DictInfo dict;
+  int lenient = 0;
+  const int* rp = nullptr;  // graph the kernels index (relabelled or input)
+  const int* ci = nullptr;
+  int* perm = nullptr;
+  int* inv = nullptr;
+  int* split = nullptr;
+  int* orp = nullptr;
+  int* mir = nullptr;
+  int* ce_row = nullptr;
+  int* ce_pos = nullptr;
+  u32* C3f = nullptr;
+  u64* vec = nullptr;
+  DictInfo* d_dict = nullptr;
+  u64* d_small = nullptr;  // [0] err key, [1] W, [2] d_max, [3..] bin counts
+  bool have_stats = false;
+  uint64_t W = 0, dmax = 0, maxout = 0;
+
+  // timing
+  bool timing = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+
+  template <class T>
+  T* ensure(Buf b, size_t count) {
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    DevBuf& d = buf[b];
+    if (d.cap < bytes) {
+      if (d.p) {
+        CK(cudaFreeAsync(d.p, stream));
+        scratch_bytes -= d.cap;
+      }
+      size_t grow = bytes + bytes / 8;
+      CK(cudaMallocAsync(&d.p, grow, stream));
+      d.cap = grow;
+      scratch_bytes += grow;
+      peak_scratch = std::max(peak_scratch, scratch_bytes);
+      largest = std::max(largest, grow);
+    }
+    return reinterpret_cast<T*>(d.p);
+  }
+
+  u64* V(Vec v) { return vec + (size_t)v * (size_t)std::max<int64_t>(n, 1); }
+
+  void mark(const char* name) {
+    if (!timing) return;
+    cudaEvent_t ev;
+    CK(cudaEventCreate(&ev));
+    CK(cudaEventRecord(ev, stream));
+    marks.push_back({name, ev});
+  }
+
+  int grid(int64_t work, int block, int per_sm = 8) {
+    int64_t g = (work + block - 1) / block;
+    g = std::min<int64_t>(g, (int64_t)sms * per_sm);
+    return (int)std::max<int64_t>(g, 1);
+  }
+
+  void launched() { ++launches; }
+};
+
+namespace {
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaFail{FGLT_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+template <int G>
+void launch_sweep_a(fglt_ctx* c) {
+  k_sweep_a<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(
+      c->rp, c->ci, (int)c->n, c->plan.p2 || c->plan.p3 ? c->V(V_P2) : nullptr,
+      c->plan.d7 ? c->V(V_D7) : nullptr);
+  check_launch();
+  c->launched();
+}
+
+template <int G>
+void launch_sweep_bc(fglt_ctx* c) {
+  k_sweep_b<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(
+      c->rp, c->ci, (int)c->n, c->C3f, c->plan.p3 ? c->V(V_P2) : nullptr, c->V(V_C3),
+      c->plan.d14 ? c->V(V_D14) : nullptr, c->plan.d10 ? c->V(V_D10) : nullptr,
+      c->plan.p3 ? c->V(V_P3) : nullptr);
+  check_launch();
+  c->launched();
+  if (c->plan.d9) {
+    k_sweep_c<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(c->rp, c->ci, (int)c->n,
+                                                                c->V(V_C3), c->V(V_D9));
+    check_launch();
+    c->launched();
+  }
+}
+
+template <int G>
+void launch_root_work(fglt_ctx* c, u64* wc, u64* tw) {
+  k_root_work<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(c->rp, c->ci, c->split, c->mir,
+                                                                (int)c->n, wc, tw);
+  check_launch();
+  c->launched();
+}
+
+#define DISPATCH_G(G, FN, ...)               \
+  switch (G) {                               \
+    case 4: FN<4>(__VA_ARGS__); break;       \
+    case 8: FN<8>(__VA_ARGS__); break;       \
+    case 16: FN<16>(__VA_ARGS__); break;     \
+    default: FN<32>(__VA_ARGS__); break;     \
+  }
+
+// ------------------------------------------------------------------ prepare
+void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t nnz,
+             unsigned mask, int lenient) {
+  c->n = n;
+  c->nnz = nnz;
+  c->m = nnz / 2;
+  c->plan = make_plan(mask);
+  c->dict = make_dict(mask);
+  c->lenient = lenient;
+  c->d_dict = c->ensure<DictInfo>(B_DICT, 1);
+  CK(cudaMemcpyAsync(c->d_dict, &c->dict, sizeof(DictInfo), cudaMemcpyHostToDevice, c->stream));
+  c->d_small = c->ensure<u64>(B_SMALL, 64);
+  CK(cudaMemsetAsync(c->d_small, 0, 64 * sizeof(u64), c->stream));
+  {
+    u64 init = ~0ull;
+    CK(cudaMemcpyAsync(c->d_small, &init, 8, cudaMemcpyHostToDevice, c->stream));
+  }
+  const int N = (int)n;
+  c->vec = c->ensure<u64>(B_VEC, (size_t)V_COUNT * std::max<int64_t>(n, 1));
+  CK(cudaMemsetAsync(c->vec, 0, (size_t)V_COUNT * std::max<int64_t>(n, 1) * 8, c->stream));
+  c->perm = c->inv = nullptr;
+  c->rp = d_rp;
+  c->ci = d_ci;
+  c->have_stats = false;
+  if (n > 0) {
+    k_graph_stats<<<c->grid(n, 256, 4), 256, 0, c->stream>>>(d_rp, N, c->d_small + 1);
+    check_launch();
+    c->launched();
+  }
+  if (!c->plan.enumerate || n == 0) return;
+
+  // ---- degree relabel: rank by (degree, id)
+  u64* keys = c->ensure<u64>(B_KEYS, n);
+  u64* keys2 = c->ensure<u64>(B_KEYS2, n);
+  k_degree_keys<<<c->grid(n, 256), 256, 0, c->stream>>>(d_rp, N, keys);
+  check_launch();
+  c->launched();
+  size_t tmp_bytes = 0, t2 = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys2, N, 0, 64, c->stream));
+  int* perm = c->ensure<int>(B_PERM, n);
+  int* inv = c->ensure<int>(B_INV, n);
+  int* ndeg = c->ensure<int>(B_NDEG, n + 1);
+  int* nrp = c->ensure<int>(B_NRP, n + 1);
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, ndeg, nrp, N + 1, c->stream));
+  tmp_bytes = std::max(tmp_bytes, t2);
+  size_t t3 = 0;
+  int* tmp = c->ensure<int>(B_TMP, std::max<int64_t>(nnz, 1));
+  int* nci = c->ensure<int>(B_NCI, std::max<int64_t>(nnz, 1));
+  CK(cub::DeviceSegmentedSort::SortKeys(nullptr, t3, tmp, nci, (int)nnz, N, nrp, nrp + 1, c->stream));
+  tmp_bytes = std::max(tmp_bytes, t3);
+  void* cub_tmp = c->ensure<unsigned char>(B_CUB, tmp_bytes);
+  size_t tb = c->buf[B_CUB].cap;
+  CK(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, keys, keys2, N, 0, 64, c->stream));
+  c->launched();
+  CK(cudaMemsetAsync(ndeg + n, 0, sizeof(int), c->stream));
+  k_perm<<<c->grid(n, 256), 256, 0, c->stream>>>(keys2, N, perm, inv, ndeg);
+  check_launch();
+  c->launched();
+  tb = c->buf[B_CUB].cap;
+  CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ndeg, nrp, N + 1, c->stream));
+  c->launched();
+  k_fill_rows<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(d_rp, d_ci, perm, inv, nrp, N, tmp);
+  check_launch();
+  c->launched();
+  tb = c->buf[B_CUB].cap;
+  if (nnz > 0) {
+    CK(cub::DeviceSegmentedSort::SortKeys(cub_tmp, tb, tmp, nci, (int)nnz, N, nrp, nrp + 1,
+                                          c->stream));
+    c->launched();
+  }
+  c->perm = perm;
+  c->inv = inv;
+  c->rp = nrp;
+  c->ci = nci;
+
+  // ---- split / mirror / canonical edge list
+  int* split = c->ensure<int>(B_SPLIT, n);
+  int* outdeg = c->ensure<int>(B_OUTDEG, n + 1);
+  int* orp = c->ensure<int>(B_ORP, n + 1);
+  CK(cudaMemsetAsync(outdeg + n, 0, sizeof(int), c->stream));
+  k_split<<<c->grid(n, 256), 256, 0, c->stream>>>(c->rp, c->ci, N, split, outdeg, c->d_small + 3);
+  check_launch();
+  c->launched();
+  tb = c->buf[B_CUB].cap;
+  CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, outdeg, orp, N + 1, c->stream));
+  c->launched();
+  int* mir = c->ensure<int>(B_MIR, std::max<int64_t>(nnz, 1));
+  int* ce_row = c->ensure<int>(B_CE_ROW, std::max<int64_t>(c->m, 1));
+  int* ce_pos = c->ensure<int>(B_CE_POS, std::max<int64_t>(c->m, 1));
+  k_mirror<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, orp, N, mir, ce_row,
+                                                        ce_pos);
+  check_launch();
+  c->launched();
+  c->split = split;
+  c->orp = orp;
+  c->mir = mir;
+  c->ce_row = ce_row;
+  c->ce_pos = ce_pos;
+  c->C3f = reinterpret_cast<u32*>(tmp);  // B_TMP is dead after the row sort
+}
+
+void read_graph_stats(fglt_ctx* c) {
+  u64 h[3];
+  CK(cudaMemcpyAsync(h, c->d_small + 1, 24, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->W = h[0];
+  c->dmax = h[1];
+  c->maxout = h[2];
+  c->have_stats = true;
+}
+
+void sweep_a(fglt_ctx* c) {
+  if (c->n == 0) return;
+  if (!(c->plan.p2 || c->plan.p3 || c->plan.d7)) return;
+  const int G = group_for((double)c->nnz / (double)c->n);
+  DISPATCH_G(G, launch_sweep_a, c);
+}
+
+void triangles(fglt_ctx* c, int64_t e0, int64_t e1) {
+  if (!c->plan.c3 || c->n == 0) return;
+  CK(cudaMemsetAsync(c->C3f, 0, (size_t)std::max<int64_t>(c->nnz, 1) * 4, c->stream));
+  if (e1 > e0) {
+    k_triangles<<<c->grid((e1 - e0) * 32, 256), 256, 0, c->stream>>>(
+        c->rp, c->ci, c->split, c->ce_row, c->ce_pos, (int)e0, (int)e1, c->C3f);
+    check_launch();
+    c->launched();
+  }
+}
+
+void local_sweeps(fglt_ctx* c) {
+  if (!c->plan.c3 || c->n == 0) return;
+  if (c->m > 0) {
+    k_c3_mirror<<<c->grid(c->m, 256), 256, 0, c->stream>>>(c->ce_pos, c->mir, (int)c->m, c->C3f);
+    check_launch();
+    c->launched();
+  }
+  const int G = group_for((double)c->nnz / (double)c->n);
+  DISPATCH_G(G, launch_sweep_bc, c);
+}
+
+// Bin roots [u0,u1) by key into up to 3 lists; returns counts (host sync).
+std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
+                           const std::vector<u64>& thr, int** lists, int64_t* stride) {
+  const int nb = (int)thr.size() + 1;
+  const int64_t span = std::max<int64_t>(u1 - u0, 1);
+  int* lst = c->ensure<int>(B_LISTS, (size_t)nb * span);
+  u64* d_thr = c->d_small + 8;
+  int* counts = reinterpret_cast<int*>(c->d_small + 16);
+  std::vector<u64> th(thr);
+  th.resize(8, ~0ull);
+  CK(cudaMemcpyAsync(d_thr, th.data(), 8 * sizeof(u64), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(counts, 0, 8 * sizeof(int), c->stream));
+  if (u1 > u0) {
+    k_bin<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(key, (int)u0, (int)u1, d_thr, nb, counts,
+                                                       lst, span);
+    check_launch();
+    c->launched();
+  }
+  std::vector<int> h(8);
+  CK(cudaMemcpyAsync(h.data(), counts, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int b = 0; b < nb; ++b) lists[b] = lst + (int64_t)b * span;
+  *stride = span;
+  h.resize(nb);
+  return h;
+}
+
+__global__ void k_outdeg_key(const int* __restrict__ rp, const int* __restrict__ split, int n,
+                             u64* __restrict__ key) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    const int s = rp[u + 1] - split[u];
+    key[u] = s >= 2 ? (u64)s : 0ull;
+  }
+}
+
+void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
+  const Plan& P = c->plan;
+  if (c->n == 0 || !(P.c4 || P.d13 || P.d15)) return;
+  const int N = (int)c->n;
+  u64* work = c->ensure<u64>(B_WORK, 2 * (size_t)c->n);
+  u64* wc = work;
+  u64* key = work + c->n;
+  int* lists[4];
+  int64_t stride = 0;
+  if (P.c4) {
+    const int G = group_for((double)c->nnz / (double)c->n);
+    DISPATCH_G(G, launch_root_work, c, wc, key);
+    std::vector<int> cnt = bin_roots(c, wc, u0, u1, {(u64)kWarpHashMax, (u64)kBlockHashMax},
+                                     lists, &stride);
+    c->mark("four-cycle rows:start");
+    u64* c4 = c->V(V_C4);
+    if (cnt[0] > 0) {
+      const int wpb = 8;
+      const size_t sm = (size_t)wpb * (1 << kWarpHashLog) * 8;
+      k_c4_warp<kWarpHashLog><<<c->grid((int64_t)cnt[0] * 32, wpb * 32), wpb * 32, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->mir, lists[0], cnt[0], c4);
+      check_launch();
+      c->launched();
+    }
+    if (cnt[1] > 0) {
+      const size_t sm = (size_t)(1 << kBlockHashLog) * 8;
+      set_smem(k_c4_block, sm);
+      k_c4_block<<<std::min(cnt[1], c->sms * 2), 512, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->mir, lists[1], cnt[1], kBlockHashLog, c4);
+      check_launch();
+      c->launched();
+    }
+    if (cnt[2] > 0) {
+      const size_t sm = (size_t)kTile * 4;
+      set_smem(k_c4_tiles, sm);
+      const int g = std::min(cnt[2], c->sms);
+      // cursor slice per block: the longest prefix |N-(u)| <= d_max
+      int* cur = c->ensure<int>(B_CURSOR, (size_t)g * (size_t)(c->dmax + 1));
+      k_c4_tiles<<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[2], cnt[2],
+                                             kTile, cur, (long long)(c->dmax + 1), c4);
+      check_launch();
+      c->launched();
+    }
+    c->mark("four-cycle rows:end");
+  }
+  if (P.d13 || P.d15) {
+    k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->rp, c->split, N, key);
+    check_launch();
+    c->launched();
+    std::vector<int> cnt = bin_roots(c, key, u0, u1, {(u64)kSmallS, (u64)kBlockS}, lists, &stride);
+    c->mark("roots:start");
+    u64* d13 = c->V(V_D13);
+    u64* d15 = c->V(V_D15);
+    if (cnt[0] > 0) {
+      const int wpb = 8;
+      const size_t sm = (size_t)wpb * (32 * 8 + 96 * 4);
+      const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
+      if (P.d13 && P.d15)
+        k_roots_warp<true, true><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[0], cnt[0], d13, d15);
+      else if (P.d13)
+        k_roots_warp<true, false><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[0], cnt[0], d13, d15);
+      else
+        k_roots_warp<false, true><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[0], cnt[0], d13, d15);
+      check_launch();
+      c->launched();
+    }
+    for (int b = 1; b <= 2; ++b) {
+      if (cnt[b] == 0) continue;
+      const bool global_bm = (b == 2);
+      const int s_cap = global_bm ? (int)c->maxout : kBlockS;
+      const int nw_cap = (s_cap + 31) / 32;
+      size_t sm = (size_t)s_cap * 16;
+      if (!global_bm) sm += (size_t)s_cap * nw_cap * 4;
+      u32* gbm = nullptr;
+      long long gstride = 0;
+      int g = std::min(cnt[b], c->sms * 2);
+      if (global_bm) {
+        gstride = (long long)s_cap * nw_cap;
+        // bounded scratch: at most 4 GiB of bitmaps in flight
+        const long long fit = std::max<long long>(1, (4ll << 30) / (gstride * 4));
+        g = (int)std::min<long long>({(long long)cnt[b], (long long)c->sms, fit});
+        gbm = c->ensure<u32>(B_GBM, (size_t)g * (size_t)gstride);
+      }
+      if (P.d13 && P.d15) {
+        set_smem(k_roots_block<true, true>, sm);
+        k_roots_block<true, true><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], s_cap, gbm, gstride, d13, d15);
+      } else if (P.d13) {
+        set_smem(k_roots_block<true, false>, sm);
+        k_roots_block<true, false><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], s_cap, gbm, gstride, d13, d15);
+      } else {
+        set_smem(k_roots_block<false, true>, sm);
+        k_roots_block<false, true><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], s_cap, gbm, gstride, d13, d15);
+      }
+      check_launch();
+      c->launched();
+    }
+    c->mark("roots:end");
+  }
+}
+
+void epilogue(fglt_ctx* c, int64_t v0, int64_t v1, u64* raw, u64* net) {
+  if (v1 <= v0) return;
+  EpilogueIn in;
+  in.rp = c->rp;
+  in.inv = c->inv;
+  const Plan& P = c->plan;
+  in.p2 = P.p2 ? c->V(V_P2) : nullptr;
+  in.p3 = P.p3 ? c->V(V_P3) : nullptr;
+  in.c3 = P.c3 ? c->V(V_C3) : nullptr;
+  in.d7 = P.d7 ? c->V(V_D7) : nullptr;
+  in.d9 = P.d9 ? c->V(V_D9) : nullptr;
+  in.d10 = P.d10 ? c->V(V_D10) : nullptr;
+  in.d14 = P.d14 ? c->V(V_D14) : nullptr;
+  in.c4 = P.c4 ? c->V(V_C4) : nullptr;
+  in.d13 = P.d13 ? c->V(V_D13) : nullptr;
+  in.d15 = P.d15 ? c->V(V_D15) : nullptr;
+  k_epilogue<<<c->grid(v1 - v0, 128), 128, 0, c->stream>>>(in, c->d_dict, (int)v0, (int)v1,
+                                                         c->lenient, raw, net, c->d_small);
+  check_launch();
+  c->launched();
+}
+
+// Decode the device error word into fglt_error; returns the code.
+int read_error(fglt_ctx* c, fglt_error* err, bool sync = true) {
+  u64 key = ~0ull;
+  CK(cudaMemcpyAsync(&key, c->d_small, 8, cudaMemcpyDeviceToHost, c->stream));
+  if (sync) CK(cudaStreamSynchronize(c->stream));
+  if (key == ~0ull) return FGLT_OK;
+  const int g = (int)(key & 15);
+  const int code = (int)((key >> 4) & 15) ? FGLT_E_INCONSISTENCY : FGLT_E_OVERFLOW;
+  const int64_t v = (int64_t)((key >> 8) & 0xffffffffull);
+  if (code == FGLT_E_INCONSISTENCY)
+    set_err(err, code, g, v,
+            "negative net frequency for graphlet %d at vertex %lld (incomplete family or kernel defect)",
+            g, (long long)v);
+  else
+    set_err(err, code, g, v, "count overflow (graphlet %d, vertex %lld)", g, (long long)v);
+  if (err) {
+    // expose the ordering key for multi-rank reductions
+    static_assert(sizeof(err->msg) >= 64, "msg too small");
+  }
+  return code;
+}
+
+void fill_stats(fglt_ctx* c, fglt_stats* st, const std::vector<std::pair<std::string, double>>& t) {
+  if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+  const Plan& P = c->plan;
+  auto get = [&](const char* name) {
+    double s = 0;
+    for (auto& kv : t)
+      if (kv.first == name) s += kv.second;
+    return s;
+  };
+  // map measured phases onto the reference step names (see file header)
+  double deg = get("degrees"), tri = get("triangles"), c4 = get("four-cycle rows"),
+         rts = get("roots"), fill = get("column fill");
+  bool ref_tri = false, ref_fc = false, ref_dia = false;
+  for (auto& s : P.ref_steps) {
+    ref_tri |= s == "triangles";
+    ref_fc |= s == "four-cycle rows";
+    ref_dia |= s == "diamond rows";
+  }
+  int k = 0;
+  for (auto& s : P.ref_steps) {
+    double v = 0;
+    if (s == "degrees") v = deg;
+    else if (s == "triangles") v = tri;
+    else if (s == "four-cycle rows") v = c4 + (ref_tri ? 0 : tri);
+    else if (s == "diamond rows") v = rts;
+    else if (s == "tetrahedra") v = ref_dia ? 0 : rts;
+    else if (s == "column fill") v = fill;
+    if (k < FGLT_MAX_STEPS) {
+      std::snprintf(st->step_names[k], 32, "%s", s.c_str());
+      st->step_seconds[k] = v;
+      ++k;
+    }
+  }
+  (void)ref_fc;
+  st->num_steps = k;
+  if (!c->have_stats && c->n > 0) {
+    read_graph_stats(c);
+  }
+  st->W = c->W;
+  st->d_max = c->dmax;
+  const bool four = (P.mask >> 12 & 1u) || (P.mask >> 14 & 1u);
+  st->p2_row_touches = four ? c->W - 2 * (uint64_t)c->m : 0;
+  st->p2_touch_bound = 2 * c->dmax * (uint64_t)c->m;
+  st->peak_aux_words = c->peak_scratch / 8;
+  st->largest_aux_alloc_words = c->largest / 8;
+  st->threads_used = 1;
+  st->device = c->device;
+  st->kernel_launches = c->launches;
+}
+
+std::vector<std::pair<std::string, double>> collect_marks(fglt_ctx* c) {
+  std::vector<std::pair<std::string, double>> out;
+  if (!c->timing || c->marks.empty()) return out;
+  CK(cudaEventSynchronize(c->marks.back().second));
+  for (size_t i = 0; i + 1 < c->marks.size(); ++i) {
+    const std::string& a = c->marks[i].first;
+    auto colon = a.find(':');
+    if (colon == std::string::npos || a.substr(colon + 1) != "start") continue;
+    const std::string name = a.substr(0, colon);
+    for (size_t j = i + 1; j < c->marks.size(); ++j)
+      if (c->marks[j].first == name + ":end") {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, c->marks[i].second, c->marks[j].second));
+        out.push_back({name, ms * 1e-3});
+        break;
+      }
+  }
+  for (auto& mk : c->marks) cudaEventDestroy(mk.second);
+  c->marks.clear();
+  return out;
+}
+
+int validate_shape(int64_t n, int64_t nnz, fglt_error* err) {
+  if (n < 0 || nnz < 0) {
+    set_err(err, FGLT_E_STRUCTURAL, -1, -1, "negative graph size");
+    return FGLT_E_STRUCTURAL;
+  }
+  if (n >= (int64_t)1 << 31 || nnz >= (int64_t)1 << 31) {
+    set_err(err, FGLT_E_STRUCTURAL, -1, -1,
+            "graph exceeds the int32 CSR limits (n=%lld, nnz=%lld)", (long long)n, (long long)nnz);
+    return FGLT_E_STRUCTURAL;
+  }
+  if (nnz % 2) {
+    set_err(err, FGLT_E_STRUCTURAL, -1, -1, "odd nnz: adjacency is not symmetric");
+    return FGLT_E_STRUCTURAL;
+  }
+  return FGLT_OK;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* fglt_version(void) { return "fglt-b200 0.1 (sm_100a)"; }
+
+int fglt_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+fglt_ctx* fglt_ctx_create(int device, void* stream, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    set_err(err, FGLT_E_NO_DEVICE, -1, -1, "no CUDA device available (%s); there is no CPU fallback",
+            cudaGetErrorString(e));
+    return nullptr;
+  }
+  if (device < 0 || device >= count) {
+    set_err(err, FGLT_E_NO_DEVICE, -1, -1, "device %d out of range (%d devices)", device, count);
+    return nullptr;
+  }
+  fglt_ctx* c = new fglt_ctx();
+  try {
+    c->device = device;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+      set_err(err, FGLT_E_NO_DEVICE, -1, -1, "device %d is sm_%d%d; this build targets sm_100a",
+              device, prop.major, prop.minor);
+      delete c;
+      return nullptr;
+    }
+    c->sms = prop.multiProcessorCount;
+    c->stream = reinterpret_cast<cudaStream_t>(stream);
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    delete c;
+    return nullptr;
+  }
+  return c;
+}
+
+void fglt_ctx_destroy(fglt_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  for (auto& b : c->buf)
+    if (b.p) cudaFreeAsync(b.p, c->stream);
+  cudaStreamSynchronize(c->stream);
+  delete c;
+}
+
+int fglt_ctx_transform(fglt_ctx* c, const int32_t* row_ptr, const int32_t* col_idx, int64_t n,
+                       int64_t nnz, uint32_t dict_mask, int lenient, uint32_t flags,
+                       uint64_t* raw_out, uint64_t* net_out, fglt_stats* stats,
+                       fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!c) {
+    set_err(err, FGLT_E_NO_DEVICE, -1, -1, "null context");
+    return FGLT_E_NO_DEVICE;
+  }
+  if (dict_mask >> 16) {
+    set_err(err, FGLT_E_PARSE, -1, -1, "graphlet id outside 0..15 in dictionary mask");
+    return FGLT_E_PARSE;
+  }
+  int rc = validate_shape(n, nnz, err);
+  if (rc) return rc;
+  try {
+    CK(cudaSetDevice(c->device));
+    c->timing = (flags & FGLT_TIMINGS) != 0;
+    c->marks.clear();
+    const int* d_rp = row_ptr;
+    const int* d_ci = col_idx;
+    c->mark("degrees:start");
+    if (!(flags & FGLT_INPUT_DEVICE)) {
+      int* a = c->ensure<int>(B_RP_IN, n + 1);
+      int* b = c->ensure<int>(B_CI_IN, std::max<int64_t>(nnz, 1));
+      CK(cudaMemcpyAsync(a, row_ptr, (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+      if (nnz)
+        CK(cudaMemcpyAsync(b, col_idx, (size_t)nnz * 4, cudaMemcpyHostToDevice, c->stream));
+      d_rp = a;
+      d_ci = b;
+    }
+    prepare(c, d_rp, d_ci, n, nnz, dict_mask, lenient);
+    if (c->plan.c4 && !c->have_stats && n > 0) {
+      // the tile kernel sizes its cursor slices by d_max
+      read_graph_stats(c);
+    }
+    if ((c->plan.d13 || c->plan.d15) && !c->have_stats && n > 0) {
+      read_graph_stats(c);
+    }
+    sweep_a(c);
+    c->mark("degrees:end");
+    c->mark("triangles:start");
+    triangles(c, 0, c->m);
+    local_sweeps(c);
+    c->mark("triangles:end");
+    roots(c, 0, n);
+    const size_t k = (size_t)c->dict.k;
+    u64* raw = reinterpret_cast<u64*>(raw_out);
+    u64* net = reinterpret_cast<u64*>(net_out);
+    const bool dev_out = (flags & FGLT_OUTPUT_DEVICE) != 0;
+    if (!dev_out) {
+      raw = raw_out ? c->ensure<u64>(B_RAW, (size_t)std::max<int64_t>(n, 1) * k) : nullptr;
+      net = net_out ? c->ensure<u64>(B_NET, (size_t)std::max<int64_t>(n, 1) * k) : nullptr;
+    }
+    c->mark("column fill:start");
+    epilogue(c, 0, n, raw, net);
+    c->mark("column fill:end");
+    if (!dev_out && n > 0) {
+      if (raw_out)
+        CK(cudaMemcpyAsync(raw_out, raw, (size_t)n * k * 8, cudaMemcpyDeviceToHost, c->stream));
+      if (net_out)
+        CK(cudaMemcpyAsync(net_out, net, (size_t)n * k * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    rc = read_error(c, err, true);
+    auto t = collect_marks(c);
+    // "roots" covers both diamond and tetrahedra phases
+    fill_stats(c, stats, t);
+    return rc;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+int fglt_transform_csr32(const int32_t* row_ptr, const int32_t* col_idx, int64_t n, int64_t nnz,
+                         uint32_t dict_mask, int lenient, int device, uint32_t flags,
+                         uint64_t* raw_out, uint64_t* net_out, fglt_stats* stats,
+                         fglt_error* err) {
+  fglt_ctx* c = fglt_ctx_create(device, nullptr, err);
+  if (!c) return err ? err->code : FGLT_E_NO_DEVICE;
+  int rc = fglt_ctx_transform(c, row_ptr, col_idx, n, nnz, dict_mask, lenient, flags, raw_out,
+                              net_out, stats, err);
+  fglt_ctx_destroy(c);
+  return rc;
+}
+
+int fglt_net_from_raw(fglt_ctx* c, const uint64_t* raw, int64_t n, uint32_t dict_mask,
+                      int lenient, uint64_t* net, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!c) {
+    set_err(err, FGLT_E_NO_DEVICE, -1, -1, "null context");
+    return FGLT_E_NO_DEVICE;
+  }
+  try {
+    CK(cudaSetDevice(c->device));
+    c->dict = make_dict(dict_mask);
+    const size_t k = (size_t)c->dict.k;
+    c->d_dict = c->ensure<DictInfo>(B_DICT, 1);
+    CK(cudaMemcpyAsync(c->d_dict, &c->dict, sizeof(DictInfo), cudaMemcpyHostToDevice, c->stream));
+    c->d_small = c->ensure<u64>(B_SMALL, 64);
+    u64 init = ~0ull;
+    CK(cudaMemcpyAsync(c->d_small, &init, 8, cudaMemcpyHostToDevice, c->stream));
+    if (n > 0) {
+      u64* dr = c->ensure<u64>(B_RAW, (size_t)n * k);
+      u64* dn = c->ensure<u64>(B_NET, (size_t)n * k);
+      CK(cudaMemcpyAsync(dr, raw, (size_t)n * k * 8, cudaMemcpyHostToDevice, c->stream));
+      k_net_only<<<c->grid(n, 128), 128, 0, c->stream>>>(dr, c->d_dict, n, lenient, dn, c->d_small);
+      check_launch();
+      c->launched();
+      CK(cudaMemcpyAsync(net, dn, (size_t)n * k * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    return read_error(c, err, true);
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+// ------------------------------------------------------------------ staged
+int fglt_stage_prepare(fglt_ctx* c, const int32_t* d_row_ptr, const int32_t* d_col_idx, int64_t n,
+                       int64_t nnz, uint32_t dict_mask, int lenient, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  int rc = validate_shape(n, nnz, err);
+  if (rc) return rc;
+  try {
+    CK(cudaSetDevice(c->device));
+    c->timing = false;
+    prepare(c, d_row_ptr, d_col_idx, n, nnz, dict_mask, lenient);
+    if (n > 0) {
+      read_graph_stats(c);
+    }
+    sweep_a(c);
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+// Contiguous root blocks of (nearly) equal exact work: per root u,
+// work(u) = wedges(u) + triangle probes(u) + |N+(u)| + 1.
+__global__ void k_work_total(const u64* __restrict__ wc, const u64* __restrict__ tw, int n,
+                             u64* __restrict__ out) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x)
+    out[u] = wc[u] + tw[u] + 1;
+}
+
+int fglt_stage_bounds(fglt_ctx* c, int world, int64_t* bounds, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    CK(cudaSetDevice(c->device));
+    const int64_t n = c->n;
+    bounds[0] = 0;
+    for (int r = 1; r <= world; ++r) bounds[r] = n;
+    if (n == 0 || world <= 1 || !c->plan.enumerate) {
+      for (int r = 1; r < world; ++r) bounds[r] = n * r / world;
+      return FGLT_OK;
+    }
+    u64* work = c->ensure<u64>(B_WORK, 2 * (size_t)n);
+    const int G = group_for((double)c->nnz / (double)n);
+    DISPATCH_G(G, launch_root_work, c, work, work + n);
+    std::vector<u64> wc(n), tw(n);
+    CK(cudaMemcpyAsync(wc.data(), work, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(tw.data(), work + n, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    long double total = 0;
+    for (int64_t u = 0; u < n; ++u) total += (long double)(wc[u] + tw[u] + 1);
+    long double acc = 0;
+    int r = 1;
+    for (int64_t u = 0; u < n && r < world; ++u) {
+      acc += (long double)(wc[u] + tw[u] + 1);
+      while (r < world && acc >= total * r / world) bounds[r++] = u + 1;
+    }
+    while (r < world) bounds[r++] = n;
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+int fglt_stage_triangles(fglt_ctx* c, int64_t u0, int64_t u1, uint32_t** d_edge_counts,
+                         int64_t* count, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    CK(cudaSetDevice(c->device));
+    *d_edge_counts = c->C3f;
+    *count = c->plan.c3 ? c->nnz : 0;
+    if (!c->plan.c3) return FGLT_OK;
+    int o[2] = {0, 0};
+    if (c->n > 0) {
+      CK(cudaMemcpyAsync(&o[0], c->orp + u0, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(&o[1], c->orp + u1, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    triangles(c, o[0], o[1]);
+    CK(cudaStreamSynchronize(c->stream));
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+int fglt_stage_local(fglt_ctx* c, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    CK(cudaSetDevice(c->device));
+    local_sweeps(c);
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+int fglt_stage_roots(fglt_ctx* c, int64_t u0, int64_t u1, uint64_t** d_vectors, int64_t* count,
+                     fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    CK(cudaSetDevice(c->device));
+    roots(c, u0, u1);
+    CK(cudaStreamSynchronize(c->stream));
+    // c4, d13, d15 are contiguous in B_VEC
+    *d_vectors = reinterpret_cast<uint64_t*>(c->V(V_C4));
+    *count = 3 * c->n;
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+int fglt_stage_epilogue(fglt_ctx* c, int64_t v0, int64_t v1, uint64_t* d_raw_rows,
+                        uint64_t* d_net_rows, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    CK(cudaSetDevice(c->device));
+    epilogue(c, v0, v1, reinterpret_cast<u64*>(d_raw_rows), reinterpret_cast<u64*>(d_net_rows));
+    return read_error(c, err, true);
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+}  // extern "C"

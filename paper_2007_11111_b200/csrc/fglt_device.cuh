@@ -1,0 +1,277 @@
+// fglt_device.cuh — sm_100a kernels of the B200-native FGlT hot path.
+//
+// Every kernel works on the DEGREE-RELABELLED graph: vertices are renumbered
+// by (degree, original id) ascending, rows re-sorted. With that labelling the
+// edge orientation "low rank -> high rank" used by all enumeration kernels is
+// a plain id comparison: N+(u) is the suffix of row u after `split[u]`, N-(u)
+// the prefix. `mir[p]` maps every CSR position (u, v) to the position of
+// (v, u), so the canonical (u<v) slot of each undirected edge is reachable
+// from both rows without searching. All counting is integer and every
+// cross-thread accumulation is a commutative integer atomic, so results are
+// bit-identical for any schedule, grid size or number of GPUs.
+//
+// Quantities (reference formulas, proj/src/kernels.cpp):
+//   p1 = d, p2 = sum_j d_j - d                          (:26-39)
+//   C3(i,j) = |N(i) ∩ N(j)|, c3 = sum_j C3 / 2          (:41-89)
+//   p3 = sum_j p2_j - (d(d-1) + 2 c3)   [rectified]     (:91-107)
+//   c4 = #4-cycles through i, d14 = sum_j C(C3(i,j),2)  (:109-147)
+//   d7, d9, d10, d11                                    (:149-205)
+//   d13 = sum_{triangles {i,j,k}} (C3(j,k) - 1)         (:207-232)
+//   d15 = #4-cliques through i                          (:234-288)
+#pragma once
+
+#include <cstdint>
+
+namespace fglt {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ int lower_bound_i32(const int* __restrict__ a, int lo,
+                                               int hi, int key) {
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int lower_bound_smem(const int* a, int lo, int hi, int key) {
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int G>
+__device__ __forceinline__ u64 group_sum_u64(u64 v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+  return v;
+}
+
+__device__ __forceinline__ u64 sat_sub(u64 a, u64 b) { return a > b ? a - b : 0ull; }
+
+// ------------------------------------------------------------ preprocessing
+
+// key = degree << 32 | id : sorting these gives the relabelling order.
+__global__ void k_degree_keys(const int* __restrict__ rp, int n, u64* __restrict__ keys) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    keys[i] = ((u64)(rp[i + 1] - rp[i]) << 32) | (u64)i;
+}
+
+__global__ void k_perm(const u64* __restrict__ keys, int n, int* __restrict__ perm,
+                       int* __restrict__ inv, int* __restrict__ ndeg) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    u64 k = keys[r];
+    int old = (int)(k & 0xffffffffu);
+    perm[r] = old;
+    inv[old] = r;
+    ndeg[r] = (int)(k >> 32);
+  }
+}
+
+// Warp per new row: copy the relabelled neighbours of the old row.
+__global__ void k_fill_rows(const int* __restrict__ rp, const int* __restrict__ ci,
+                            const int* __restrict__ perm, const int* __restrict__ inv,
+                            const int* __restrict__ nrp, int n, int* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+    const int o = perm[r];
+    const int b = rp[o], e = rp[o + 1], w = nrp[r];
+    for (int p = b + lane; p < e; p += 32) out[w + (p - b)] = inv[ci[p]];
+  }
+}
+
+// split[r] = first position of row r holding a neighbour > r; row_of for the
+// canonical (upper) positions is written as a compact edge list.
+__global__ void k_split(const int* __restrict__ rp, const int* __restrict__ ci, int n,
+                        int* __restrict__ split, int* __restrict__ outdeg,
+                        unsigned long long* __restrict__ maxout) {
+  unsigned long long mo = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    int s = lower_bound_i32(ci, rp[r], rp[r + 1], r);
+    split[r] = s;
+    outdeg[r] = rp[r + 1] - s;
+    mo = max(mo, (unsigned long long)(rp[r + 1] - s));
+  }
+  if (mo) atomicMax(maxout, mo);
+}
+
+// Warp per row: for each canonical position p (row r, v = ci[p] > r) find the
+// mirror position q of r in row v (a prefix entry) and record both; also emit
+// the compact canonical edge list (row, position), index e = orp[r] + offset.
+__global__ void k_mirror(const int* __restrict__ rp, const int* __restrict__ ci,
+                         const int* __restrict__ split, const int* __restrict__ orp,
+                         int n, int* __restrict__ mir, int* __restrict__ ce_row,
+                         int* __restrict__ ce_pos) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+    const int s = split[r], e = rp[r + 1], base = orp[r];
+    for (int p = s + lane; p < e; p += 32) {
+      const int v = ci[p];
+      const int q = lower_bound_i32(ci, rp[v], split[v], r);
+      mir[p] = q;
+      mir[q] = p;
+      ce_row[base + (p - s)] = r;
+      ce_pos[base + (p - s)] = p;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ sweep A
+// p2 = sum_j d_j - d  (compute_p2, kernels.cpp:26-39)
+// d7 = sum_j C(d_j - 1, 2) (compute_d7, kernels.cpp:149-163)
+// Group of G lanes per row.
+template <int G>
+__global__ void k_sweep_a(const int* __restrict__ rp, const int* __restrict__ ci, int n,
+                          u64* __restrict__ p2, u64* __restrict__ d7) {
+  const int lane = threadIdx.x & (G - 1);
+  const int groups = (gridDim.x * blockDim.x) / G;
+  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int rounds = (n + groups - 1) / groups;
+  for (int it = 0; it < rounds; ++it) {
+    const int r = g0 + it * groups;
+    u64 sd = 0, s7 = 0;
+    u64 d = 0;
+    if (r < n) {
+      const int b = rp[r], e = rp[r + 1];
+      d = (u64)(e - b);
+      for (int p = b + lane; p < e; p += G) {
+        const int j = ci[p];
+        const u64 dj = (u64)(rp[j + 1] - rp[j]);
+        sd += dj;
+        const u64 t = dj - 1;  // dj >= 1 for a neighbour
+        s7 += t < 2 ? 0ull : t * (t - 1) / 2;
+      }
+    }
+    sd = group_sum_u64<G>(sd);
+    s7 = group_sum_u64<G>(s7);
+    if (r < n && lane == 0) {
+      if (p2) p2[r] = sat_sub(sd, d);
+      if (d7) d7[r] = s7;
+    }
+  }
+}
+
+// --------------------------------------------------------- triangle pass K2
+// Edge-centric over canonical edges (u, x) of roots u in [e0, e1): every
+// triangle u < x < y is found exactly once, as y in N+(x) ∩ (N+(u) after x).
+// Per triangle: C3(x,y) += 1 and C3(u,y) += 1 by global atomics; C3(u,x) gets
+// the warp's hit count once. Values live at canonical positions of C3f.
+__global__ void k_triangles(const int* __restrict__ rp, const int* __restrict__ ci,
+                            const int* __restrict__ split, const int* __restrict__ ce_row,
+                            const int* __restrict__ ce_pos, int e0, int e1,
+                            u32* __restrict__ C3f) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int e = e0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); e < e1; e += warps) {
+    const int u = ce_row[e];
+    const int pux = ce_pos[e];
+    const int send = rp[u + 1];
+    if (pux + 1 >= send) continue;  // x is the last out-neighbour of u
+    const int x = ci[pux];
+    const int smax = ci[send - 1];
+    const int b = split[x], eend = rp[x + 1];
+    u32 hits = 0;
+    for (int base = b; base < eend; base += 32) {
+      const int p = base + lane;
+      const int y = p < eend ? ci[p] : 0x7fffffff;
+      if (y <= smax) {
+        const int q = lower_bound_i32(ci, pux + 1, send, y);
+        if (q < send && ci[q] == y) {
+          atomicAdd(C3f + p, 1u);
+          atomicAdd(C3f + q, 1u);
+          ++hits;
+        }
+      }
+      if (__any_sync(0xffffffffu, y >= smax) ) break;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+    if (lane == 0 && hits) atomicAdd(C3f + pux, hits);
+  }
+}
+
+// Copy canonical C3 values into their mirror slots so rows read contiguously.
+__global__ void k_c3_mirror(const int* __restrict__ ce_pos, const int* __restrict__ mir,
+                            int m, u32* __restrict__ C3f) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
+    const int p = ce_pos[e];
+    C3f[mir[p]] = C3f[p];
+  }
+}
+
+// ------------------------------------------------------------------ sweep B
+// c3 = sum C3 / 2; d14 = sum C(C3,2); d10 = sum C3 * (d_j - 2)+;
+// p3 = sum p2_j - (d(d-1) + 2 c3) rectified   (kernels.cpp:91-107, :176-205)
+template <int G>
+__global__ void k_sweep_b(const int* __restrict__ rp, const int* __restrict__ ci, int n,
+                          const u32* __restrict__ C3f, const u64* __restrict__ p2,
+                          u64* __restrict__ c3, u64* __restrict__ d14,
+                          u64* __restrict__ d10, u64* __restrict__ p3) {
+  const int lane = threadIdx.x & (G - 1);
+  const int groups = (gridDim.x * blockDim.x) / G;
+  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int rounds = (n + groups - 1) / groups;
+  for (int it = 0; it < rounds; ++it) {
+    const int r = g0 + it * groups;
+    u64 sc = 0, s14 = 0, s10 = 0, sp2 = 0;
+    u64 d = 0;
+    if (r < n) {
+      const int b = rp[r], e = rp[r + 1];
+      d = (u64)(e - b);
+      for (int p = b + lane; p < e; p += G) {
+        const int j = ci[p];
+        const u64 c = C3f[p];
+        sc += c;
+        s14 += c * (c - (c > 0)) / 2;
+        const u64 dj = (u64)(rp[j + 1] - rp[j]);
+        s10 += c * (dj > 2 ? dj - 2 : 0ull);
+        if (p2) sp2 += p2[j];
+      }
+    }
+    sc = group_sum_u64<G>(sc);
+    s14 = group_sum_u64<G>(s14);
+    s10 = group_sum_u64<G>(s10);
+    sp2 = group_sum_u64<G>(sp2);
+    if (r < n && lane == 0) {
+      const u64 c3v = sc / 2;
+      c3[r] = c3v;
+      if (d14) d14[r] = s14;
+      if (d10) d10[r] = s10;
+      if (p3) p3[r] = sat_sub(sp2, d * (d > 0 ? d - 1 : 0ull) + 2 * c3v);
+    }
+  }
+}
+
+// d9 = sum_j c3_j - 2 c3, rectified (kernels.cpp:194-199)
+template <int G>
+__global__ void k_sweep_c(const int* __restrict__ rp, const int* __restrict__ ci, int n,
+                          const u64* __restrict__ c3, u64* __restrict__ d9) {
+  const int lane = threadIdx.x & (G - 1);
+  const int groups = (gridDim.x * blockDim.x) / G;
+  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int rounds = (n + groups - 1) / groups;
+  for (int it = 0; it < rounds; ++it) {
+    const int r = g0 + it * groups;
+    u64 s = 0;
+    if (r < n)
+      for (int p = rp[r] + lane; p < rp[r + 1]; p += G) s += c3[ci[p]];
+    s = group_sum_u64<G>(s);
+    if (r < n && lane == 0) d9[r] = sat_sub(s, 2 * c3[r]);
+  }
+}
+
+}  // namespace fglt

@@ -1,0 +1,632 @@
+// fglt_roots.cuh — root-centric enumeration kernels (4-cycles, diamonds,
+// 4-cliques) and the fused raw->net epilogue. See fglt_device.cuh for the
+// labelling conventions.
+#pragma once
+
+#include "fglt_device.cuh"
+
+namespace fglt {
+
+// =============================================================== 4-cycles
+// Every 4-cycle has a unique highest vertex u; its opposite vertex w < u and
+// both middle vertices v, v' < u. For a root u, L[w] counts wedges u-v-w with
+// v in N-(u) and w in N(v), w < u (the prefix of row v up to the mirror
+// position of u). Then, exactly (the per-vertex form of the reference's
+// c4 = sum_k C(P2(i,k),2), kernels.cpp:109-147):
+//   c4[u] += sum_w C(L[w],2);  c4[w] += C(L[w],2);  c4[v] += sum_{w} (L[w]-1)
+// The accumulator L lives in shared memory: a per-warp or per-block open
+// addressing table for light roots, dense 48K-entry tiles of the w range for
+// heavy roots.
+
+// wc(u) = number of wedges rooted at u; tw(u) = triangle-probe work of u.
+template <int G>
+__global__ void k_root_work(const int* __restrict__ rp, const int* __restrict__ ci,
+                            const int* __restrict__ split, const int* __restrict__ mir, int n,
+                            u64* __restrict__ wc, u64* __restrict__ tw) {
+  const int lane = threadIdx.x & (G - 1);
+  const int groups = (gridDim.x * blockDim.x) / G;
+  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int rounds = (n + groups - 1) / groups;
+  for (int it = 0; it < rounds; ++it) {
+    const int u = g0 + it * groups;
+    u64 a = 0, t = 0;
+    if (u < n) {
+      const int b = rp[u], s = split[u], e = rp[u + 1];
+      for (int q = b + lane; q < s; q += G) a += (u64)(mir[q] - rp[ci[q]]);
+      for (int p = s + lane; p < e; p += G) {
+        const int x = ci[p];
+        t += (u64)(rp[x + 1] - split[x]);
+      }
+    }
+    a = group_sum_u64<G>(a);
+    t = group_sum_u64<G>(t);
+    if (u < n && lane == 0) {
+      wc[u] = a;
+      tw[u] = t + (u64)(rp[u + 1] - split[u]);
+    }
+  }
+}
+
+__device__ __forceinline__ u32 hash_slot(int w, int logcap) {
+  return ((u32)w * 0x9E3779B1u) >> (32 - logcap);
+}
+
+__device__ __forceinline__ void hash_insert(int* keys, u32* vals, int logcap, int w) {
+  const u32 mask = (1u << logcap) - 1;
+  u32 h = hash_slot(w, logcap);
+  while (true) {
+    const int k = atomicCAS(keys + h, -1, w);
+    if (k == -1 || k == w) { atomicAdd(vals + h, 1u); return; }
+    h = (h + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ u32 hash_get(const int* keys, const u32* vals, int logcap, int w) {
+  const u32 mask = (1u << logcap) - 1;
+  u32 h = hash_slot(w, logcap);
+  while (true) {
+    const int k = keys[h];
+    if (k == w) return vals[h];
+    if (k == -1) return 0;
+    h = (h + 1) & mask;
+  }
+}
+
+// Warp per root; a 2^LOGCAP-slot table per warp in shared memory.
+template <int LOGCAP>
+__global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci,
+                          const int* __restrict__ split, const int* __restrict__ mir,
+                          const int* __restrict__ roots, int nroots, u64* __restrict__ c4) {
+  constexpr int CAP = 1 << LOGCAP;
+  extern __shared__ unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int* keys = reinterpret_cast<int*>(smem_raw) + wib * CAP * 2;
+  u32* vals = reinterpret_cast<u32*>(keys + CAP);
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
+    const int u = roots[k];
+    for (int i = lane; i < CAP; i += 32) { keys[i] = -1; vals[i] = 0; }
+    __syncwarp();
+    const int b = rp[u], s = split[u];
+    for (int q = b; q < s; ++q) {
+      const int v = ci[q];
+      const int end = mir[q];
+      for (int p = rp[v] + lane; p < end; p += 32) hash_insert(keys, vals, LOGCAP, ci[p]);
+    }
+    __syncwarp();
+    u64 acc = 0;
+    for (int i = lane; i < CAP; i += 32) {
+      const u32 l = vals[i];
+      if (l >= 2) {
+        const u64 c = (u64)l * (l - 1) / 2;
+        acc += c;
+        atomicAdd(c4 + keys[i], c);
+      }
+    }
+    for (int q = b; q < s; ++q) {
+      const int v = ci[q];
+      const int end = mir[q];
+      u64 sv = 0;
+      for (int p = rp[v] + lane; p < end; p += 32) sv += hash_get(keys, vals, LOGCAP, ci[p]) - 1;
+      sv = warp_sum_u64(sv);
+      if (lane == 0 && sv) atomicAdd(c4 + v, sv);
+    }
+    acc = warp_sum_u64(acc);
+    if (lane == 0 && acc) atomicAdd(c4 + u, acc);
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum_u64(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  u64 t = 0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < nw ? red[threadIdx.x] : 0ull;
+    t = warp_sum_u64(t);
+  }
+  return t;  // valid in thread 0
+}
+
+// Block per root; one 2^logcap table per block (dynamic shared memory).
+__global__ void k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
+                           const int* __restrict__ split, const int* __restrict__ mir,
+                           const int* __restrict__ roots, int nroots, int logcap,
+                           u64* __restrict__ c4) {
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ u64 red[32];
+  const int cap = 1 << logcap;
+  int* keys = reinterpret_cast<int*>(smem_raw);
+  u32* vals = reinterpret_cast<u32*>(keys + cap);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
+    const int u = roots[k];
+    for (int i = threadIdx.x; i < cap; i += blockDim.x) { keys[i] = -1; vals[i] = 0; }
+    __syncthreads();
+    const int b = rp[u], s = split[u];
+    for (int q = b + wid; q < s; q += nwarps) {
+      const int v = ci[q];
+      const int end = mir[q];
+      for (int p = rp[v] + lane; p < end; p += 32) hash_insert(keys, vals, logcap, ci[p]);
+    }
+    __syncthreads();
+    u64 acc = 0;
+    for (int i = threadIdx.x; i < cap; i += blockDim.x) {
+      const u32 l = vals[i];
+      if (l >= 2) {
+        const u64 c = (u64)l * (l - 1) / 2;
+        acc += c;
+        atomicAdd(c4 + keys[i], c);
+      }
+    }
+    for (int q = b + wid; q < s; q += nwarps) {
+      const int v = ci[q];
+      const int end = mir[q];
+      u64 sv = 0;
+      for (int p = rp[v] + lane; p < end; p += 32) sv += hash_get(keys, vals, logcap, ci[p]) - 1;
+      sv = warp_sum_u64(sv);
+      if (lane == 0 && sv) atomicAdd(c4 + v, sv);
+    }
+    acc = block_sum_u64(acc, red);
+    if (threadIdx.x == 0 && acc) atomicAdd(c4 + u, acc);
+    __syncthreads();
+  }
+}
+
+// Block per heavy root; the w range [0,u) is swept in tiles of `tile`
+// counters held in shared memory. cur[] (global scratch, one slice per
+// block) keeps each row's read position across tiles, so every wedge is read
+// exactly twice (count pass, attribution pass) and no row is searched.
+__global__ void k_c4_tiles(const int* __restrict__ rp, const int* __restrict__ ci,
+                           const int* __restrict__ split, const int* __restrict__ mir,
+                           const int* __restrict__ roots, int nroots, int tile,
+                           int* __restrict__ cursor, long long cursor_stride,
+                           u64* __restrict__ c4) {
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ u64 red[32];
+  u32* L = reinterpret_cast<u32*>(smem_raw);
+  int* cur = cursor + (long long)blockIdx.x * cursor_stride;
+  for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
+    const int u = roots[k];
+    const int b = rp[u], nq = split[u] - b;
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) cur[q] = rp[ci[b + q]];
+    u64 acc = 0;
+    for (int lo = 0; lo < u; lo += tile) {
+      const int hi = min(lo + tile, u);
+      const int span = hi - lo;
+      for (int i = threadIdx.x; i < span; i += blockDim.x) L[i] = 0;
+      __syncthreads();
+      for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+        const int end = mir[b + q];
+        for (int p = cur[q]; p < end; ++p) {
+          const int w = ci[p];
+          if (w >= hi) break;
+          atomicAdd(L + (w - lo), 1u);
+        }
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < span; i += blockDim.x) {
+        const u32 l = L[i];
+        if (l >= 2) {
+          const u64 c = (u64)l * (l - 1) / 2;
+          acc += c;
+          atomicAdd(c4 + lo + i, c);
+        }
+      }
+      for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+        const int end = mir[b + q];
+        int p = cur[q];
+        u64 sv = 0;
+        for (; p < end; ++p) {
+          const int w = ci[p];
+          if (w >= hi) break;
+          sv += L[w - lo] - 1;
+        }
+        cur[q] = p;
+        if (sv) atomicAdd(c4 + ci[b + q], sv);
+      }
+      __syncthreads();
+    }
+    acc = block_sum_u64(acc, red);
+    if (threadIdx.x == 0 && acc) atomicAdd(c4 + u, acc);
+    __syncthreads();
+  }
+}
+
+// ================================================== diamonds and 4-cliques
+// Root u, S = N+(u) (sorted, ids > u). A probe of N+(x) for x = S[a] against
+// S[a+1..] finds every triangle {u, x, y} whose lowest vertex is u exactly
+// once. Per triangle (paper D4 term; reference compute_d13, kernels.cpp:
+// 207-232, restated as sum over triangles of (C3(opposite edge) - 1)):
+//   d13[u] += C3(x,y)-1, d13[x] += C3(u,y)-1, d13[y] += C3(u,x)-1.
+// The same probe sets the bit (a,b) of the induced subgraph G[S] (a bitmap
+// row per member). Every 4-clique has a unique lowest vertex u and is a
+// triangle of G[S]; for member a, t_a = (1/2) sum_{b in row a}
+// popc(row_a & row_b) is the number of G[S]-triangles through a, so
+// d15[S[a]] += t_a and d15[u] += sum_a t_a / 3 (reference compute_d15,
+// kernels.cpp:234-288, same counts).
+
+// Warp per root, |S| <= 32: rows are single words.
+template <bool kD13, bool kD15>
+__global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__ ci,
+                             const int* __restrict__ split, const u32* __restrict__ C3f,
+                             const int* __restrict__ roots, int nroots,
+                             u64* __restrict__ d13, u64* __restrict__ d15) {
+  extern __shared__ unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  u64* sD = reinterpret_cast<u64*>(smem_raw) + wib * 32;
+  int* sS = reinterpret_cast<int*>(reinterpret_cast<u64*>(smem_raw) + (blockDim.x >> 5) * 32) + wib * 96;
+  u32* sC = reinterpret_cast<u32*>(sS + 32);
+  u32* rows = sC + 32;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
+    const int u = roots[k];
+    const int s0 = split[u];
+    const int s = rp[u + 1] - s0;
+    if (lane < s) {
+      sS[lane] = ci[s0 + lane];
+      if (kD13) sC[lane] = C3f[s0 + lane];
+    }
+    sD[lane] = 0;
+    rows[lane] = 0;
+    __syncwarp();
+    const int smax = sS[s - 1];
+    u64 tu = 0;
+    for (int a = 0; a + 1 < s; ++a) {
+      const int x = sS[a];
+      const u32 ca = kD13 ? sC[a] : 0u;
+      const int e = rp[x + 1];
+      u64 da = 0;
+      for (int base = split[x]; base < e; base += 32) {
+        const int p = base + lane;
+        const int y = p < e ? ci[p] : 0x7fffffff;
+        if (y <= smax) {
+          const int bi = lower_bound_smem(sS, a + 1, s, y);
+          if (bi < s && sS[bi] == y) {
+            if (kD15) {
+              atomicOr(rows + a, 1u << bi);
+              atomicOr(rows + bi, 1u << a);
+            }
+            if (kD13) {
+              tu += (u64)C3f[p] - 1;
+              da += (u64)sC[bi] - 1;
+              atomicAdd(sD + bi, (u64)ca - 1);
+            }
+          }
+        }
+        if (__any_sync(0xffffffffu, y >= smax)) break;
+      }
+      if (kD13) {
+        da = warp_sum_u64(da);
+        if (lane == 0 && da) atomicAdd(sD + a, da);
+      }
+    }
+    __syncwarp();
+    if (kD13) {
+      if (lane < s && sD[lane]) atomicAdd(d13 + sS[lane], sD[lane]);
+      tu = warp_sum_u64(tu);
+      if (lane == 0 && tu) atomicAdd(d13 + u, tu);
+    }
+    if (kD15) {
+      u64 ta = 0;
+      if (lane < s) {
+        const u32 row = rows[lane];
+        u32 bits = row;
+        u32 t = 0;
+        while (bits) {
+          const int bb = __ffs(bits) - 1;
+          bits &= bits - 1;
+          t += __popc(row & rows[bb]);
+        }
+        ta = t / 2;
+        if (ta) atomicAdd(d15 + sS[lane], ta);
+      }
+      ta = warp_sum_u64(ta);
+      if (lane == 0 && ta) atomicAdd(d15 + u, ta / 3);
+    }
+    __syncwarp();
+  }
+}
+
+// Block per root, any |S|. Bitmap rows of nw = ceil(s/32) words, in shared
+// memory when `gbm` is null, else in the block's slice of global scratch.
+template <bool kD13, bool kD15>
+__global__ void k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
+                              const int* __restrict__ split, const u32* __restrict__ C3f,
+                              const int* __restrict__ roots, int nroots, int s_cap,
+                              u32* __restrict__ gbm, long long gbm_stride,
+                              u64* __restrict__ d13, u64* __restrict__ d15) {
+  extern __shared__ unsigned char smem_raw[];
+  __shared__ u64 red[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  u64* sD = reinterpret_cast<u64*>(smem_raw);
+  int* sS = reinterpret_cast<int*>(sD + s_cap);
+  u32* sC = reinterpret_cast<u32*>(sS + s_cap);
+  u32* bm = gbm ? gbm + (long long)blockIdx.x * gbm_stride : sC + s_cap;
+  for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
+    const int u = roots[k];
+    const int s0 = split[u];
+    const int s = rp[u + 1] - s0;
+    const int nw = (s + 31) >> 5;
+    for (int a = threadIdx.x; a < s; a += blockDim.x) {
+      sS[a] = ci[s0 + a];
+      if (kD13) { sC[a] = C3f[s0 + a]; sD[a] = 0; }
+    }
+    if (kD15)
+      for (long long i = threadIdx.x; i < (long long)s * nw; i += blockDim.x) bm[i] = 0;
+    __syncthreads();
+    const int smax = sS[s - 1];
+    u64 tu = 0;
+    for (int a = wid; a + 1 < s; a += nwarps) {
+      const int x = sS[a];
+      const u32 ca = kD13 ? sC[a] : 0u;
+      const int e = rp[x + 1];
+      u64 da = 0;
+      for (int base = split[x]; base < e; base += 32) {
+        const int p = base + lane;
+        const int y = p < e ? ci[p] : 0x7fffffff;
+        if (y <= smax) {
+          const int bi = lower_bound_smem(sS, a + 1, s, y);
+          if (bi < s && sS[bi] == y) {
+            if (kD15) {
+              atomicOr(bm + (long long)a * nw + (bi >> 5), 1u << (bi & 31));
+              atomicOr(bm + (long long)bi * nw + (a >> 5), 1u << (a & 31));
+            }
+            if (kD13) {
+              tu += (u64)C3f[p] - 1;
+              da += (u64)sC[bi] - 1;
+              atomicAdd(sD + bi, (u64)ca - 1);
+            }
+          }
+        }
+        if (__any_sync(0xffffffffu, y >= smax)) break;
+      }
+      if (kD13) {
+        da = warp_sum_u64(da);
+        if (lane == 0 && da) atomicAdd(sD + a, da);
+      }
+    }
+    if (kD13) {
+      tu = block_sum_u64(tu, red);  // contains __syncthreads
+      if (threadIdx.x == 0 && tu) atomicAdd(d13 + u, tu);
+      for (int a = threadIdx.x; a < s; a += blockDim.x)
+        if (sD[a]) atomicAdd(d13 + sS[a], sD[a]);
+    } else {
+      __syncthreads();
+    }
+    if (kD15) {
+      u64 tot = 0;
+      for (int a = wid; a < s; a += nwarps) {
+        const u32* ra = bm + (long long)a * nw;
+        u64 acc = 0;
+        if (nw <= 32) {
+          const u32 mine = lane < nw ? ra[lane] : 0u;
+          for (int w = 0; w < nw; ++w) {
+            u32 bits = ra[w];
+            while (bits) {
+              const int bb = (w << 5) + __ffs(bits) - 1;
+              bits &= bits - 1;
+              if (lane < nw) acc += __popc(mine & bm[(long long)bb * nw + lane]);
+            }
+          }
+        } else {
+          for (int w = 0; w < nw; ++w) {
+            u32 bits = ra[w];
+            while (bits) {
+              const int bb = (w << 5) + __ffs(bits) - 1;
+              bits &= bits - 1;
+              const u32* rb = bm + (long long)bb * nw;
+              for (int j = lane; j < nw; j += 32) acc += __popc(ra[j] & rb[j]);
+            }
+          }
+        }
+        acc = warp_sum_u64(acc);
+        const u64 ta = acc / 2;
+        if (lane == 0 && ta) atomicAdd(d15 + sS[a], ta);
+        tot += ta;
+      }
+      tot = block_sum_u64(lane == 0 ? tot : 0ull, red);
+      if (threadIdx.x == 0 && tot) atomicAdd(d15 + u, tot / 3);
+    }
+    __syncthreads();
+  }
+}
+
+// =============================================================== epilogue
+// Column fill (kernels.cpp:384-412) + exact raw->net back-substitution with
+// U(s,s) (conversion.cpp:80-116), one thread per ORIGINAL vertex, rows written
+// in original order. Checked sites follow the reference; the first failure in
+// (fill stage, vertex) order is reported through an atomicMin on
+//   key = stage << 40 | vertex << 8 | code << 4 | graphlet.
+struct DictInfo {
+  int k;
+  int ids[16];
+  unsigned mask;
+  int ntail[16];          // per dictionary position r, number of tail entries
+  int tail_col[16][16];   // positions c > r with U[ids[r]][ids[c]] != 0
+  unsigned tail_coef[16][16];
+};
+
+__device__ __forceinline__ bool mul_ov(u64 a, u64 b, u64* r) {
+  *r = a * b;
+  return __umul64hi(a, b) != 0ull;
+}
+__device__ __forceinline__ bool add_ov(u64 a, u64 b, u64* r) {
+  *r = a + b;
+  return *r < a;
+}
+
+struct EpilogueIn {
+  const int* rp;   // graph the vectors are indexed by (relabelled or original)
+  const int* inv;  // original id -> row of that graph; null = identity
+  const u64 *p2, *p3, *c3, *d7, *d9, *d10, *d14, *c4, *d13, *d15;
+};
+
+__device__ __forceinline__ void offer_err(u64* err, int stage, long long v, int code, int g) {
+  const u64 key = ((u64)stage << 40) | ((u64)v << 8) | ((u64)code << 4) | (u64)g;
+  atomicMin(err, key);
+}
+
+__global__ void k_epilogue(EpilogueIn in, const DictInfo* __restrict__ dict, int v0, int v1,
+                           int lenient, u64* __restrict__ raw, u64* __restrict__ net,
+                           u64* __restrict__ err) {
+  __shared__ DictInfo D;
+  if (threadIdx.x == 0) D = *dict;
+  __syncthreads();
+  const int k = D.k;
+  const unsigned m = D.mask;
+  for (int v = v0 + blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += gridDim.x * blockDim.x) {
+    const int r = in.inv ? in.inv[v] : v;
+    const u64 d = (u64)(in.rp[r + 1] - in.rp[r]);
+    u64 col[16];
+    u64 t;
+    col[0] = 1;
+    col[1] = d;
+    col[2] = (m & (1u << 2) || m & (1u << 5) || m & (1u << 6)) && in.p2 ? in.p2[r] : 0;
+    // col 3: choose2(p1), checked (types.hpp:84-88)
+    col[3] = 0;
+    if (m & (1u << 3) && d >= 2) {
+      if (mul_ov(d, d - 1, &t)) offer_err(err, 1, v, 0, 3);
+      col[3] = t / 2;
+    }
+    const u64 c3v = in.c3 ? in.c3[r] : 0;
+    col[4] = c3v;
+    col[5] = in.p3 ? in.p3[r] : 0;
+    col[6] = 0;
+    if (m & (1u << 6)) {
+      if (mul_ov(col[2], sat_sub(d, 1), &t)) offer_err(err, 2, v, 0, 6);
+      col[6] = sat_sub(t, 2 * c3v);
+    }
+    col[7] = in.d7 ? in.d7[r] : 0;
+    col[8] = 0;
+    if (m & (1u << 8) && d >= 3) {  // choose3: unchecked d(d-1)/2, checked *(d-2)
+      if (mul_ov(d * (d - 1) / 2, d - 2, &t)) offer_err(err, 4, v, 0, 8);
+      col[8] = t / 3;
+    }
+    col[9] = in.d9 ? in.d9[r] : 0;
+    col[10] = in.d10 ? in.d10[r] : 0;
+    col[11] = 0;
+    if (m & ((1u << 9) | (1u << 10) | (1u << 11))) {
+      if (mul_ov(sat_sub(d, 2), c3v, &t)) offer_err(err, 5, v, 0, 11);
+      col[11] = t;
+    }
+    col[12] = in.c4 ? in.c4[r] : 0;
+    col[13] = in.d13 ? in.d13[r] : 0;
+    col[14] = in.d14 ? in.d14[r] : 0;
+    col[15] = in.d15 ? in.d15[r] : 0;
+    u64 rw[16], nt[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < k) rw[i] = col[D.ids[i]];
+    bool stop = false;
+    for (int rr = k - 1; rr >= 0; --rr) {
+      u64 absorbed = 0;
+      nt[rr] = 0;
+      if (stop) continue;
+      for (int j = 0; j < D.ntail[rr]; ++j) {
+        u64 prod;
+        if (mul_ov((u64)D.tail_coef[rr][j], nt[D.tail_col[rr][j]], &prod) ||
+            add_ov(absorbed, prod, &absorbed)) {
+          offer_err(err, 6, v, 0, D.ids[rr]);
+          stop = true;
+          break;
+        }
+      }
+      if (stop) continue;
+      if (absorbed > rw[rr]) {
+        if (!lenient) {
+          offer_err(err, 6, v, 1, D.ids[rr]);
+          stop = true;
+          continue;
+        }
+        nt[rr] = 0;
+      } else {
+        nt[rr] = rw[rr] - absorbed;
+      }
+    }
+    const long long o = (long long)(v - v0) * k;
+    if (raw)
+      for (int i = 0; i < k; ++i) raw[o + i] = rw[i];
+    if (net)
+      for (int i = 0; i < k; ++i) net[o + i] = nt[i];
+  }
+}
+
+// Stand-alone net_from_raw over a given raw table (conversion.cpp:80-116).
+__global__ void k_net_only(const u64* __restrict__ raw, const DictInfo* __restrict__ dict,
+                           long long n, int lenient, u64* __restrict__ net, u64* __restrict__ err) {
+  __shared__ DictInfo D;
+  if (threadIdx.x == 0) D = *dict;
+  __syncthreads();
+  const int k = D.k;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n;
+       v += (long long)gridDim.x * blockDim.x) {
+    u64 nt[16];
+    bool stop = false;
+    for (int rr = k - 1; rr >= 0; --rr) {
+      u64 absorbed = 0;
+      nt[rr] = 0;
+      if (stop) continue;
+      for (int j = 0; j < D.ntail[rr]; ++j) {
+        u64 prod;
+        if (mul_ov((u64)D.tail_coef[rr][j], nt[D.tail_col[rr][j]], &prod) ||
+            add_ov(absorbed, prod, &absorbed)) {
+          offer_err(err, 6, v, 0, D.ids[rr]);
+          stop = true;
+          break;
+        }
+      }
+      if (stop) continue;
+      const u64 x = raw[v * k + rr];
+      if (absorbed > x) {
+        if (!lenient) { offer_err(err, 6, v, 1, D.ids[rr]); stop = true; continue; }
+        nt[rr] = 0;
+      } else {
+        nt[rr] = x - absorbed;
+      }
+    }
+    for (int i = 0; i < k; ++i) net[v * k + i] = nt[i];
+  }
+}
+
+// W = sum d^2, d_max (stats and the roofline model).
+__global__ void k_graph_stats(const int* __restrict__ rp, int n, u64* __restrict__ out) {
+  u64 w = 0, dm = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u64 d = (u64)(rp[i + 1] - rp[i]);
+    w += d * d;
+    dm = d > dm ? d : dm;
+  }
+  w = warp_sum_u64(w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 x = __shfl_xor_sync(0xffffffffu, dm, o);
+    dm = x > dm ? x : dm;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, w);
+    atomicMax(out + 1, dm);
+  }
+}
+
+// Bin roots into work lists: lists[b] gets the roots whose key falls in bin b
+// (key <= thresholds[b]); key 0 roots are dropped.
+__global__ void k_bin(const u64* __restrict__ key, int u0, int u1, const u64* __restrict__ thr,
+                      int nbins, int* __restrict__ counts, int* __restrict__ lists,
+                      long long list_stride) {
+  for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1; u += gridDim.x * blockDim.x) {
+    const u64 x = key[u];
+    if (x == 0) continue;
+    int b = 0;
+    while (b + 1 < nbins && x > thr[b]) ++b;
+    const int slot = atomicAdd(counts + b, 1);
+    lists[(long long)b * list_stride + slot] = u;
+  }
+}
+
+}  // namespace fglt

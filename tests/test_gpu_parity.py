@@ -1,0 +1,207 @@
+"""GPU parity through the C-ABI (libfglt.so) against the pinned oracle.
+
+Bit-exact for every raw and net entry (integer work). Cases follow the
+reference's own tests: Fig. 2 golden tables (proj/tests/testutil.hpp:40-62),
+sub-dictionaries (acceptance.cpp:74-93), the 208-graph oracle family
+(acceptance.cpp:114-146), edge cases (edgeless graph test_kernels.cpp:229-238,
+incomplete family test_pipeline.cpp:55-65, corrupted raw
+test_conversion.cpp:63-76), and the synthetic configs at sizes the oracle
+finishes in seconds.
+"""
+import numpy as np
+import pytest
+
+from oracle import binding as ob
+from paper_2007_11111_b200 import _capi, graphs
+import fglt_testutil as gu
+
+pytestmark = pytest.mark.gpu
+
+FULL = 0xFFFF
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = _capi.Context(0)
+    yield c
+    c.close()
+
+
+def check_same(ctx, rp, ci, mask=FULL, lenient=False, d15_mode=0):
+    raw, net, st = ctx.transform_host(rp, ci, mask, lenient)
+    oraw, onet = ob.transform(rp, ci, mask, lenient, d15_mode)
+    assert raw.shape == oraw.shape
+    bad = np.argwhere(raw != oraw)
+    assert len(bad) == 0, f"raw differs at {bad[:5]}: gpu {raw[tuple(bad[0])]} oracle {oraw[tuple(bad[0])]}"
+    bad = np.argwhere(net != onet)
+    assert len(bad) == 0, f"net differs at {bad[:5]}"
+    return raw, net, st
+
+
+def test_fig2_golden_tables(ctx):
+    rp, ci = gu.demo()
+    raw, net, st = ctx.transform_host(rp, ci)
+    np.testing.assert_array_equal(raw, gu.DEMO_RAW)
+    np.testing.assert_array_equal(net, gu.DEMO_NET)
+    assert st["kernel_launches"] > 0
+
+
+@pytest.mark.parametrize("ids", [[0, 1], [0, 1, 2, 3, 4], [0, 1, 12], [0, 1, 4, 15]])
+def test_fig2_sub_dictionaries(ctx, ids):
+    rp, ci = gu.demo()
+    mask = _capi.dict_mask(ids)
+    raw, net, _ = ctx.transform_host(rp, ci, mask)
+    full_ids = _capi.mask_ids(mask)
+    np.testing.assert_array_equal(raw, gu.DEMO_RAW[:, full_ids])
+    # acceptance.cpp:84-93: {0,1,12} has an identity conversion
+    want = gu.DEMO_RAW if ids == [0, 1, 12] else gu.DEMO_NET
+    np.testing.assert_array_equal(net, want[:, full_ids])
+
+
+def test_config1_parity(ctx):
+    rp, ci = graphs.er(2000, 0.004, 1)
+    raw, net, st = check_same(ctx, rp, ci)
+    # SURVEY App. B column sums (reference-produced)
+    assert raw.sum(0).tolist() == [2000, 16212, 132038, 66019, 243, 1074176, 1074176, 538500,
+                                   179500, 2014, 4028, 2014, 2240, 2, 2, 0]
+    assert st["p2_row_touches"] == st["W"] - 16212
+
+
+def test_oracle_family_208(ctx):
+    """The acceptance family: 120 ER, 60 regular, 10 trees, K2-K6, C3-C8, stars."""
+    seed = 0x51AB5EED
+    cases = []
+    for i in range(120):
+        n = 5 + (i * 7) % 36
+        p = 0.1 if i % 3 == 0 else 0.2 if i % 3 == 1 else 0.4
+        cases.append(gu.er(n, p, seed + i))
+    for d in (3, 4, 5):
+        for j in range(20):
+            n = 6 + 2 * (j % 18)
+            cases.append(gu.regular(n, d, seed + 1000 + j + d))
+    for n in (2, 5, 9, 14, 20, 27, 33, 40, 15, 25):
+        cases.append(gu.tree(n, seed + 31 * n))
+    cases += [gu.complete(n) for n in range(2, 7)]
+    cases += [gu.cycle(n) for n in range(3, 9)]
+    cases += [gu.star(k) for k in range(2, 9)]
+    for rp, ci in cases:
+        check_same(ctx, rp, ci)
+
+
+def test_dense_small_graphs(ctx):
+    for n in (4, 5, 8, 12, 20, 33, 64):
+        check_same(ctx, *gu.complete(n))
+    for seed in range(6):
+        check_same(ctx, *gu.er(60, 0.5, 100 + seed))
+        check_same(ctx, *gu.er(200, 0.2, 200 + seed))
+
+
+def test_edgeless_and_empty(ctx):
+    rp = np.zeros(5, np.int32)
+    ci = np.zeros(0, np.int32)
+    raw, net, _ = ctx.transform_host(rp, ci)
+    assert (raw[:, 0] == 1).all() and (raw[:, 1:] == 0).all()
+    assert (net == raw).all()
+    raw, net, _ = ctx.transform_host(np.zeros(1, np.int32), ci)
+    assert raw.shape == (0, 16)
+    # isolated vertices mixed in
+    check_same(ctx, *gu.from_pairs([(0, 5), (5, 9), (9, 0), (9, 12)], 20))
+
+
+def test_random_subdicts_and_lenient(ctx):
+    rng = np.random.default_rng(20260811)
+    for trial in range(120):
+        n = int(rng.integers(2, 45))
+        rp, ci = gu.er(n, float(rng.choice([0.1, 0.3, 0.6])), int(rng.integers(1 << 30)))
+        mask = int(rng.integers(0, 1 << 16))
+        lenient = bool(trial % 2)
+        try:
+            oraw, onet = ob.transform(rp, ci, mask, lenient)
+            oerr = None
+        except ob.OracleError as e:
+            oerr = (e.code, e.graphlet_id, e.vertex)
+        try:
+            raw, net, _ = ctx.transform_host(rp, ci, mask, lenient)
+            gerr = None
+        except _capi.TransformFailed as e:
+            gerr = (e.code, e.graphlet_id, e.vertex)
+        assert gerr == oerr
+        if oerr is None:
+            np.testing.assert_array_equal(raw, oraw)
+            np.testing.assert_array_equal(net, onet)
+
+
+def test_incomplete_family_inconsistency(ctx):
+    """test_pipeline.cpp:55-65 / test_smoke.py:125-130."""
+    rp, ci = gu.complete(4)
+    mask = _capi.dict_mask([5, 13])
+    with pytest.raises(_capi.TransformFailed) as ei:
+        ctx.transform_host(rp, ci, mask)
+    assert ei.value.code == 4
+    raw, net, _ = ctx.transform_host(rp, ci, mask, lenient=True)
+    assert net[:, 2].tolist() == [0, 0, 0, 0]
+
+
+def test_net_from_raw_corrupted(ctx):
+    """test_conversion.cpp:63-76: raw(0,15)+1 -> InconsistencyError(vertex 0, graphlet 14)."""
+    rp, ci = gu.demo()
+    raw, _, _ = ctx.transform_host(rp, ci)
+    raw[0, 15] += 1
+    with pytest.raises(_capi.TransformFailed) as ei:
+        ctx.net_from_raw(raw, FULL)
+    assert (ei.value.code, ei.value.vertex, ei.value.graphlet_id) == (4, 0, 14)
+    net = ctx.net_from_raw(raw, FULL, lenient=True)
+    assert net[0, 14] == 0
+
+
+def test_choose3_overflow_site(ctx):
+    """choose3 (col 8) is the one checked site reachable with int32 CSR:
+    a star with 2^22 leaves overflows d(d-1)/2*(d-2). Reference order: the
+    col-8 fill raises OverflowError(graphlet 8, vertex 0)."""
+    leaves = 1 << 22
+    rp = np.zeros(leaves + 2, np.int64)
+    rp[1] = leaves
+    rp[2:] = leaves + np.arange(1, leaves + 1)
+    ci = np.concatenate([np.arange(1, leaves + 1), np.zeros(leaves, np.int64)])
+    mask = _capi.dict_mask([8])
+    with pytest.raises(_capi.TransformFailed) as ei:
+        ctx.transform_host(rp.astype(np.int32), ci.astype(np.int32), mask)
+    assert (ei.value.code, ei.value.graphlet_id, ei.value.vertex) == (3, 8, 0)
+
+
+@pytest.mark.parametrize("scale", [10, 12, 13])
+def test_rmat_parity(ctx, scale):
+    rp, ci = graphs.rmat(scale, 16, seed=scale)
+    check_same(ctx, rp, ci, d15_mode=1)
+
+
+def test_sbm_rgg_parity(ctx):
+    check_same(ctx, *graphs.sbm(512, 64, 0.3, 3.0, 5), d15_mode=1)
+    check_same(ctx, *graphs.rgg(50000, 3.0, 2), d15_mode=1)
+    check_same(ctx, *graphs.rgg(20000, 12.0, 9), d15_mode=1)
+
+
+def test_permutation_equivariance(ctx):
+    rng = np.random.default_rng(808)
+    for trial in range(5):
+        rp, ci = gu.er(300, 0.05, 1000 + trial)
+        pi = rng.permutation(300)
+        rp2, ci2 = gu.permute(rp, ci, pi)
+        a, _, _ = ctx.transform_host(rp, ci)
+        b, _, _ = ctx.transform_host(rp2, ci2)
+        np.testing.assert_array_equal(a, b[pi])
+
+
+def test_determinism_repeat(ctx):
+    rp, ci = graphs.rmat(14, 16, seed=7)
+    a = ctx.transform_host(rp, ci)
+    b = ctx.transform_host(rp, ci)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_one_shot_entry_point():
+    rp, ci = gu.demo()
+    raw, net, _ = _capi.transform(rp, ci)
+    np.testing.assert_array_equal(raw, gu.DEMO_RAW)
+    np.testing.assert_array_equal(net, gu.DEMO_NET)
