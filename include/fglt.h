@@ -57,6 +57,8 @@ typedef struct fglt_error {
   int32_t graphlet_id; /* -1 when not applicable */
   int64_t vertex;      /* -1 when not applicable (original vertex id) */
   char msg[256];
+  uint64_t order_key;  /* reference failure order (stage, vertex); lowest
+                          wins when ranks combine their errors; ~0 = none */
 } fglt_error;
 
 #define FGLT_MAX_STEPS 12
@@ -136,6 +138,9 @@ int fglt_stage_roots(fglt_ctx* ctx, int64_t u0, int64_t u1,
 int fglt_stage_epilogue(fglt_ctx* ctx, int64_t v0, int64_t v1,
                         uint64_t* d_raw_rows, uint64_t* d_net_rows,
                         fglt_error* err);
+
+/* Number of kernels this context has launched so far (CUB calls count 1). */
+uint64_t fglt_ctx_kernel_launches(const fglt_ctx* ctx);
 
 /* Library facts */
 const char* fglt_version(void);

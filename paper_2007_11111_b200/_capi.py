@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfglt.so")
+LIB_PATH = os.environ.get("FGLT_LIB_OVERRIDE") or os.path.join(_HERE, "libfglt.so")
 
 FGLT_INPUT_DEVICE = 0x1
 FGLT_OUTPUT_DEVICE = 0x2
@@ -24,13 +24,14 @@ EXPORTS = [
     "fglt_ctx_create", "fglt_ctx_destroy", "fglt_ctx_transform", "fglt_transform_csr32",
     "fglt_net_from_raw", "fglt_stage_prepare", "fglt_stage_bounds", "fglt_stage_triangles",
     "fglt_stage_local", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
-    "fglt_device_count",
+    "fglt_device_count", "fglt_ctx_kernel_launches",
 ]
 
 
 class FgltError(ctypes.Structure):
     _fields_ = [("code", ctypes.c_int32), ("graphlet_id", ctypes.c_int32),
-                ("vertex", ctypes.c_int64), ("msg", ctypes.c_char * 256)]
+                ("vertex", ctypes.c_int64), ("msg", ctypes.c_char * 256),
+                ("order_key", ctypes.c_uint64)]
 
 
 MAX_STEPS = 12
@@ -102,6 +103,8 @@ def lib():
         L.fglt_stage_epilogue.restype = ctypes.c_int
         L.fglt_stage_epilogue.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, vp, vp,
                                           ctypes.POINTER(FgltError)]
+        L.fglt_ctx_kernel_launches.restype = ctypes.c_uint64
+        L.fglt_ctx_kernel_launches.argtypes = [vp]
         L.fglt_version.restype = ctypes.c_char_p
         L.fglt_version.argtypes = []
         L.fglt_device_count.restype = ctypes.c_int
@@ -144,6 +147,9 @@ class Context:
         self._h = self._L.fglt_ctx_create(device, ctypes.c_void_p(stream), ctypes.byref(err))
         if not self._h:
             _raise(err.code, err)
+
+    def kernel_launches(self) -> int:
+        return int(self._L.fglt_ctx_kernel_launches(self._h))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -441,6 +441,7 @@ void local_sweeps(fglt_ctx* c) {
 std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
                            const std::vector<u64>& thr, int** lists, int64_t* stride) {
   const int nb = (int)thr.size() + 1;
+  if (nb > 8) throw CudaFail{FGLT_E_CUDA, "internal: at most 8 root bins"};
   const int64_t span = std::max<int64_t>(u1 - u0, 1);
   int* lst = c->ensure<int>(B_LISTS, (size_t)nb * span);
   u64* d_thr = c->d_small + 8;
@@ -479,7 +480,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   u64* work = c->ensure<u64>(B_WORK, 2 * (size_t)c->n);
   u64* wc = work;
   u64* key = work + c->n;
-  int* lists[4];
+  int* lists[8];
   int64_t stride = 0;
   if (P.c4) {
     const int G = group_for((double)c->nnz / (double)c->n);
@@ -521,7 +522,8 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->rp, c->split, N, key);
     check_launch();
     c->launched();
-    std::vector<int> cnt = bin_roots(c, key, u0, u1, {(u64)kSmallS, (u64)kBlockS}, lists, &stride);
+    const std::vector<u64> thr = {(u64)kSmallS, 128, 256, 512, (u64)kBlockS};
+    std::vector<int> cnt = bin_roots(c, key, u0, u1, thr, lists, &stride);
     c->mark("roots:start");
     u64* d13 = c->V(V_D13);
     u64* d15 = c->V(V_D15);
@@ -538,33 +540,43 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       check_launch();
       c->launched();
     }
-    for (int b = 1; b <= 2; ++b) {
+    for (int b = 1; b < (int)cnt.size(); ++b) {
       if (cnt[b] == 0) continue;
-      const bool global_bm = (b == 2);
-      const int s_cap = global_bm ? (int)c->maxout : kBlockS;
-      const int nw_cap = (s_cap + 31) / 32;
-      size_t sm = (size_t)s_cap * 16;
-      if (!global_bm) sm += (size_t)s_cap * nw_cap * 4;
-      u32* gbm = nullptr;
-      long long gstride = 0;
-      int g = std::min(cnt[b], c->sms * 2);
-      if (global_bm) {
-        gstride = (long long)s_cap * nw_cap;
-        // bounded scratch: at most 4 GiB of bitmaps in flight
-        const long long fit = std::max<long long>(1, (4ll << 30) / (gstride * 4));
+      const bool global = b == (int)cnt.size() - 1;  // s > kBlockS
+      RootsLayout L;
+      L.s_cap = global ? (int)c->maxout : (int)std::min<u64>(thr[b], std::max<u64>(c->maxout, 33));
+      L.hlog = 6;
+      while ((1 << L.hlog) < 4 * L.s_cap) ++L.hlog;
+      L.hcap = 1 << L.hlog;
+      L.nwarps = 8;
+      L.stride_cap = ((L.s_cap + 31) / 32) | 1;
+      size_t sm = L.bytes_core();
+      unsigned char* slab = nullptr;
+      long long slab_stride = 0;
+      int g = std::min(cnt[b], c->sms * 8);
+      if (global) {
+        slab_stride = (long long)((L.bytes_aux() + 255) & ~(size_t)255);
+        const long long fit = std::max<long long>(1, (4ll << 30) / slab_stride);
         g = (int)std::min<long long>({(long long)cnt[b], (long long)c->sms, fit});
-        gbm = c->ensure<u32>(B_GBM, (size_t)g * (size_t)gstride);
-      }
-      if (P.d13 && P.d15) {
-        set_smem(k_roots_block<true, true>, sm);
-        k_roots_block<true, true><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], s_cap, gbm, gstride, d13, d15);
-      } else if (P.d13) {
-        set_smem(k_roots_block<true, false>, sm);
-        k_roots_block<true, false><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], s_cap, gbm, gstride, d13, d15);
+        slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
       } else {
-        set_smem(k_roots_block<false, true>, sm);
-        k_roots_block<false, true><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], s_cap, gbm, gstride, d13, d15);
+        sm += L.bytes_aux();
       }
+#define LAUNCH_ROOTS(D13, D15, GL)                                                          \
+  do {                                                                                      \
+    set_smem(k_roots_block<D13, D15, GL>, sm);                                              \
+    k_roots_block<D13, D15, GL><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f,  \
+                                                           lists[b], cnt[b], L, slab,       \
+                                                           slab_stride, d13, d15);          \
+  } while (0)
+      if (P.d13 && P.d15) {
+        if (global) LAUNCH_ROOTS(true, true, true); else LAUNCH_ROOTS(true, true, false);
+      } else if (P.d13) {
+        if (global) LAUNCH_ROOTS(true, false, true); else LAUNCH_ROOTS(true, false, false);
+      } else {
+        if (global) LAUNCH_ROOTS(false, true, true); else LAUNCH_ROOTS(false, true, false);
+      }
+#undef LAUNCH_ROOTS
       check_launch();
       c->launched();
     }
@@ -599,6 +611,7 @@ int read_error(fglt_ctx* c, fglt_error* err, bool sync = true) {
   u64 key = ~0ull;
   CK(cudaMemcpyAsync(&key, c->d_small, 8, cudaMemcpyDeviceToHost, c->stream));
   if (sync) CK(cudaStreamSynchronize(c->stream));
+  if (err) err->order_key = key;
   if (key == ~0ull) return FGLT_OK;
   const int g = (int)(key & 15);
   const int code = (int)((key >> 4) & 15) ? FGLT_E_INCONSISTENCY : FGLT_E_OVERFLOW;
@@ -609,10 +622,7 @@ int read_error(fglt_ctx* c, fglt_error* err, bool sync = true) {
             g, (long long)v);
   else
     set_err(err, code, g, v, "count overflow (graphlet %d, vertex %lld)", g, (long long)v);
-  if (err) {
-    // expose the ordering key for multi-rank reductions
-    static_assert(sizeof(err->msg) >= 64, "msg too small");
-  }
+  if (err) err->order_key = key;
   return code;
 }
 
@@ -710,6 +720,8 @@ int validate_shape(int64_t n, int64_t nnz, fglt_error* err) {
 
 // =================================================================== C-ABI
 extern "C" {
+
+uint64_t fglt_ctx_kernel_launches(const fglt_ctx* c) { return c ? c->launches : 0; }
 
 const char* fglt_version(void) { return "fglt-b200 0.1 (sm_100a)"; }
 

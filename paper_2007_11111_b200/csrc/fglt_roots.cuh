@@ -5,6 +5,20 @@
 
 #include "fglt_device.cuh"
 
+#ifdef FGLT_DEBUG_BOUNDS
+#include <cstdio>
+#define FGLT_BOUNDS(cond, tag, a, b)                                                   \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("FGLT bounds %s: %lld %lld (block %d thread %d)\n", tag, (long long)(a),   \
+             (long long)(b), blockIdx.x, threadIdx.x);                                 \
+      return;                                                                          \
+    }                                                                                  \
+  } while (0)
+#else
+#define FGLT_BOUNDS(cond, tag, a, b) do { } while (0)
+#endif
+
 namespace fglt {
 
 // =============================================================== 4-cycles
@@ -333,52 +347,115 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
   }
 }
 
-// Block per root, any |S|. Bitmap rows of nw = ceil(s/32) words, in shared
-// memory when `gbm` is null, else in the block's slice of global scratch.
-template <bool kD13, bool kD15>
-__global__ void k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
-                              const int* __restrict__ split, const u32* __restrict__ C3f,
-                              const int* __restrict__ roots, int nroots, int s_cap,
-                              u32* __restrict__ gbm, long long gbm_stride,
-                              u64* __restrict__ d13, u64* __restrict__ d15) {
-  extern __shared__ unsigned char smem_raw[];
+// Block per root, |S| > 32. Shared-memory layout (host computes the same
+// sizes, roots_smem_bytes): sD u64[s_cap] | sS int[s_cap] | sC u32[s_cap] |
+// hash keys int[hcap] | hash idx u16[hcap] | per-warp pair lists u16[nw x s_cap]
+// | bitmap u32[s_cap x stride_cap]. With kGlobal the bitmap, hash and lists
+// live in the block's slice of a global slab instead (rare, very large S).
+// Bitmap rows use an odd word stride so lanes reading different rows at the
+// same word index spread over banks.
+struct RootsLayout {
+  int s_cap, hcap, hlog, nwarps, stride_cap;
+  __host__ __device__ size_t bytes_core() const {  // always in smem
+    return (size_t)s_cap * (8 + 4 + 4);
+  }
+  __host__ __device__ size_t bytes_aux() const {  // smem or slab
+    size_t h = (size_t)hcap * 4 + (((size_t)hcap * 2 + 15) & ~(size_t)15);
+    size_t l = (((size_t)nwarps * s_cap * 2) + 15) & ~(size_t)15;
+    return h + l + (size_t)s_cap * stride_cap * 4;
+  }
+};
+
+__device__ __forceinline__ int s_hash_find(const int* keys, const unsigned short* idx, int hlog,
+                                           int y) {
+  const u32 mask = (1u << hlog) - 1;
+  u32 h = ((u32)y * 0x9E3779B1u) >> (32 - hlog);
+  while (true) {
+    const int k = keys[h];
+    if (k == y) return idx[h];
+    if (k < 0) return -1;
+    h = (h + 1) & mask;
+  }
+}
+
+template <bool kD13, bool kD15, bool kGlobal>
+__global__ void __launch_bounds__(256)
+k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
+              const int* __restrict__ split, const u32* __restrict__ C3f,
+              const int* __restrict__ roots, int nroots, RootsLayout L,
+              unsigned char* __restrict__ slab, long long slab_stride,
+              u64* __restrict__ d13, u64* __restrict__ d15) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  __shared__ int next_item[2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u64* sD = reinterpret_cast<u64*>(smem_raw);
-  int* sS = reinterpret_cast<int*>(sD + s_cap);
-  u32* sC = reinterpret_cast<u32*>(sS + s_cap);
-  u32* bm = gbm ? gbm + (long long)blockIdx.x * gbm_stride : sC + s_cap;
+  int* sS = reinterpret_cast<int*>(sD + L.s_cap);
+  u32* sC = reinterpret_cast<u32*>(sS + L.s_cap);
+  unsigned char* aux = kGlobal ? slab + (long long)blockIdx.x * slab_stride
+                               : reinterpret_cast<unsigned char*>(sC + L.s_cap);
+  int* hkeys = reinterpret_cast<int*>(aux);
+  unsigned short* hidx = reinterpret_cast<unsigned short*>(hkeys + L.hcap);
+  unsigned short* lists = reinterpret_cast<unsigned short*>(
+      aux + (size_t)L.hcap * 4 + ((((size_t)L.hcap * 2) + 15) & ~(size_t)15));
+  u32* bm = reinterpret_cast<u32*>(
+      reinterpret_cast<unsigned char*>(lists) +
+      ((((size_t)L.nwarps * L.s_cap * 2) + 15) & ~(size_t)15));
+  unsigned short* mylist = lists + (size_t)wid * L.s_cap;
+
   for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
     const int u = roots[k];
     const int s0 = split[u];
     const int s = rp[u + 1] - s0;
     const int nw = (s + 31) >> 5;
+    const int stride = nw | 1;
+    int hlog = 6;
+    while ((1 << hlog) < 4 * s) ++hlog;
+    const int hcap = 1 << hlog;
+    FGLT_BOUNDS(s <= L.s_cap && s > 32, "s", s, L.s_cap);
+    FGLT_BOUNDS(hlog <= L.hlog, "hlog", hlog, L.hlog);
+    FGLT_BOUNDS(stride <= L.stride_cap, "stride", stride, L.stride_cap);
     for (int a = threadIdx.x; a < s; a += blockDim.x) {
       sS[a] = ci[s0 + a];
       if (kD13) { sC[a] = C3f[s0 + a]; sD[a] = 0; }
     }
+    for (int i = threadIdx.x; i < hcap; i += blockDim.x) hkeys[i] = -1;
     if (kD15)
-      for (long long i = threadIdx.x; i < (long long)s * nw; i += blockDim.x) bm[i] = 0;
+      for (long long i = threadIdx.x; i < (long long)s * stride; i += blockDim.x) bm[i] = 0;
+    if (threadIdx.x == 0) { next_item[0] = 0; next_item[1] = 0; }
+    __syncthreads();
+    for (int a = threadIdx.x; a < s; a += blockDim.x) {
+      const int y = sS[a];
+      u32 h = ((u32)y * 0x9E3779B1u) >> (32 - hlog);
+      while (atomicCAS(hkeys + h, -1, y) != -1) h = (h + 1) & (hcap - 1);
+      hidx[h] = (unsigned short)a;
+    }
     __syncthreads();
     const int smax = sS[s - 1];
     u64 tu = 0;
-    for (int a = wid; a + 1 < s; a += nwarps) {
+    // ---- probe: every triangle {u, S[a], S[b]} with a < b, once
+    while (true) {
+      int a = 0;
+      if (lane == 0) a = atomicAdd(next_item, 1);
+      a = __shfl_sync(0xffffffffu, a, 0);
+      if (a + 1 >= s) break;
       const int x = sS[a];
       const u32 ca = kD13 ? sC[a] : 0u;
       const int e = rp[x + 1];
       u64 da = 0;
       for (int base = split[x]; base < e; base += 32) {
         const int p = base + lane;
-        const int y = p < e ? ci[p] : 0x7fffffff;
+        const int y = p < e ? __ldg(ci + p) : 0x7fffffff;
         if (y <= smax) {
-          const int bi = lower_bound_smem(sS, a + 1, s, y);
-          if (bi < s && sS[bi] == y) {
+          const int bi = s_hash_find(hkeys, hidx, hlog, y);
+          FGLT_BOUNDS(bi < s && (bi < 0 || bi > a), "bi", bi, a);
+          if (bi >= 0) {
             if (kD15) {
-              atomicOr(bm + (long long)a * nw + (bi >> 5), 1u << (bi & 31));
-              atomicOr(bm + (long long)bi * nw + (a >> 5), 1u << (a & 31));
+              atomicOr(bm + (long long)a * stride + (bi >> 5), 1u << (bi & 31));
+              atomicOr(bm + (long long)bi * stride + (a >> 5), 1u << (a & 31));
             }
             if (kD13) {
-              tu += (u64)C3f[p] - 1;
+              tu += (u64)__ldg(C3f + p) - 1;
               da += (u64)sC[bi] - 1;
               atomicAdd(sD + bi, (u64)ca - 1);
             }
@@ -391,36 +468,68 @@ __global__ void k_roots_block(const int* __restrict__ rp, const int* __restrict_
         if (lane == 0 && da) atomicAdd(sD + a, da);
       }
     }
+    __syncthreads();
     if (kD13) {
-      tu = block_sum_u64(tu, red);  // contains __syncthreads
-      if (threadIdx.x == 0 && tu) atomicAdd(d13 + u, tu);
       for (int a = threadIdx.x; a < s; a += blockDim.x)
         if (sD[a]) atomicAdd(d13 + sS[a], sD[a]);
-    } else {
-      __syncthreads();
+      tu = block_sum_u64(tu, red);
+      if (threadIdx.x == 0 && tu) atomicAdd(d13 + u, tu);
     }
     if (kD15) {
+      // t_a = sum_{b in row a} popc(row_a & row_b) = 2 x (#G[S]-triangles at a)
       u64 tot = 0;
-      for (int a = wid; a < s; a += nwarps) {
-        const u32* ra = bm + (long long)a * nw;
+      while (true) {
+        int a = 0;
+        if (lane == 0) a = atomicAdd(next_item + 1, 1);
+        a = __shfl_sync(0xffffffffu, a, 0);
+        if (a >= s) break;
+        const u32* ra = bm + (long long)a * stride;
         u64 acc = 0;
-        if (nw <= 32) {
-          const u32 mine = lane < nw ? ra[lane] : 0u;
-          for (int w = 0; w < nw; ++w) {
-            u32 bits = ra[w];
-            while (bits) {
-              const int bb = (w << 5) + __ffs(bits) - 1;
-              bits &= bits - 1;
-              if (lane < nw) acc += __popc(mine & bm[(long long)bb * nw + lane]);
+        // row degree decides the lane mapping
+        int deg = 0;
+        for (int j = lane; j < nw; j += 32) deg += __popc(ra[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
+        if (deg == 0) continue;
+        if (deg >= 24 && deg <= L.s_cap) {
+          // lanes over pairs: extract the neighbour list of a, then each lane
+          // ANDs whole rows
+          int written = 0;
+          for (int j0 = 0; j0 < nw; j0 += 32) {
+            const int j = j0 + lane;
+            u32 w = j < nw ? ra[j] : 0u;
+            const int c = __popc(w);
+            int incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int t = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += t;
             }
+            int off = written + incl - c;
+            while (w) {
+              mylist[off++] = (unsigned short)((j << 5) + __ffs(w) - 1);
+              w &= w - 1;
+            }
+            written += __shfl_sync(0xffffffffu, incl, 31);
           }
+          __syncwarp();
+          FGLT_BOUNDS(written == deg, "written", written, deg);
+          for (int i = lane; i < deg; i += 32) {
+            FGLT_BOUNDS(mylist[i] < s, "list", mylist[i], s);
+            const u32* rb = bm + (long long)mylist[i] * stride;
+            u32 c = 0;
+            for (int j = 0; j < nw; ++j) c += __popc(ra[j] & rb[j]);
+            acc += c;
+          }
+          __syncwarp();
         } else {
-          for (int w = 0; w < nw; ++w) {
-            u32 bits = ra[w];
+          // lanes over words
+          for (int w0 = 0; w0 < nw; ++w0) {
+            u32 bits = ra[w0];
             while (bits) {
-              const int bb = (w << 5) + __ffs(bits) - 1;
+              const int bb = (w0 << 5) + __ffs(bits) - 1;
               bits &= bits - 1;
-              const u32* rb = bm + (long long)bb * nw;
+              const u32* rb = bm + (long long)bb * stride;
               for (int j = lane; j < nw; j += 32) acc += __popc(ra[j] & rb[j]);
             }
           }

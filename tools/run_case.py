@@ -1,0 +1,24 @@
+"""Run one transform on a generated graph and check it against the oracle
+(dev tool for bisecting failures): python tools/run_case.py rmat 17 [check]"""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+from paper_2007_11111_b200 import _capi, graphs  # noqa: E402
+
+kind, arg = sys.argv[1], int(sys.argv[2])
+check = len(sys.argv) > 3
+if kind == "rmat":
+    rp, ci = graphs.rmat(arg, 16, seed=1)
+elif kind == "sbm":
+    rp, ci = graphs.sbm(arg, 64, 0.3, 3.0, 5)
+else:
+    rp, ci = graphs.config(arg)[1:]
+ctx = _capi.Context(0)
+raw, net, st = ctx.transform_host(rp, ci)
+print(kind, arg, "ok", st["kernel_launches"], flush=True)
+if check:
+    from oracle import binding as ob
+    oraw, onet = ob.transform(rp, ci, 0xFFFF, False, 1)
+    print("parity", np.array_equal(raw, oraw), np.array_equal(net, onet))
