@@ -142,6 +142,14 @@ int fglt_stage_epilogue(fglt_ctx* ctx, int64_t v0, int64_t v1,
 /* Number of kernels this context has launched so far (CUB calls count 1). */
 uint64_t fglt_ctx_kernel_launches(const fglt_ctx* ctx);
 
+/* Test hooks: force one internal code path for every root so small graphs
+ * exercise paths that otherwise only large graphs reach. Results must be
+ * identical for any setting (the parity tests check exactly that). */
+#define FGLT_DEBUG_C4_CLASS 1  /* 0 auto, 2 hash passes, 3 packed tiles, 4 tiles */
+#define FGLT_DEBUG_C4_PARTS 2  /* hash passes per root when class 2 is forced  */
+#define FGLT_DEBUG_ROOTS_BIN 3 /* 0 auto, 1..4 smem bitmap bins, 5 global slab */
+int fglt_ctx_set_debug(fglt_ctx* ctx, int key, int value);
+
 /* Library facts */
 const char* fglt_version(void);
 int fglt_device_count(void);

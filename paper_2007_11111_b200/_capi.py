@@ -24,8 +24,10 @@ EXPORTS = [
     "fglt_ctx_create", "fglt_ctx_destroy", "fglt_ctx_transform", "fglt_transform_csr32",
     "fglt_net_from_raw", "fglt_stage_prepare", "fglt_stage_bounds", "fglt_stage_triangles",
     "fglt_stage_local", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
-    "fglt_device_count", "fglt_ctx_kernel_launches",
+    "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug",
 ]
+
+DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN = 1, 2, 3
 
 
 class FgltError(ctypes.Structure):
@@ -103,6 +105,8 @@ def lib():
         L.fglt_stage_epilogue.restype = ctypes.c_int
         L.fglt_stage_epilogue.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, vp, vp,
                                           ctypes.POINTER(FgltError)]
+        L.fglt_ctx_set_debug.restype = ctypes.c_int
+        L.fglt_ctx_set_debug.argtypes = [vp, ctypes.c_int, ctypes.c_int]
         L.fglt_ctx_kernel_launches.restype = ctypes.c_uint64
         L.fglt_ctx_kernel_launches.argtypes = [vp]
         L.fglt_version.restype = ctypes.c_char_p
@@ -147,6 +151,11 @@ class Context:
         self._h = self._L.fglt_ctx_create(device, ctypes.c_void_p(stream), ctypes.byref(err))
         if not self._h:
             _raise(err.code, err)
+
+    def set_debug(self, key: int, value: int):
+        rc = self._L.fglt_ctx_set_debug(self._h, key, value)
+        if rc:
+            raise ValueError(f"bad debug key {key}")
 
     def kernel_launches(self) -> int:
         return int(self._L.fglt_ctx_kernel_launches(self._h))

@@ -56,10 +56,6 @@ const unsigned char kU16[16][16] = {
 constexpr int kSmallS = 32;       // roots with |N+(u)| <= 32: warp kernel
 constexpr int kBlockS = 1024;     // <= 1024: block kernel, bitmap in smem
 constexpr int kWarpHashLog = 9;   // 512-slot table per warp
-constexpr int kWarpHashMax = 256; // wedges per root for the warp table
-constexpr int kBlockHashLog = 14; // 16384-slot table per block (128 KB)
-constexpr int kBlockHashMax = 8192;
-constexpr int kTile = 49152;      // dense tile counters (192 KB)
 
 enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
@@ -201,6 +197,9 @@ struct fglt_ctx {
   u64* d_small = nullptr;  // [0] err key, [1] W, [2] d_max, [3..] bin counts
   bool have_stats = false;
   uint64_t W = 0, dmax = 0, maxout = 0;
+
+  // test hooks (fglt_ctx_set_debug): force one code path for every root
+  int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1;
 
   // timing
   bool timing = false;
@@ -466,10 +465,14 @@ std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
 }
 
 __global__ void k_outdeg_key(const int* __restrict__ rp, const int* __restrict__ split, int n,
-                             u64* __restrict__ key) {
+                             u64* __restrict__ key, u64 force_key) {
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
     const int s = rp[u + 1] - split[u];
-    key[u] = s >= 2 ? (u64)s : 0ull;
+    u64 k = s >= 2 ? (u64)s : 0ull;
+    // test hook: push roots into a larger bin (a bin's kernel handles any s
+    // below its cap, so forcing upward is always valid)
+    if (k && force_key && force_key > k) k = force_key;
+    key[u] = k;
   }
 }
 
@@ -477,16 +480,21 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   const Plan& P = c->plan;
   if (c->n == 0 || !(P.c4 || P.d13 || P.d15)) return;
   const int N = (int)c->n;
-  u64* work = c->ensure<u64>(B_WORK, 2 * (size_t)c->n);
+  u64* work = c->ensure<u64>(B_WORK, 4 * (size_t)c->n);
   u64* wc = work;
   u64* key = work + c->n;
+  u64* cls = work + 2 * c->n;
+  u64* parts = work + 3 * c->n;
   int* lists[8];
   int64_t stride = 0;
   if (P.c4) {
     const int G = group_for((double)c->nnz / (double)c->n);
     DISPATCH_G(G, launch_root_work, c, wc, key);
-    std::vector<int> cnt = bin_roots(c, wc, u0, u1, {(u64)kWarpHashMax, (u64)kBlockHashMax},
-                                     lists, &stride);
+    k_c4_class<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(
+        c->rp, c->split, wc, (int)u0, (int)u1, cls, parts, c->force_c4_class, c->force_c4_parts);
+    check_launch();
+    c->launched();
+    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3}, lists, &stride);
     c->mark("four-cycle rows:start");
     u64* c4 = c->V(V_C4);
     if (cnt[0] > 0) {
@@ -498,28 +506,36 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       c->launched();
     }
     if (cnt[1] > 0) {
-      const size_t sm = (size_t)(1 << kBlockHashLog) * 8;
-      set_smem(k_c4_block, sm);
-      k_c4_block<<<std::min(cnt[1], c->sms * 2), 512, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->mir, lists[1], cnt[1], kBlockHashLog, c4);
+      const size_t sm = (size_t)(1 << kC4HashLog) * 8;
+      set_smem(k_c4_hashp<8>, sm);
+      k_c4_hashp<8><<<std::min(cnt[1], c->sms), 512, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->mir, lists[1], cnt[1], parts, c4);
       check_launch();
       c->launched();
     }
-    if (cnt[2] > 0) {
-      const size_t sm = (size_t)kTile * 4;
-      set_smem(k_c4_tiles, sm);
-      const int g = std::min(cnt[2], c->sms);
-      // cursor slice per block: the longest prefix |N-(u)| <= d_max
+    for (int bb = 2; bb <= 3; ++bb) {
+      if (cnt[bb] == 0) continue;
+      const size_t sm = 196608;
+      const int g = std::min(cnt[bb], c->sms);
       int* cur = c->ensure<int>(B_CURSOR, (size_t)g * (size_t)(c->dmax + 1));
-      k_c4_tiles<<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[2], cnt[2],
-                                             kTile, cur, (long long)(c->dmax + 1), c4);
+      if (bb == 2) {
+        set_smem(k_c4_dense<true>, sm);
+        k_c4_dense<true><<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[bb],
+                                                     cnt[bb], cur, (long long)(c->dmax + 1), c4);
+      } else {
+        set_smem(k_c4_dense<false>, sm);
+        k_c4_dense<false><<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[bb],
+                                                      cnt[bb], cur, (long long)(c->dmax + 1), c4);
+      }
       check_launch();
       c->launched();
     }
     c->mark("four-cycle rows:end");
   }
   if (P.d13 || P.d15) {
-    k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->rp, c->split, N, key);
+    static const u64 kForceKey[] = {0, 33, 129, 257, 513, 1025};
+    const u64 fk = (c->force_roots_bin > 0 && c->force_roots_bin < 6) ? kForceKey[c->force_roots_bin] : 0;
+    k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->rp, c->split, N, key, fk);
     check_launch();
     c->launched();
     const std::vector<u64> thr = {(u64)kSmallS, 128, 256, 512, (u64)kBlockS};
@@ -722,6 +738,16 @@ int validate_shape(int64_t n, int64_t nnz, fglt_error* err) {
 extern "C" {
 
 uint64_t fglt_ctx_kernel_launches(const fglt_ctx* c) { return c ? c->launches : 0; }
+
+int fglt_ctx_set_debug(fglt_ctx* c, int key, int value) {
+  if (!c) return FGLT_E_NO_DEVICE;
+  switch (key) {
+    case FGLT_DEBUG_C4_CLASS: c->force_c4_class = value; return FGLT_OK;
+    case FGLT_DEBUG_C4_PARTS: c->force_c4_parts = value; return FGLT_OK;
+    case FGLT_DEBUG_ROOTS_BIN: c->force_roots_bin = value; return FGLT_OK;
+    default: return FGLT_E_PARSE;
+  }
+}
 
 const char* fglt_version(void) { return "fglt-b200 0.1 (sm_100a)"; }
 

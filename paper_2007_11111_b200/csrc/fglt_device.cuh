@@ -61,6 +61,20 @@ __device__ __forceinline__ u64 group_sum_u64(u64 v) {
 
 __device__ __forceinline__ u64 sat_sub(u64 a, u64 b) { return a > b ? a - b : 0ull; }
 
+// Exact 64-bit accumulation in shared memory from native 32-bit atomics: the
+// low word wraps, its carry goes to the high word. Little-endian [lo, hi], so
+// the pair reads back as one u64 after a barrier. (A 64-bit shared atomicAdd
+// compiles to a CAS spin loop, ATOMS.CAST.SPIN.64, which lost updates under
+// contention in our kernels — see DESIGN.md.)
+__device__ __forceinline__ void smem_add_u64(u64* addr, u64 v) {
+  u32* w = reinterpret_cast<u32*>(addr);
+  const u32 vl = (u32)v;
+  const u32 vh = (u32)(v >> 32);
+  const u32 old = atomicAdd(w, vl);
+  const u32 carry = (u32)(old + vl < old);
+  if (vh + carry) atomicAdd(w + 1, vh + carry);
+}
+
 // ------------------------------------------------------------ preprocessing
 
 // key = degree << 32 | id : sorting these gives the relabelling order.

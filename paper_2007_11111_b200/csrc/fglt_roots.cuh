@@ -146,44 +146,114 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
   return t;  // valid in thread 0
 }
 
-// Block per root; one 2^logcap table per block (dynamic shared memory).
-__global__ void k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
-                           const int* __restrict__ split, const int* __restrict__ mir,
-                           const int* __restrict__ roots, int nroots, int logcap,
-                           u64* __restrict__ c4) {
-  extern __shared__ unsigned char smem_raw[];
+// Cost-model classes for roots with wc(u) > 0 (k_c4_class):
+//   1 warp table     wc <= 256
+//   2 block table, P hash-partition passes over the wedges, P = ceil(wc/12288)
+//   3 dense tiles, 16-bit packed counters (|N-(u)| < 65536), 96K ids per tile
+//   4 dense tiles, 32-bit counters, 48K ids per tile
+// Class 2 vs 3/4 is chosen per root by the cheaper of the two modelled costs.
+constexpr int kC4HashLog = 14;              // 16384 slots (keys + counts = 128 KB)
+constexpr u64 kC4HashFill = 12288;          // distinct targets per pass (LF 0.75)
+constexpr int kC4Tile16 = 98304;            // ids per packed tile (192 KB)
+constexpr int kC4Tile32 = 49152;            // ids per 32-bit tile (192 KB)
+constexpr int kC4Long = 48;                 // rows at least this long: warp-cooperative
+
+__global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
+                           const u64* __restrict__ wc, int u0, int u1, u64* __restrict__ cls,
+                           u64* __restrict__ parts, int force_cls, int force_parts) {
+  for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1;
+       u += gridDim.x * blockDim.x) {
+    const u64 w = wc[u];
+    u64 c = 0, P = 1;
+    if (w == 0) {
+      c = 0;
+    } else if (w <= 256) {
+      c = 1;
+    } else {
+      const u64 nq = (u64)(split[u] - rp[u]);
+      P = (w + kC4HashFill - 1) / kC4HashFill;
+      const u64 cost_hash = P * (w + 16384) + w;
+      const bool pack = nq < 65536;
+      const u64 tile = pack ? kC4Tile16 : kC4Tile32;
+      const u64 tiles = ((u64)u + tile - 1) / tile;
+      const u64 cost_dense = tiles * (2 * 49152 / 4 + nq) + 2 * w;
+      if (cost_hash <= cost_dense) c = 2;
+      else c = pack ? 3 : 4;
+    }
+    if (force_cls > 0 && w > 0) {  // test hook: route every root to one path
+      const u64 nq = (u64)(split[u] - rp[u]);
+      c = (u64)force_cls;
+      if (c == 1 && w > 256) c = 2;
+      if (c == 3 && nq >= 65536) c = 4;
+      if (c == 2) P = force_parts > 0 ? (u64)force_parts : P;
+    }
+    cls[u] = c;
+    parts[u] = P;
+  }
+}
+
+// Block per root, P hash-partition passes: pass `part` inserts only targets w
+// with part_of(w) == part, so every pass fits the table. G lanes per row.
+__device__ __forceinline__ u32 part_of(int w, u32 P) {
+  return (u32)(((u64)(((u32)w * 0x85EBCA6Bu) ^ ((u32)w >> 13)) * P) >> 32);
+}
+
+template <int G>
+__global__ void __launch_bounds__(512)
+k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
+           const int* __restrict__ split, const int* __restrict__ mir,
+           const int* __restrict__ roots, int nroots, const u64* __restrict__ parts,
+           u64* __restrict__ c4) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
-  const int cap = 1 << logcap;
+  constexpr int cap = 1 << kC4HashLog;
   int* keys = reinterpret_cast<int*>(smem_raw);
   u32* vals = reinterpret_cast<u32*>(keys + cap);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int gl = threadIdx.x & (G - 1);
+  const int gid = threadIdx.x / G, ngroups = blockDim.x / G;
   for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
     const int u = roots[k];
-    for (int i = threadIdx.x; i < cap; i += blockDim.x) { keys[i] = -1; vals[i] = 0; }
-    __syncthreads();
+    const u32 P = (u32)parts[u];
     const int b = rp[u], s = split[u];
-    for (int q = b + wid; q < s; q += nwarps) {
-      const int v = ci[q];
-      const int end = mir[q];
-      for (int p = rp[v] + lane; p < end; p += 32) hash_insert(keys, vals, logcap, ci[p]);
-    }
-    __syncthreads();
     u64 acc = 0;
-    for (int i = threadIdx.x; i < cap; i += blockDim.x) {
-      const u32 l = vals[i];
-      if (l >= 2) {
-        const u64 c = (u64)l * (l - 1) / 2;
-        acc += c;
-        atomicAdd(c4 + keys[i], c);
+    for (u32 part = 0; part < P; ++part) {
+      for (int i = threadIdx.x; i < cap; i += blockDim.x) { keys[i] = -1; vals[i] = 0; }
+      __syncthreads();
+      for (int q = b + gid; q < s; q += ngroups) {
+        const int v = ci[q];
+        const int end = mir[q];
+        for (int p = rp[v] + gl; p < end; p += G) {
+          const int w = __ldg(ci + p);
+          if (P == 1 || part_of(w, P) == part) hash_insert(keys, vals, kC4HashLog, w);
+        }
       }
-    }
-    for (int q = b + wid; q < s; q += nwarps) {
-      const int v = ci[q];
-      const int end = mir[q];
-      u64 sv = 0;
-      for (int p = rp[v] + lane; p < end; p += 32) sv += hash_get(keys, vals, logcap, ci[p]) - 1;
-      sv = warp_sum_u64(sv);
-      if (lane == 0 && sv) atomicAdd(c4 + v, sv);
+      __syncthreads();
+      for (int i = threadIdx.x; i < cap; i += blockDim.x) {
+        const u32 l = vals[i];
+        if (l >= 2) {
+          const u64 c = (u64)l * (l - 1) / 2;
+          acc += c;
+          atomicAdd(c4 + keys[i], c);
+        }
+      }
+      // warp-uniform trip count: the group reduction shuffles the full warp
+      const int rounds = (s - b + ngroups - 1) / ngroups;
+      for (int it = 0; it < rounds; ++it) {
+        const int q = b + gid + it * ngroups;
+        u64 sv = 0;
+        int v = -1;
+        if (q < s) {
+          v = ci[q];
+          const int end = mir[q];
+          for (int p = rp[v] + gl; p < end; p += G) {
+            const int w = __ldg(ci + p);
+            if (P == 1 || part_of(w, P) == part) sv += hash_get(keys, vals, kC4HashLog, w) - 1;
+          }
+        }
+        sv = group_sum_u64<G>(sv);
+        if (gl == 0 && sv) atomicAdd(c4 + v, sv);
+      }
+      __syncthreads();
     }
     acc = block_sum_u64(acc, red);
     if (threadIdx.x == 0 && acc) atomicAdd(c4 + u, acc);
@@ -191,57 +261,138 @@ __global__ void k_c4_block(const int* __restrict__ rp, const int* __restrict__ c
   }
 }
 
-// Block per heavy root; the w range [0,u) is swept in tiles of `tile`
-// counters held in shared memory. cur[] (global scratch, one slice per
-// block) keeps each row's read position across tiles, so every wedge is read
-// exactly twice (count pass, attribution pass) and no row is searched.
-__global__ void k_c4_tiles(const int* __restrict__ rp, const int* __restrict__ ci,
-                           const int* __restrict__ split, const int* __restrict__ mir,
-                           const int* __restrict__ roots, int nroots, int tile,
-                           int* __restrict__ cursor, long long cursor_stride,
-                           u64* __restrict__ c4) {
-  extern __shared__ unsigned char smem_raw[];
+// Block per heavy root; the w range [0,u) is swept in dense shared-memory
+// tiles (PACK: two 16-bit counters per word, valid since L[w] <= |N-(u)| <
+// 65536). Each row keeps a cursor across tiles, so every wedge is read exactly
+// twice (count, attribution). Rows are split at the first one of length >=
+// kC4Long (rows of N-(u) are in ascending degree): short rows thread-per-row,
+// long rows warp-cooperative.
+template <bool PACK>
+__global__ void __launch_bounds__(1024)
+k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
+           const int* __restrict__ split, const int* __restrict__ mir,
+           const int* __restrict__ roots, int nroots, int* __restrict__ cursor,
+           long long cursor_stride, u64* __restrict__ c4) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
+  __shared__ int next_long;
+  constexpr int TILE = PACK ? kC4Tile16 : kC4Tile32;
   u32* L = reinterpret_cast<u32*>(smem_raw);
   int* cur = cursor + (long long)blockIdx.x * cursor_stride;
+  const int lane = threadIdx.x & 31;
+  auto inc = [&](int off) {
+    if (PACK) atomicAdd(L + (off >> 1), 1u << ((off & 1) << 4));
+    else atomicAdd(L + off, 1u);
+  };
+  auto get = [&](int off) -> u32 {
+    if (PACK) return (L[off >> 1] >> ((off & 1) << 4)) & 0xffffu;
+    return L[off];
+  };
   for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
     const int u = roots[k];
     const int b = rp[u], nq = split[u] - b;
+    // first long row (rows in N-(u) have nondecreasing degree)
+    int lo_q = 0, hi_q = nq;
+    while (lo_q < hi_q) {
+      const int mid = (lo_q + hi_q) >> 1;
+      const int v = ci[b + mid];
+      if (rp[v + 1] - rp[v] < kC4Long) lo_q = mid + 1; else hi_q = mid;
+    }
+    const int qs = lo_q;
     for (int q = threadIdx.x; q < nq; q += blockDim.x) cur[q] = rp[ci[b + q]];
     u64 acc = 0;
-    for (int lo = 0; lo < u; lo += tile) {
-      const int hi = min(lo + tile, u);
-      const int span = hi - lo;
-      for (int i = threadIdx.x; i < span; i += blockDim.x) L[i] = 0;
+    for (int lo = 0; lo < u; lo += TILE) {
+      const int hi = min(lo + TILE, u);
+      const int words = PACK ? (hi - lo + 1) >> 1 : hi - lo;
+      {
+        uint4* L4 = reinterpret_cast<uint4*>(L);
+        const int n4 = (words + 3) >> 2;
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) L4[i] = make_uint4(0, 0, 0, 0);
+      }
+      if (threadIdx.x == 0) next_long = qs;
       __syncthreads();
-      for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+      // count pass
+      for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
         for (int p = cur[q]; p < end; ++p) {
           const int w = ci[p];
           if (w >= hi) break;
-          atomicAdd(L + (w - lo), 1u);
+          inc(w - lo);
+        }
+      }
+      while (true) {
+        int q = 0;
+        if (lane == 0) q = atomicAdd(&next_long, 1);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= nq) break;
+        const int end = mir[b + q];
+        for (int p0 = cur[q]; p0 < end; p0 += 32) {
+          const int p = p0 + lane;
+          const int w = p < end ? __ldg(ci + p) : 0x7fffffff;
+          if (w < hi) inc(w - lo);
+          if (__any_sync(0xffffffffu, w >= hi)) break;
         }
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < span; i += blockDim.x) {
-        const u32 l = L[i];
-        if (l >= 2) {
-          const u64 c = (u64)l * (l - 1) / 2;
+      for (int i = threadIdx.x; i < words; i += blockDim.x) {
+        const u32 x = L[i];
+        if (PACK) {
+          const u32 l0 = x & 0xffffu, l1 = x >> 16;
+          if (l0 >= 2) {
+            const u64 c = (u64)l0 * (l0 - 1) / 2;
+            acc += c;
+            atomicAdd(c4 + lo + 2 * i, c);
+          }
+          if (l1 >= 2) {
+            const u64 c = (u64)l1 * (l1 - 1) / 2;
+            acc += c;
+            atomicAdd(c4 + lo + 2 * i + 1, c);
+          }
+        } else if (x >= 2) {
+          const u64 c = (u64)x * (x - 1) / 2;
           acc += c;
           atomicAdd(c4 + lo + i, c);
         }
       }
-      for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+      if (threadIdx.x == 0) next_long = qs;
+      __syncthreads();
+      // attribution pass: c4[v] += sum (L[w] - 1), cursors advance
+      for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
         int p = cur[q];
         u64 sv = 0;
         for (; p < end; ++p) {
           const int w = ci[p];
           if (w >= hi) break;
-          sv += L[w - lo] - 1;
+          sv += get(w - lo) - 1;
         }
         cur[q] = p;
         if (sv) atomicAdd(c4 + ci[b + q], sv);
+      }
+      while (true) {
+        int q = 0;
+        if (lane == 0) q = atomicAdd(&next_long, 1);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= nq) break;
+        const int end = mir[b + q];
+        int p0 = cur[q];
+        u64 sv = 0;
+        for (; p0 < end; p0 += 32) {
+          const int p = p0 + lane;
+          const int w = p < end ? __ldg(ci + p) : 0x7fffffff;
+          const bool in = w < hi;
+          if (in) sv += get(w - lo) - 1;
+          const unsigned ball = __ballot_sync(0xffffffffu, in);
+          if (ball != 0xffffffffu) {
+            p0 += __popc(ball);
+            break;
+          }
+        }
+        sv = warp_sum_u64(sv);
+        if (lane == 0) {
+          cur[q] = min(p0, end);
+          if (sv) atomicAdd(c4 + ci[b + q], sv);
+        }
       }
       __syncthreads();
     }
@@ -309,7 +460,7 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
             if (kD13) {
               tu += (u64)C3f[p] - 1;
               da += (u64)sC[bi] - 1;
-              atomicAdd(sD + bi, (u64)ca - 1);
+              smem_add_u64(sD + bi, (u64)ca - 1);
             }
           }
         }
@@ -317,7 +468,7 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
       }
       if (kD13) {
         da = warp_sum_u64(da);
-        if (lane == 0 && da) atomicAdd(sD + a, da);
+        if (lane == 0 && da) smem_add_u64(sD + a, da);
       }
     }
     __syncwarp();
@@ -412,7 +563,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     int hlog = 6;
     while ((1 << hlog) < 4 * s) ++hlog;
     const int hcap = 1 << hlog;
-    FGLT_BOUNDS(s <= L.s_cap && s > 32, "s", s, L.s_cap);
+    FGLT_BOUNDS(s <= L.s_cap, "s", s, L.s_cap);
     FGLT_BOUNDS(hlog <= L.hlog, "hlog", hlog, L.hlog);
     FGLT_BOUNDS(stride <= L.stride_cap, "stride", stride, L.stride_cap);
     for (int a = threadIdx.x; a < s; a += blockDim.x) {
@@ -457,7 +608,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
             if (kD13) {
               tu += (u64)__ldg(C3f + p) - 1;
               da += (u64)sC[bi] - 1;
-              atomicAdd(sD + bi, (u64)ca - 1);
+              smem_add_u64(sD + bi, (u64)ca - 1);
             }
           }
         }
@@ -465,7 +616,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
       }
       if (kD13) {
         da = warp_sum_u64(da);
-        if (lane == 0 && da) atomicAdd(sD + a, da);
+        if (lane == 0 && da) smem_add_u64(sD + a, da);
       }
     }
     __syncthreads();

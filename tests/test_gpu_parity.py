@@ -205,3 +205,44 @@ def test_one_shot_entry_point():
     raw, net, _ = _capi.transform(rp, ci)
     np.testing.assert_array_equal(raw, gu.DEMO_RAW)
     np.testing.assert_array_equal(net, gu.DEMO_NET)
+
+
+FORCED = [
+    ("c4 hash P=1", _capi.DEBUG_C4_CLASS, 2, 1),
+    ("c4 hash P=3", _capi.DEBUG_C4_CLASS, 2, 3),
+    ("c4 packed tiles", _capi.DEBUG_C4_CLASS, 3, 0),
+    ("c4 32-bit tiles", _capi.DEBUG_C4_CLASS, 4, 0),
+    ("roots bin 1", _capi.DEBUG_ROOTS_BIN, 1, 0),
+    ("roots bin 2", _capi.DEBUG_ROOTS_BIN, 2, 0),
+    ("roots bin 4", _capi.DEBUG_ROOTS_BIN, 4, 0),
+    ("roots global slab", _capi.DEBUG_ROOTS_BIN, 5, 0),
+]
+
+
+@pytest.mark.parametrize("label,key,value,parts", FORCED, ids=[f[0] for f in FORCED])
+def test_forced_code_paths(label, key, value, parts):
+    """Every internal path (normally reached only at scale) must give the
+    same bits: force it for all roots on small graphs."""
+    c = _capi.Context(0)
+    c.set_debug(key, value)
+    if parts:
+        c.set_debug(_capi.DEBUG_C4_PARTS, parts)
+    cases = [gu.er(200, 0.2, 7), gu.complete(40), graphs.rmat(12, 16, seed=5),
+             graphs.sbm(64, 64, 0.3, 3.0, 9), gu.star(70), gu.demo()]
+    for rp, ci in cases:
+        check_same(c, rp, ci, d15_mode=1)
+    c.close()
+
+
+def test_repeat_determinism_at_scale():
+    """Bit-identical results across repeated runs at a size where every
+    root bin and 4-cycle class is populated (guards against lost updates;
+    a 64-bit shared atomicAdd once dropped d13 contributions here)."""
+    rp, ci = graphs.rmat(19, 16, seed=3)
+    c = _capi.Context(0)
+    base = c.transform_host(rp, ci)
+    for _ in range(6):
+        raw, net, _ = c.transform_host(rp, ci)
+        np.testing.assert_array_equal(raw, base[0])
+        np.testing.assert_array_equal(net, base[1])
+    c.close()
