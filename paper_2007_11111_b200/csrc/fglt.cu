@@ -288,6 +288,16 @@ void launch_root_work(fglt_ctx* c, u64* wc, u64* tw) {
   c->launched();
 }
 
+template <int G>
+void launch_c4_hashp(fglt_ctx* c, int g, int block, size_t sm, const int* roots, int nroots,
+                     const u64* wc, const u64* parts, int max_log, u64* c4) {
+  set_smem(k_c4_hashp<G>, sm);
+  k_c4_hashp<G><<<g, block, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, roots, nroots, wc,
+                                             parts, max_log, c4);
+  check_launch();
+  c->launched();
+}
+
 #define DISPATCH_G(G, FN, ...)               \
   switch (G) {                               \
     case 4: FN<4>(__VA_ARGS__); break;       \
@@ -418,7 +428,7 @@ void triangles(fglt_ctx* c, int64_t e0, int64_t e1) {
   if (!c->plan.c3 || c->n == 0) return;
   CK(cudaMemsetAsync(c->C3f, 0, (size_t)std::max<int64_t>(c->nnz, 1) * 4, c->stream));
   if (e1 > e0) {
-    k_triangles<<<c->grid((e1 - e0) * 32, 256), 256, 0, c->stream>>>(
+    k_triangles<<<c->grid(e1 - e0, 256), 256, 0, c->stream>>>(
         c->rp, c->ci, c->split, c->ce_row, c->ce_pos, (int)e0, (int)e1, c->C3f);
     check_launch();
     c->launched();
@@ -494,7 +504,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         c->rp, c->split, wc, (int)u0, (int)u1, cls, parts, c->force_c4_class, c->force_c4_parts);
     check_launch();
     c->launched();
-    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3}, lists, &stride);
+    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4}, lists, &stride);
     c->mark("four-cycle rows:start");
     u64* c4 = c->V(V_C4);
     if (cnt[0] > 0) {
@@ -505,20 +515,22 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       check_launch();
       c->launched();
     }
-    if (cnt[1] > 0) {
-      const size_t sm = (size_t)(1 << kC4HashLog) * 8;
-      set_smem(k_c4_hashp<8>, sm);
-      k_c4_hashp<8><<<std::min(cnt[1], c->sms), 512, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->mir, lists[1], cnt[1], parts, c4);
-      check_launch();
-      c->launched();
+    if (cnt[1] > 0) {  // small tables: 128-thread blocks, several per SM
+      const size_t sm = (size_t)(1 << kC4SmallLog) * 8;
+      const int g = std::min(cnt[1], c->sms * 6);
+      DISPATCH_G(G, launch_c4_hashp, c, g, 128, sm, lists[1], cnt[1], wc, parts, kC4SmallLog, c4);
     }
-    for (int bb = 2; bb <= 3; ++bb) {
+    if (cnt[2] > 0) {
+      const size_t sm = (size_t)(1 << kC4HashLog) * 8;
+      const int g = std::min(cnt[2], c->sms);
+      DISPATCH_G(G, launch_c4_hashp, c, g, 512, sm, lists[2], cnt[2], wc, parts, kC4HashLog, c4);
+    }
+    for (int bb = 3; bb <= 4; ++bb) {
       if (cnt[bb] == 0) continue;
       const size_t sm = 196608;
       const int g = std::min(cnt[bb], c->sms);
-      int* cur = c->ensure<int>(B_CURSOR, (size_t)g * (size_t)(c->dmax + 1));
-      if (bb == 2) {
+      int* cur = c->ensure<int>(B_CURSOR, 2 * (size_t)g * (size_t)(c->dmax + 1));
+      if (bb == 3) {
         set_smem(k_c4_dense<true>, sm);
         k_c4_dense<true><<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[bb],
                                                      cnt[bb], cur, (long long)(c->dmax + 1), c4);

@@ -75,6 +75,51 @@ __device__ __forceinline__ void smem_add_u64(u64* addr, u64 v) {
   if (vh + carry) atomicAdd(w + 1, vh + carry);
 }
 
+// ------------------------------------------------- warp segment flattening
+// A warp holds one segment per lane (start, len). flat_prefix computes the
+// exclusive offsets and the total; flat_row maps a flattened element index k
+// to the lane (row) owning it with a 5-step shuffle search over the offsets
+// (the largest r with off[r] <= k; empty rows are skipped automatically).
+// Consumers then stream the batch's elements with all 32 lanes busy and
+// independent loads (no data-dependent loop exits).
+__device__ __forceinline__ int flat_prefix(int len, int* total) {
+  const int lane = threadIdx.x & 31;
+  int incl = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  *total = __shfl_sync(0xffffffffu, incl, 31);
+  return incl - len;
+}
+
+__device__ __forceinline__ int flat_row(int off, int k) {
+  int r = 0;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    const int o = __shfl_sync(0xffffffffu, off, r + s);
+    if (o <= k) r += s;
+  }
+  return r;
+}
+
+// Segmented sum across the warp of values whose rows are nondecreasing in the
+// lane index: returns, in the LAST lane of each run of equal `row`, the run's
+// total and sets *tail there.
+__device__ __forceinline__ u64 seg_sum_runs(int row, u64 v, bool* tail) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 t = __shfl_up_sync(0xffffffffu, v, o);
+    const int tr = __shfl_up_sync(0xffffffffu, row, o);
+    if (lane >= o && tr == row) v += t;
+  }
+  const int nr = __shfl_down_sync(0xffffffffu, row, 1);
+  *tail = (lane == 31) || (nr != row);
+  return v;
+}
+
 // ------------------------------------------------------------ preprocessing
 
 // key = degree << 32 | id : sorting these gives the relabelling order.
@@ -184,37 +229,70 @@ __global__ void k_sweep_a(const int* __restrict__ rp, const int* __restrict__ ci
 // triangle u < x < y is found exactly once, as y in N+(x) ∩ (N+(u) after x).
 // Per triangle: C3(x,y) += 1 and C3(u,y) += 1 by global atomics; C3(u,x) gets
 // the warp's hit count once. Values live at canonical positions of C3f.
-__global__ void k_triangles(const int* __restrict__ rp, const int* __restrict__ ci,
-                            const int* __restrict__ split, const int* __restrict__ ce_row,
-                            const int* __restrict__ ce_pos, int e0, int e1,
-                            u32* __restrict__ C3f) {
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int e = e0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); e < e1; e += warps) {
-    const int u = ce_row[e];
-    const int pux = ce_pos[e];
-    const int send = rp[u + 1];
-    if (pux + 1 >= send) continue;  // x is the last out-neighbour of u
-    const int x = ci[pux];
-    const int smax = ci[send - 1];
-    const int b = split[x], eend = rp[x + 1];
-    u32 hits = 0;
-    for (int base = b; base < eend; base += 32) {
-      const int p = base + lane;
-      const int y = p < eend ? ci[p] : 0x7fffffff;
-      if (y <= smax) {
-        const int q = lower_bound_i32(ci, pux + 1, send, y);
-        if (q < send && ci[q] == y) {
-          atomicAdd(C3f + p, 1u);
-          atomicAdd(C3f + q, 1u);
-          ++hits;
-        }
+__global__ void __launch_bounds__(256)
+k_triangles(const int* __restrict__ rp, const int* __restrict__ ci,
+            const int* __restrict__ split, const int* __restrict__ ce_row,
+            const int* __restrict__ ce_pos, int e0, int e1, u32* __restrict__ C3f) {
+  // Warp batches of 32 canonical edges (u, x); their probe lists N+(x), cut at
+  // max N+(u), are flattened in interleaved (coalesced) order and each lane
+  // tracks its current edge through per-warp shared tables.
+  __shared__ int t_base[8][32], t_off[8][33], t_lo[8][32], t_hi[8][32];
+  __shared__ u32 t_hits[8][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int* bst = t_base[wid];
+  int* boff = t_off[wid];
+  int* blo = t_lo[wid];
+  int* bhi = t_hi[wid];
+  u32* hits = t_hits[wid];
+  hits[lane] = 0;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
+  for (long long eb = e0 + gw * 32; eb < e1; eb += nwarps * 32) {
+    const long long e = eb + lane;
+    const bool valid = e < e1;
+    int pux = 0, send = 0, st = 0, se = 0;
+    if (valid) {
+      const int u = ce_row[e];
+      pux = ce_pos[e];
+      send = rp[u + 1];
+      if (pux + 1 < send) {
+        const int x = ci[pux];
+        const int smax = ci[send - 1];
+        st = split[x];
+        se = lower_bound_i32(ci, st, rp[x + 1], smax + 1);
       }
-      if (__any_sync(0xffffffffu, y >= smax) ) break;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
-    if (lane == 0 && hits) atomicAdd(C3f + pux, hits);
+    int T;
+    const int off = flat_prefix(se - st, &T);
+    bst[lane] = st - off;
+    boff[lane] = off;
+    blo[lane] = pux + 1;
+    bhi[lane] = send;
+    if (lane == 0) boff[32] = T;
+    __syncwarp();
+    int r = 0;
+    u32 h = 0;
+    for (int kk = lane; kk < T; kk += 32) {
+      if (boff[r + 1] <= kk) {
+        if (h) atomicAdd(hits + r, h);
+        h = 0;
+        do { ++r; } while (boff[r + 1] <= kk);
+      }
+      const int p = bst[r] + kk;
+      const int y = __ldg(ci + p);
+      const int hi = bhi[r];
+      const int q = lower_bound_i32(ci, blo[r], hi, y);
+      if (q < hi && __ldg(ci + q) == y) {
+        atomicAdd(C3f + p, 1u);
+        atomicAdd(C3f + q, 1u);
+        ++h;
+      }
+    }
+    if (h) atomicAdd(hits + r, h);
+    __syncwarp();
+    if (valid && hits[lane]) atomicAdd(C3f + pux, hits[lane]);
+    hits[lane] = 0;
+    __syncwarp();
   }
 }
 

@@ -148,15 +148,17 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 
 // Cost-model classes for roots with wc(u) > 0 (k_c4_class):
 //   1 warp table     wc <= 256
-//   2 block table, P hash-partition passes over the wedges, P = ceil(wc/12288)
-//   3 dense tiles, 16-bit packed counters (|N-(u)| < 65536), 96K ids per tile
-//   4 dense tiles, 32-bit counters, 48K ids per tile
-// Class 2 vs 3/4 is chosen per root by the cheaper of the two modelled costs.
+//   2 small block table (128 threads, <= 4096 slots), wc <= 2048
+//   3 block table, P hash-partition passes over the wedges, P = ceil(wc/12288)
+//   4 dense tiles, 16-bit packed counters (|N-(u)| < 65536), 96K ids per tile
+//   5 dense tiles, 32-bit counters, 48K ids per tile
+// Class 3 vs 4/5 is chosen per root by the cheaper of the two modelled costs.
 constexpr int kC4HashLog = 14;              // 16384 slots (keys + counts = 128 KB)
+constexpr int kC4SmallLog = 12;             // 4096 slots (32 KB)
 constexpr u64 kC4HashFill = 12288;          // distinct targets per pass (LF 0.75)
 constexpr int kC4Tile16 = 98304;            // ids per packed tile (192 KB)
 constexpr int kC4Tile32 = 49152;            // ids per 32-bit tile (192 KB)
-constexpr int kC4Long = 48;                 // rows at least this long: warp-cooperative
+constexpr int kC4Long = 48;                 // rows at least this long: flattened batches
 
 __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
                            const u64* __restrict__ wc, int u0, int u1, u64* __restrict__ cls,
@@ -169,6 +171,8 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       c = 0;
     } else if (w <= 256) {
       c = 1;
+    } else if (w <= 2048) {
+      c = 2;
     } else {
       const u64 nq = (u64)(split[u] - rp[u]);
       P = (w + kC4HashFill - 1) / kC4HashFill;
@@ -177,15 +181,18 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       const u64 tile = pack ? kC4Tile16 : kC4Tile32;
       const u64 tiles = ((u64)u + tile - 1) / tile;
       const u64 cost_dense = tiles * (2 * 49152 / 4 + nq) + 2 * w;
-      if (cost_hash <= cost_dense) c = 2;
-      else c = pack ? 3 : 4;
+      if (cost_hash <= cost_dense) c = 3;
+      else c = pack ? 4 : 5;
     }
     if (force_cls > 0 && w > 0) {  // test hook: route every root to one path
       const u64 nq = (u64)(split[u] - rp[u]);
-      c = (u64)force_cls;
-      if (c == 1 && w > 256) c = 2;
-      if (c == 3 && nq >= 65536) c = 4;
-      if (c == 2) P = force_parts > 0 ? (u64)force_parts : P;
+      // external numbering: 2 hash passes, 3 packed tiles, 4 32-bit tiles
+      c = (u64)force_cls + 1;
+      if (c == 4 && nq >= 65536) c = 5;
+      if (c == 3) {
+        P = (w + kC4HashFill - 1) / kC4HashFill;
+        if (force_parts > 0) P = (u64)force_parts;
+      }
     }
     cls[u] = c;
     parts[u] = P;
@@ -198,23 +205,32 @@ __device__ __forceinline__ u32 part_of(int w, u32 P) {
   return (u32)(((u64)(((u32)w * 0x85EBCA6Bu) ^ ((u32)w >> 13)) * P) >> 32);
 }
 
+// Block per root with a shared hash table of 2^hlog slots sized to the
+// root (hlog <= max_log); P hash-partition passes when the distinct targets
+// could exceed the table. G lanes per row; trip counts are warp-uniform
+// because the group reductions shuffle the full warp.
 template <int G>
-__global__ void __launch_bounds__(512)
+__global__ void
 k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
-           const int* __restrict__ roots, int nroots, const u64* __restrict__ parts,
-           u64* __restrict__ c4) {
+           const int* __restrict__ roots, int nroots, const u64* __restrict__ wcv,
+           const u64* __restrict__ parts, int max_log, u64* __restrict__ c4) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
-  constexpr int cap = 1 << kC4HashLog;
+  const int maxcap = 1 << max_log;
   int* keys = reinterpret_cast<int*>(smem_raw);
-  u32* vals = reinterpret_cast<u32*>(keys + cap);
+  u32* vals = reinterpret_cast<u32*>(keys + maxcap);
   const int gl = threadIdx.x & (G - 1);
   const int gid = threadIdx.x / G, ngroups = blockDim.x / G;
   for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
     const int u = roots[k];
     const u32 P = (u32)parts[u];
+    const u64 per_pass = (wcv[u] + P - 1) / P;
+    int hlog = 6;
+    while (hlog < max_log && ((u64)1 << hlog) < 2 * per_pass) ++hlog;
+    const int cap = 1 << hlog;
     const int b = rp[u], s = split[u];
+    const int rounds = (s - b + ngroups - 1) / ngroups;
     u64 acc = 0;
     for (u32 part = 0; part < P; ++part) {
       for (int i = threadIdx.x; i < cap; i += blockDim.x) { keys[i] = -1; vals[i] = 0; }
@@ -224,7 +240,7 @@ k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
         const int end = mir[q];
         for (int p = rp[v] + gl; p < end; p += G) {
           const int w = __ldg(ci + p);
-          if (P == 1 || part_of(w, P) == part) hash_insert(keys, vals, kC4HashLog, w);
+          if (P == 1 || part_of(w, P) == part) hash_insert(keys, vals, hlog, w);
         }
       }
       __syncthreads();
@@ -236,8 +252,6 @@ k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
           atomicAdd(c4 + keys[i], c);
         }
       }
-      // warp-uniform trip count: the group reduction shuffles the full warp
-      const int rounds = (s - b + ngroups - 1) / ngroups;
       for (int it = 0; it < rounds; ++it) {
         const int q = b + gid + it * ngroups;
         u64 sv = 0;
@@ -247,7 +261,7 @@ k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
           const int end = mir[q];
           for (int p = rp[v] + gl; p < end; p += G) {
             const int w = __ldg(ci + p);
-            if (P == 1 || part_of(w, P) == part) sv += hash_get(keys, vals, kC4HashLog, w) - 1;
+            if (P == 1 || part_of(w, P) == part) sv += hash_get(keys, vals, hlog, w) - 1;
           }
         }
         sv = group_sum_u64<G>(sv);
@@ -267,6 +281,49 @@ k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
 // twice (count, attribution). Rows are split at the first one of length >=
 // kC4Long (rows of N-(u) are in ascending degree): short rows thread-per-row,
 // long rows warp-cooperative.
+// Block-wide flattening of one segment per thread: writes exclusive offsets
+// (g_off[0..nthreads], g_off[nthreads] = total) and per-row element bases
+// g_st[r] = start - off; returns the total. Contains __syncthreads.
+__device__ __forceinline__ int block_flatten(int len, int start, int* g_off, int* g_st,
+                                             int* wtot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wtot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int x = lane < nw ? wtot[lane] : 0;
+    int xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += t;
+    }
+    if (lane < nw) wtot[lane] = xi - x;  // exclusive warp base
+    if (lane == 31) g_off[blockDim.x] = xi;
+  }
+  __syncthreads();
+  const int off = wtot[wid] + incl - len;
+  g_off[threadIdx.x] = off;
+  g_st[threadIdx.x] = start - off;
+  __syncthreads();
+  return g_off[blockDim.x];
+}
+
+// Row of flattened element k: the largest r with g_off[r] <= k.
+__device__ __forceinline__ int upper_row(const int* g_off, int k, int n) {
+  int lo = 0, hi = n;  // invariant: g_off[lo] <= k (k >= 0 = g_off[0])
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (g_off[mid] <= k) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 template <bool PACK>
 __global__ void __launch_bounds__(1024)
 k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
@@ -275,11 +332,22 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
            long long cursor_stride, u64* __restrict__ c4) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
-  __shared__ int next_long;
+  __shared__ u64 rsum[32][32];
+  __shared__ int bst_all[32][32];
+  __shared__ int boff_all[32][33];
+  __shared__ int next_batch[2];
+  __shared__ int g_off[1025];
+  __shared__ int g_st[1024];
+  __shared__ u64 g_sum[1024];
+  __shared__ int wtot[32];
   constexpr int TILE = PACK ? kC4Tile16 : kC4Tile32;
   u32* L = reinterpret_cast<u32*>(smem_raw);
-  int* cur = cursor + (long long)blockIdx.x * cursor_stride;
-  const int lane = threadIdx.x & 31;
+  int* cur = cursor + (long long)blockIdx.x * 2 * cursor_stride;
+  int* segend = cur + cursor_stride;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u64* rs = rsum[wid];
+  int* bst = bst_all[wid];
+  int* boff = boff_all[wid];
   auto inc = [&](int off) {
     if (PACK) atomicAdd(L + (off >> 1), 1u << ((off & 1) << 4));
     else atomicAdd(L + off, 1u);
@@ -288,6 +356,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     if (PACK) return (L[off >> 1] >> ((off & 1) << 4)) & 0xffffu;
     return L[off];
   };
+  rs[lane] = 0;
   for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
     const int u = roots[k];
     const int b = rp[u], nq = split[u] - b;
@@ -299,6 +368,17 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
       if (rp[v + 1] - rp[v] < kC4Long) lo_q = mid + 1; else hi_q = mid;
     }
     const int qs = lo_q;
+    // giant rows: expected >= 64 elements per tile -> block-wide flattening
+    const int ntiles = (u + TILE - 1) / TILE;
+    const int giant_deg = max(kC4Long, 64 * ntiles);
+    hi_q = nq;
+    while (lo_q < hi_q) {
+      const int mid = (lo_q + hi_q) >> 1;
+      const int v = ci[b + mid];
+      if (rp[v + 1] - rp[v] < giant_deg) lo_q = mid + 1; else hi_q = mid;
+    }
+    const int qg = lo_q;
+    const int nb = (qg - qs + 31) >> 5;  // batches of 32 long rows
     for (int q = threadIdx.x; q < nq; q += blockDim.x) cur[q] = rp[ci[b + q]];
     u64 acc = 0;
     for (int lo = 0; lo < u; lo += TILE) {
@@ -309,9 +389,31 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         const int n4 = (words + 3) >> 2;
         for (int i = threadIdx.x; i < n4; i += blockDim.x) L4[i] = make_uint4(0, 0, 0, 0);
       }
-      if (threadIdx.x == 0) next_long = qs;
+      if (threadIdx.x == 0) { next_batch[0] = 0; next_batch[1] = 0; }
       __syncthreads();
-      // count pass
+      // ---- count pass: giant rows block-wide, then short and long rows
+      for (int g0 = qg; g0 < nq; g0 += blockDim.x) {
+        const int q = g0 + threadIdx.x;
+        const bool valid = q < nq;
+        int st = 0, se = 0;
+        if (valid) {
+          st = cur[q];
+          const int em = mir[b + q];
+          se = hi >= u ? em : lower_bound_i32(ci, st, em, hi);
+          segend[q] = se;
+        }
+        const int T = block_flatten(se - st, st, g_off, g_st, wtot);
+        // each warp streams a contiguous slice of the flattened elements
+        const int nwarp = blockDim.x >> 5;
+        const int per = (((T + nwarp - 1) / nwarp) + 31) & ~31;
+        const int k0 = wid * per, k1 = min(T, k0 + per);
+        int r = k0 + lane < k1 ? upper_row(g_off, k0 + lane, blockDim.x) : 0;
+        for (int kk = k0 + lane; kk < k1; kk += 32) {
+          while (g_off[r + 1] <= kk) ++r;
+          inc(__ldg(ci + g_st[r] + kk) - lo);
+        }
+        __syncthreads();
+      }
       for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
         for (int p = cur[q]; p < end; ++p) {
@@ -321,17 +423,32 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         }
       }
       while (true) {
-        int q = 0;
-        if (lane == 0) q = atomicAdd(&next_long, 1);
-        q = __shfl_sync(0xffffffffu, q, 0);
-        if (q >= nq) break;
-        const int end = mir[b + q];
-        for (int p0 = cur[q]; p0 < end; p0 += 32) {
-          const int p = p0 + lane;
-          const int w = p < end ? __ldg(ci + p) : 0x7fffffff;
-          if (w < hi) inc(w - lo);
-          if (__any_sync(0xffffffffu, w >= hi)) break;
+        int bt = 0;
+        if (lane == 0) bt = atomicAdd(next_batch, 1);
+        bt = __shfl_sync(0xffffffffu, bt, 0);
+        if (bt >= nb) break;
+        bt = nb - 1 - bt;  // largest rows first
+        const int q = qs + (bt << 5) + lane;
+        const bool valid = q < qg;
+        int st = 0, se = 0;
+        if (valid) {
+          st = cur[q];
+          const int em = mir[b + q];
+          se = hi >= u ? em : lower_bound_i32(ci, st, em, hi);
+          segend[q] = se;
         }
+        int T;
+        const int off = flat_prefix(se - st, &T);
+        bst[lane] = st - off;  // element k of row r lives at bst[r] + k
+        boff[lane] = off;
+        if (lane == 0) boff[32] = T;
+        __syncwarp();
+        int r = 0;
+        for (int kk = lane; kk < T; kk += 32) {
+          while (boff[r + 1] <= kk) ++r;
+          inc(__ldg(ci + bst[r] + kk) - lo);
+        }
+        __syncwarp();
       }
       __syncthreads();
       for (int i = threadIdx.x; i < words; i += blockDim.x) {
@@ -354,9 +471,36 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
           atomicAdd(c4 + lo + i, c);
         }
       }
-      if (threadIdx.x == 0) next_long = qs;
+      // ---- attribution pass: c4[v] += sum (L[w] - 1); cursors advance
       __syncthreads();
-      // attribution pass: c4[v] += sum (L[w] - 1), cursors advance
+      for (int g0 = qg; g0 < nq; g0 += blockDim.x) {
+        const int q = g0 + threadIdx.x;
+        const bool valid = q < nq;
+        const int st = valid ? cur[q] : 0;
+        const int se = valid ? segend[q] : 0;
+        g_sum[threadIdx.x] = 0;
+        const int T = block_flatten(se - st, st, g_off, g_st, wtot);
+        const int nwarp = blockDim.x >> 5;
+        const int per = (((T + nwarp - 1) / nwarp) + 31) & ~31;
+        const int k0 = wid * per, k1 = min(T, k0 + per);
+        int r = k0 + lane < k1 ? upper_row(g_off, k0 + lane, blockDim.x) : 0;
+        u64 part = 0;
+        for (int kk = k0 + lane; kk < k1; kk += 32) {
+          if (g_off[r + 1] <= kk) {
+            if (part) smem_add_u64(g_sum + r, part);
+            part = 0;
+            do { ++r; } while (g_off[r + 1] <= kk);
+          }
+          part += get(__ldg(ci + g_st[r] + kk) - lo) - 1;
+        }
+        if (part) smem_add_u64(g_sum + r, part);
+        __syncthreads();
+        if (valid) {
+          if (g_sum[threadIdx.x]) atomicAdd(c4 + ci[b + q], g_sum[threadIdx.x]);
+          cur[q] = se;
+        }
+        __syncthreads();
+      }
       for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
         int p = cur[q];
@@ -370,29 +514,39 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         if (sv) atomicAdd(c4 + ci[b + q], sv);
       }
       while (true) {
-        int q = 0;
-        if (lane == 0) q = atomicAdd(&next_long, 1);
-        q = __shfl_sync(0xffffffffu, q, 0);
-        if (q >= nq) break;
-        const int end = mir[b + q];
-        int p0 = cur[q];
-        u64 sv = 0;
-        for (; p0 < end; p0 += 32) {
-          const int p = p0 + lane;
-          const int w = p < end ? __ldg(ci + p) : 0x7fffffff;
-          const bool in = w < hi;
-          if (in) sv += get(w - lo) - 1;
-          const unsigned ball = __ballot_sync(0xffffffffu, in);
-          if (ball != 0xffffffffu) {
-            p0 += __popc(ball);
-            break;
+        int bt = 0;
+        if (lane == 0) bt = atomicAdd(next_batch + 1, 1);
+        bt = __shfl_sync(0xffffffffu, bt, 0);
+        if (bt >= nb) break;
+        bt = nb - 1 - bt;  // largest rows first
+        const int q = qs + (bt << 5) + lane;
+        const bool valid = q < qg;
+        const int st = valid ? cur[q] : 0;
+        const int se = valid ? segend[q] : 0;
+        int T;
+        const int off = flat_prefix(se - st, &T);
+        bst[lane] = st - off;
+        boff[lane] = off;
+        if (lane == 0) boff[32] = T;
+        __syncwarp();
+        int r = 0;
+        u64 part = 0;
+        for (int kk = lane; kk < T; kk += 32) {
+          if (boff[r + 1] <= kk) {
+            if (part) smem_add_u64(rs + r, part);
+            part = 0;
+            do { ++r; } while (boff[r + 1] <= kk);
           }
+          part += get(__ldg(ci + bst[r] + kk) - lo) - 1;
         }
-        sv = warp_sum_u64(sv);
-        if (lane == 0) {
-          cur[q] = min(p0, end);
-          if (sv) atomicAdd(c4 + ci[b + q], sv);
+        if (part) smem_add_u64(rs + r, part);
+        __syncwarp();
+        if (valid) {
+          if (rs[lane]) atomicAdd(c4 + ci[b + q], rs[lane]);
+          cur[q] = se;
         }
+        rs[lane] = 0;
+        __syncwarp();
       }
       __syncthreads();
     }
