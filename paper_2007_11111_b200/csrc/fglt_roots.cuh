@@ -408,9 +408,20 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         const int per = (((T + nwarp - 1) / nwarp) + 31) & ~31;
         const int k0 = wid * per, k1 = min(T, k0 + per);
         int r = k0 + lane < k1 ? upper_row(g_off, k0 + lane, blockDim.x) : 0;
-        for (int kk = k0 + lane; kk < k1; kk += 32) {
-          while (g_off[r + 1] <= kk) ++r;
-          inc(__ldg(ci + g_st[r] + kk) - lo);
+        for (int kk = k0 + lane; kk < k1; kk += 128) {  // 4 independent loads in flight
+          int w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int kj = kk + 32 * j;
+            w[j] = -1;
+            if (kj < k1) {
+              while (g_off[r + 1] <= kj) ++r;
+              w[j] = __ldg(ci + g_st[r] + kj);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (w[j] >= 0) inc(w[j] - lo);
         }
         __syncthreads();
       }
@@ -444,9 +455,20 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         if (lane == 0) boff[32] = T;
         __syncwarp();
         int r = 0;
-        for (int kk = lane; kk < T; kk += 32) {
-          while (boff[r + 1] <= kk) ++r;
-          inc(__ldg(ci + bst[r] + kk) - lo);
+        for (int kk = lane; kk < T; kk += 128) {  // 4 independent loads in flight
+          int w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int kj = kk + 32 * j;
+            w[j] = -1;
+            if (kj < T) {
+              while (boff[r + 1] <= kj) ++r;
+              w[j] = __ldg(ci + bst[r] + kj);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (w[j] >= 0) inc(w[j] - lo);
         }
         __syncwarp();
       }
@@ -484,16 +506,32 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         const int per = (((T + nwarp - 1) / nwarp) + 31) & ~31;
         const int k0 = wid * per, k1 = min(T, k0 + per);
         int r = k0 + lane < k1 ? upper_row(g_off, k0 + lane, blockDim.x) : 0;
+        int cr = r;  // row that `part` accumulates for
         u64 part = 0;
-        for (int kk = k0 + lane; kk < k1; kk += 32) {
-          if (g_off[r + 1] <= kk) {
-            if (part) smem_add_u64(g_sum + r, part);
-            part = 0;
-            do { ++r; } while (g_off[r + 1] <= kk);
+        for (int kk = k0 + lane; kk < k1; kk += 128) {  // 4 independent loads in flight
+          int w[4], rr[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int kj = kk + 32 * j;
+            w[j] = -1;
+            if (kj < k1) {
+              while (g_off[r + 1] <= kj) ++r;
+              rr[j] = r;
+              w[j] = __ldg(ci + g_st[r] + kj);
+            }
           }
-          part += get(__ldg(ci + g_st[r] + kk) - lo) - 1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (w[j] < 0) break;
+            if (rr[j] != cr) {
+              if (part) smem_add_u64(g_sum + cr, part);
+              part = 0;
+              cr = rr[j];
+            }
+            part += get(w[j] - lo) - 1;
+          }
         }
-        if (part) smem_add_u64(g_sum + r, part);
+        if (part) smem_add_u64(g_sum + cr, part);
         __syncthreads();
         if (valid) {
           if (g_sum[threadIdx.x]) atomicAdd(c4 + ci[b + q], g_sum[threadIdx.x]);
@@ -529,17 +567,32 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         boff[lane] = off;
         if (lane == 0) boff[32] = T;
         __syncwarp();
-        int r = 0;
+        int r = 0, cr = 0;
         u64 part = 0;
-        for (int kk = lane; kk < T; kk += 32) {
-          if (boff[r + 1] <= kk) {
-            if (part) smem_add_u64(rs + r, part);
-            part = 0;
-            do { ++r; } while (boff[r + 1] <= kk);
+        for (int kk = lane; kk < T; kk += 128) {
+          int w[4], rr[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int kj = kk + 32 * j;
+            w[j] = -1;
+            if (kj < T) {
+              while (boff[r + 1] <= kj) ++r;
+              rr[j] = r;
+              w[j] = __ldg(ci + bst[r] + kj);
+            }
           }
-          part += get(__ldg(ci + bst[r] + kk) - lo) - 1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (w[j] < 0) break;
+            if (rr[j] != cr) {
+              if (part) smem_add_u64(rs + cr, part);
+              part = 0;
+              cr = rr[j];
+            }
+            part += get(w[j] - lo) - 1;
+          }
         }
-        if (part) smem_add_u64(rs + r, part);
+        if (part) smem_add_u64(rs + cr, part);
         __syncwarp();
         if (valid) {
           if (rs[lane]) atomicAdd(c4 + ci[b + q], rs[lane]);
@@ -937,7 +990,7 @@ __global__ void k_epilogue(EpilogueIn in, const DictInfo* __restrict__ dict, int
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (i < k) rw[i] = col[D.ids[i]];
-    bool stop = false;
+    bool stop = net == nullptr;  // raw only: the conversion never runs
     for (int rr = k - 1; rr >= 0; --rr) {
       u64 absorbed = 0;
       nt[rr] = 0;

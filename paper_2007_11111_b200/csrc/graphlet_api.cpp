@@ -1,0 +1,583 @@
+// graphlet_api.cpp — the graphlet:: C++ API (include/graphlet/*.hpp) over the
+// C-ABI (include/fglt.h). Host-side only: dictionary planning, CSR ingest and
+// text parsing, conversion-matrix utilities. Every frequency is computed by
+// libfglt.so on the device; there is no CPU path for the transform.
+//
+// Reference interfaces mirrored (proj/include/graphlet/…):
+//   dictionary.hpp:29-83  Dictionary, parse_dictionary, resolve_dependencies
+//   graph.hpp:41-100      SparseAdjacency, parsers, build_adjacency
+//   conversion.hpp:14-61  ConversionMatrix, full_u16, sub_matrix, net_from_raw
+//   kernels.hpp:105-123   TransformStats, KernelOptions, raw_frequencies
+//   transform.hpp:8-23    TransformOptions, TransformResult, transform
+#include <algorithm>
+#include <array>
+#include <charconv>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+
+#include "fglt.h"
+#include "graphlet/transform.hpp"
+
+namespace graphlet {
+
+// ================================================================ dictionary
+namespace {
+
+// Σ16 descriptors: family order = vertex count, then edge count, then the
+// degree of the incidence node (Table 1).
+constexpr std::array<GraphletDescriptor, kNumGraphlets> kSigma16{{
+    {0, "singleton", 1, 0, "the vertex"},
+    {1, "1-path, at an end", 2, 1, "either end"},
+    {2, "2-path, at an end", 3, 2, "either end"},
+    {3, "bi-fork, at the root", 3, 2, "the center"},
+    {4, "3-clique, at any node", 3, 3, "any vertex"},
+    {5, "3-path, at an end", 4, 3, "either end"},
+    {6, "3-path, at an interior node", 4, 3, "either interior vertex"},
+    {7, "claw, at a leaf", 4, 3, "any leaf"},
+    {8, "claw, at the root", 4, 3, "the center"},
+    {9, "dipper, at the handle tip", 4, 4, "the pendant vertex"},
+    {10, "dipper, at a base node", 4, 4, "either triangle vertex off the handle"},
+    {11, "dipper, at the center", 4, 4, "the degree-3 vertex"},
+    {12, "4-cycle, at any node", 4, 4, "any vertex"},
+    {13, "diamond, at an off-cord node", 4, 5, "either degree-2 vertex"},
+    {14, "diamond, at an on-cord node", 4, 5, "either degree-3 vertex"},
+    {15, "4-clique, at any node", 4, 6, "any vertex"},
+}};
+
+std::string_view strip_spaces(std::string_view s) {
+  std::size_t b = s.find_first_not_of(' ');
+  if (b == std::string_view::npos) return {};
+  std::size_t e = s.find_last_not_of(' ');
+  return s.substr(b, e - b + 1);
+}
+
+int graphlet_id_of(std::string_view tok) {
+  int v = -1;
+  const char* end = tok.data() + tok.size();
+  auto res = std::from_chars(tok.data(), end, v);
+  if (res.ec != std::errc{} || res.ptr != end)
+    throw ParseError("malformed graphlet id '" + std::string(tok) + "'");
+  if (v < 0 || v >= kNumGraphlets)
+    throw ParseError("graphlet id " + std::to_string(v) + " outside 0..15");
+  return v;
+}
+
+}  // namespace
+
+std::span<const GraphletDescriptor, kNumGraphlets> graphlet_descriptors() { return kSigma16; }
+
+Dictionary Dictionary::from_ids(std::span<const int> ids) {
+  std::uint32_t m = 3u;
+  for (int id : ids) {
+    if (id < 0 || id >= kNumGraphlets)
+      throw ParseError("graphlet id " + std::to_string(id) + " outside 0..15");
+    m |= 1u << id;
+  }
+  Dictionary d;
+  for (int i = 0; i < kNumGraphlets; ++i)
+    if (m >> i & 1u) d.ids_.push_back(i);
+  return d;
+}
+
+Dictionary Dictionary::all() {
+  std::array<int, kNumGraphlets> ids{};
+  for (int i = 0; i < kNumGraphlets; ++i) ids[i] = i;
+  return from_ids(ids);
+}
+
+bool Dictionary::contains(int id) const {
+  return std::binary_search(ids_.begin(), ids_.end(), id);
+}
+
+std::size_t Dictionary::position_of(int id) const {
+  auto it = std::lower_bound(ids_.begin(), ids_.end(), id);
+  if (it == ids_.end() || *it != id)
+    throw Error("graphlet " + std::to_string(id) + " not in dictionary");
+  return static_cast<std::size_t>(it - ids_.begin());
+}
+
+std::uint32_t Dictionary::mask() const {
+  std::uint32_t m = 0;
+  for (int id : ids_) m |= 1u << id;
+  return m;
+}
+
+ParsedDictionary parse_dictionary(std::string_view spec) {
+  spec = strip_spaces(spec);
+  if (spec.empty()) throw ParseError("empty dictionary spec");
+  std::vector<int> ids;
+  if (spec == "all") {
+    for (int i = 0; i < kNumGraphlets; ++i) ids.push_back(i);
+  } else {
+    std::size_t start = 0;
+    while (true) {
+      const std::size_t comma = spec.find(',', start);
+      const std::string_view tok = strip_spaces(
+          spec.substr(start, comma == std::string_view::npos ? std::string_view::npos
+                                                             : comma - start));
+      if (tok.empty()) throw ParseError("empty token in dictionary spec");
+      const std::size_t dash = tok.find('-');
+      if (dash == std::string_view::npos) {
+        ids.push_back(graphlet_id_of(tok));
+      } else {
+        const int lo = graphlet_id_of(strip_spaces(tok.substr(0, dash)));
+        const int hi = graphlet_id_of(strip_spaces(tok.substr(dash + 1)));
+        if (lo > hi)
+          throw ParseError("descending range '" + std::string(tok) + "' in dictionary spec");
+        for (int i = lo; i <= hi; ++i) ids.push_back(i);
+      }
+      if (comma == std::string_view::npos) break;
+      start = comma + 1;
+      if (start == spec.size()) throw ParseError("trailing comma in dictionary spec");
+    }
+  }
+  ParsedDictionary out;
+  out.dict = Dictionary::from_ids(ids);
+  for (int must : {0, 1})
+    if (std::find(ids.begin(), ids.end(), must) == ids.end()) out.implicitly_added.push_back(must);
+  return out;
+}
+
+const char* aux_step_name(AuxStep s) {
+  static const char* const kNames[] = {"degrees",         "triangles",    "two-paths",
+                                       "three-paths",     "four-cycle rows",
+                                       "diamond rows",    "tetrahedra"};
+  const int i = static_cast<int>(s);
+  return i >= 0 && i < 7 ? kNames[i] : "?";
+}
+
+std::vector<AuxStep> resolve_dependencies(const Dictionary& d) {
+  const std::uint32_t m = d.mask();
+  auto any = [m](std::uint32_t bits) { return (m & bits) != 0; };
+  auto bit = [](std::initializer_list<int> ids) {
+    std::uint32_t b = 0;
+    for (int i : ids) b |= 1u << i;
+    return b;
+  };
+  std::vector<AuxStep> plan{AuxStep::kDegrees};
+  if (any(bit({4, 5, 6, 9, 10, 11, 13}))) plan.push_back(AuxStep::kTriangles);
+  if (any(bit({2, 5, 6}))) plan.push_back(AuxStep::kTwoPaths);
+  if (any(bit({5}))) plan.push_back(AuxStep::kThreePaths);
+  if (any(bit({12, 14}))) plan.push_back(AuxStep::kFourCycles);
+  if (any(bit({13}))) plan.push_back(AuxStep::kDiamonds);
+  if (any(bit({15}))) plan.push_back(AuxStep::kTetrahedra);
+  return plan;
+}
+
+std::vector<FamilyAdvisory> warn_incomplete_family(const Dictionary& d) {
+  const ConversionMatrix& u = full_u16();
+  std::vector<FamilyAdvisory> out;
+  for (int id : d.ids()) {
+    FamilyAdvisory a{id, {}, {}};
+    for (int c = id + 1; c < kNumGraphlets; ++c)
+      if (u.coeff(id, c) && !d.contains(c)) a.missing_supergraphs.push_back(c);
+    if (a.missing_supergraphs.empty()) continue;
+    std::ostringstream msg;
+    msg << "net counts for graphlet " << id << " (" << kSigma16[id].name
+        << ") will include non-induced occurrences: missing supergraph(s)";
+    for (int c : a.missing_supergraphs) msg << ' ' << c;
+    a.message = msg.str();
+    out.push_back(std::move(a));
+  }
+  return out;
+}
+
+// ===================================================================== graph
+SparseAdjacency::SparseAdjacency(std::vector<std::int64_t> row_offsets,
+                                 std::vector<vertex_t> col_indices)
+    : offsets_(std::move(row_offsets)), cols_(std::move(col_indices)) {
+  n_ = offsets_.empty() ? 0 : static_cast<vertex_t>(offsets_.size()) - 1;
+  if (offsets_.empty()) offsets_.push_back(0);
+  m_ = static_cast<count_t>(cols_.size()) / 2;
+  for (vertex_t v = 0; v < n_; ++v) d_max_ = std::max(d_max_, degree(v));
+}
+
+bool SparseAdjacency::has_edge(vertex_t u, vertex_t v) const {
+  auto r = row(u);
+  return std::binary_search(r.begin(), r.end(), v);
+}
+
+void SparseAdjacency::validate() const {
+  if (offsets_.front() != 0 || offsets_.back() != static_cast<std::int64_t>(cols_.size()))
+    throw StructuralError("corrupt row offsets");
+  for (vertex_t v = 0; v < n_; ++v) {
+    vertex_t prev = -1;
+    for (vertex_t x : row(v)) {
+      if (x < 0 || x >= n_) throw StructuralError("column out of range");
+      if (x == v) throw StructuralError("self-loop in adjacency");
+      if (x <= prev) throw StructuralError("row not strictly increasing");
+      if (!has_edge(x, v))
+        throw StructuralError("asymmetric adjacency at (" + std::to_string(v) + "," +
+                              std::to_string(x) + ")");
+      prev = x;
+    }
+  }
+}
+
+const Csr32& SparseAdjacency::csr32() const {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!narrow_) {
+    if (n_ >= (vertex_t{1} << 31) || cols_.size() >= (std::size_t{1} << 31))
+      throw StructuralError("graph exceeds the int32 CSR limits of the device path");
+    auto c = std::make_shared<Csr32>();
+    c->row_ptr.assign(offsets_.begin(), offsets_.end());
+    c->col_idx.assign(cols_.begin(), cols_.end());
+    narrow_ = std::move(c);
+  }
+  return *narrow_;
+}
+
+namespace {
+
+std::vector<std::string_view> tokens(std::string_view s) {
+  std::vector<std::string_view> out;
+  std::size_t i = 0;
+  while (i < s.size()) {
+    while (i < s.size() && std::isspace(static_cast<unsigned char>(s[i]))) ++i;
+    std::size_t j = i;
+    while (j < s.size() && !std::isspace(static_cast<unsigned char>(s[j]))) ++j;
+    if (j > i) out.push_back(s.substr(i, j - i));
+    i = j;
+  }
+  return out;
+}
+
+std::int64_t to_int(std::string_view t, std::size_t line, const char* what) {
+  std::int64_t v = 0;
+  const char* end = t.data() + t.size();
+  auto r = std::from_chars(t.data(), end, v);
+  if (r.ec != std::errc{} || r.ptr != end)
+    throw ParseError("line " + std::to_string(line) + ": malformed " + what + " '" +
+                     std::string(t) + "'");
+  return v;
+}
+
+std::string lower(std::string_view s) {
+  std::string o(s);
+  for (char& c : o) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+  return o;
+}
+
+bool skip_line(std::string_view body) {
+  auto t = tokens(body);
+  return t.empty() || t[0][0] == '#' || t[0][0] == '%';
+}
+
+}  // namespace
+
+EdgeCollection parse_edge_list(std::istream& in) {
+  EdgeCollection ec;
+  ec.origin = EdgeOrigin::kEdgeList;
+  std::string line;
+  std::size_t ln = 0;
+  while (std::getline(in, line)) {
+    ++ln;
+    if (skip_line(line)) continue;
+    auto t = tokens(line);
+    if (t.size() != 2)
+      throw ParseError("line " + std::to_string(ln) + ": expected 'u v', got " +
+                       std::to_string(t.size()) + " tokens");
+    const vertex_t u = to_int(t[0], ln, "vertex id"), v = to_int(t[1], ln, "vertex id");
+    if (u < 0 || v < 0) throw ParseError("line " + std::to_string(ln) + ": negative vertex id");
+    ec.edges.emplace_back(u, v);
+  }
+  return ec;
+}
+
+EdgeCollection parse_matrix_market(std::istream& in) {
+  std::string line;
+  if (!std::getline(in, line)) throw ParseError("empty Matrix Market stream");
+  auto banner = tokens(line);
+  if (banner.size() < 5 || lower(banner[0]) != "%%matrixmarket" || lower(banner[1]) != "matrix")
+    throw ParseError("line 1: missing %%MatrixMarket matrix banner");
+  if (lower(banner[2]) != "coordinate")
+    throw ParseError("line 1: only coordinate format is supported, got '" +
+                     std::string(banner[2]) + "'");
+  const std::string field = lower(banner[3]), sym = lower(banner[4]);
+  if (field != "pattern" && field != "real" && field != "integer")
+    throw ParseError("line 1: unsupported field '" + field + "'");
+  if (sym != "general" && sym != "symmetric")
+    throw ParseError("line 1: unsupported symmetry '" + sym + "'");
+  const std::size_t per_entry = field == "pattern" ? 2 : 3;
+  std::size_t ln = 1;
+  std::int64_t rows = -1, cols = -1, nnz = -1;
+  while (std::getline(in, line)) {
+    ++ln;
+    if (skip_line(line)) continue;
+    auto t = tokens(line);
+    if (t.size() != 3) throw ParseError("line " + std::to_string(ln) + ": expected 'rows cols nnz'");
+    rows = to_int(t[0], ln, "row count");
+    cols = to_int(t[1], ln, "column count");
+    nnz = to_int(t[2], ln, "entry count");
+    break;
+  }
+  if (rows < 0 && cols < 0 && nnz < 0) throw ParseError("unexpected end of stream before size line");
+  if (rows != cols)
+    throw ParseError("dimension mismatch: adjacency must be square, got " + std::to_string(rows) +
+                     "x" + std::to_string(cols));
+  if (rows < 0 || nnz < 0) throw ParseError("negative size header");
+  EdgeCollection ec;
+  ec.origin = sym == "symmetric" ? EdgeOrigin::kMatrixMarketSymmetric : EdgeOrigin::kMatrixMarketGeneral;
+  ec.declared_n = rows;
+  ec.edges.reserve(static_cast<std::size_t>(nnz));
+  std::int64_t got = 0;
+  while (got < nnz) {
+    if (!std::getline(in, line))
+      throw ParseError("unexpected end of stream: got " + std::to_string(got) + " of " +
+                       std::to_string(nnz) + " entries");
+    ++ln;
+    if (skip_line(line)) continue;
+    auto t = tokens(line);
+    if (t.size() != per_entry)
+      throw ParseError("line " + std::to_string(ln) + ": expected " + std::to_string(per_entry) +
+                       " tokens per entry");
+    const vertex_t i = to_int(t[0], ln, "row index"), j = to_int(t[1], ln, "column index");
+    if (i < 1 || i > rows || j < 1 || j > cols)
+      throw ParseError("line " + std::to_string(ln) + ": entry (" + std::to_string(i) + "," +
+                       std::to_string(j) + ") out of declared range " + std::to_string(rows));
+    ec.edges.emplace_back(i - 1, j - 1);
+    ++got;
+  }
+  return ec;
+}
+
+BuildResult build_adjacency(const EdgeCollection& ec, const SanitizeOptions& opt) {
+  vertex_t n = ec.declared_n.value_or(0);
+  for (const auto& [u, v] : ec.edges) {
+    if (u < 0 || v < 0) throw StructuralError("negative vertex id in edge collection");
+    n = std::max(n, std::max(u, v) + 1);
+  }
+  BuildResult out;
+  const bool mirror = opt.symmetrize || ec.declared_symmetric();
+  // pack (u, v) into one sortable 64-bit key per directed entry
+  std::vector<std::pair<vertex_t, vertex_t>> dir;
+  dir.reserve(ec.edges.size() * (mirror ? 2 : 1));
+  for (const auto& [u, v] : ec.edges) {
+    if (u == v) {
+      if (!opt.drop_self_loops)
+        throw StructuralError("self-loop at vertex " + std::to_string(u) +
+                              " (drop_self_loops is off)");
+      ++out.report.self_loops_dropped;
+      continue;
+    }
+    dir.emplace_back(u, v);
+    if (mirror) dir.emplace_back(v, u);
+  }
+  std::sort(dir.begin(), dir.end());
+  const std::size_t before = dir.size();
+  dir.erase(std::unique(dir.begin(), dir.end()), dir.end());
+  if (dir.size() != before) {
+    if (!opt.dedupe) throw StructuralError("duplicate edges present (dedupe is off)");
+    out.report.duplicates_merged = static_cast<count_t>(before - dir.size()) / 2;
+  }
+  std::vector<std::int64_t> off(static_cast<std::size_t>(n) + 1, 0);
+  std::vector<vertex_t> col(dir.size());
+  for (std::size_t k = 0; k < dir.size(); ++k) {
+    ++off[static_cast<std::size_t>(dir[k].first) + 1];
+    col[k] = dir[k].second;
+  }
+  for (std::size_t i = 1; i < off.size(); ++i) off[i] += off[i - 1];
+  out.graph = SparseAdjacency(std::move(off), std::move(col));
+  if (!mirror) {
+    // a non-symmetrised input must already be symmetric
+    const auto& g = out.graph;
+    for (vertex_t v = 0; v < g.num_vertices(); ++v)
+      for (vertex_t x : g.row(v))
+        if (!g.has_edge(x, v))
+          throw StructuralError("asymmetric adjacency at (" + std::to_string(v) + "," +
+                                std::to_string(x) + ")");
+  }
+  return out;
+}
+
+std::vector<count_t> degree_vector(const SparseAdjacency& g) {
+  std::vector<count_t> d(static_cast<std::size_t>(g.num_vertices()));
+  for (vertex_t v = 0; v < g.num_vertices(); ++v) d[v] = static_cast<count_t>(g.degree(v));
+  return d;
+}
+
+// ================================================================ conversion
+namespace {
+
+// U16 (Table 2): rows raw graphlet, columns net graphlet.
+constexpr unsigned char kU[kNumGraphlets][kNumGraphlets] = {
+    {1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, {0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 1, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 1, 0, 2, 4, 2, 6},
+    {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 2, 2, 2, 4, 6}, {0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 2, 1, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 1, 1}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 0, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 2, 6}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 3}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 3}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
+};
+
+}  // namespace
+
+ConversionMatrix::ConversionMatrix(std::vector<int> ids, std::vector<std::vector<count_t>> dense)
+    : ids_(std::move(ids)), dense_(std::move(dense)), tails_(ids_.size()) {
+  for (std::size_t r = 0; r < ids_.size(); ++r) {
+    if (dense_[r][r] != 1)
+      throw Error("conversion matrix is not unit-diagonal at row " + std::to_string(r));
+    for (std::size_t c = 0; c < ids_.size(); ++c) {
+      if (c < r && dense_[r][c])
+        throw Error("conversion matrix is not upper triangular at (" + std::to_string(r) + "," +
+                    std::to_string(c) + ")");
+      if (c > r && dense_[r][c]) tails_[r].emplace_back(c, dense_[r][c]);
+    }
+  }
+}
+
+ConversionMatrix sub_matrix(const Dictionary& d) {
+  const auto& ids = d.ids();
+  std::vector<std::vector<count_t>> m(ids.size(), std::vector<count_t>(ids.size(), 0));
+  for (std::size_t r = 0; r < ids.size(); ++r)
+    for (std::size_t c = 0; c < ids.size(); ++c) m[r][c] = kU[ids[r]][ids[c]];
+  return ConversionMatrix(ids, std::move(m));
+}
+
+const ConversionMatrix& full_u16() {
+  static const ConversionMatrix u = sub_matrix(Dictionary::all());
+  return u;
+}
+
+RawFrequencyField apply_conversion(const NetFrequencyField& net, const ConversionMatrix& U) {
+  if (net.dictionary().ids() != U.ids())
+    throw Error("conversion matrix does not match the field's dictionary");
+  RawFrequencyField raw(net.num_vertices(), net.dictionary());
+  for (vertex_t v = 0; v < net.num_vertices(); ++v) {
+    auto in = net.vertex_row(v);
+    auto out = raw.vertex_row(v);
+    for (std::size_t r = 0; r < U.dim(); ++r) {
+      count_t acc = in[r];
+      for (auto [c, k] : U.row_tail(r))
+        acc = checked_add(acc, checked_mul(k, in[c], U.ids()[r], v), U.ids()[r], v);
+      out[r] = acc;
+    }
+  }
+  return raw;
+}
+
+bool inverse_pattern_check(const ConversionMatrix& U) {
+  const std::size_t k = U.dim();
+  // exact integer inverse, column by column (unit upper triangular)
+  std::vector<std::vector<std::int64_t>> inv(k, std::vector<std::int64_t>(k, 0));
+  for (std::size_t col = 0; col < k; ++col)
+    for (std::size_t r = k; r-- > 0;) {
+      std::int64_t x = r == col ? 1 : 0;
+      for (auto [c, coef] : U.row_tail(r)) x -= static_cast<std::int64_t>(coef) * inv[c][col];
+      inv[r][col] = x;
+    }
+  for (std::size_t r = 0; r < k; ++r)
+    for (std::size_t c = 0; c < k; ++c)
+      if (inv[r][c] && !U.coeff(r, c)) return false;  // fill-in outside U's pattern
+  for (std::size_t r = 0; r < k; ++r)
+    for (std::size_t j = r + 1; j < k; ++j)
+      if (U.coeff(r, j))
+        for (std::size_t c = j + 1; c < k; ++c)
+          if (U.coeff(j, c) && !U.coeff(r, c)) return false;  // not transitively closed
+  return true;
+}
+
+// ============================================================ device bridge
+namespace {
+
+std::mutex g_ctx_mu;
+std::map<int, fglt_ctx*> g_ctx;
+
+fglt_ctx* context_for(int device) {
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  auto it = g_ctx.find(device);
+  if (it != g_ctx.end()) return it->second;
+  fglt_error err{};
+  fglt_ctx* c = fglt_ctx_create(device, nullptr, &err);
+  if (!c) throw Error(std::string("CUDA device unavailable: ") + err.msg);
+  g_ctx[device] = c;
+  return c;
+}
+
+[[noreturn]] void rethrow(int rc, const fglt_error& e) {
+  switch (rc) {
+    case FGLT_E_PARSE: throw ParseError(e.msg);
+    case FGLT_E_STRUCTURAL: throw StructuralError(e.msg);
+    case FGLT_E_OVERFLOW: throw OverflowError(e.msg, e.graphlet_id, e.vertex);
+    case FGLT_E_INCONSISTENCY: throw InconsistencyError(e.msg, e.graphlet_id, e.vertex);
+    case FGLT_E_IO: throw IoError(e.msg);
+    default: throw Error(std::string("device transform failed: ") + e.msg);
+  }
+}
+
+TransformStats stats_of(const fglt_stats& s) {
+  TransformStats t;
+  for (int i = 0; i < s.num_steps; ++i) t.kernel_times.push_back({s.step_names[i], s.step_seconds[i]});
+  t.p2_row_touches = s.p2_row_touches;
+  t.p2_touch_bound = s.p2_touch_bound;
+  t.peak_aux_words = s.peak_aux_words;
+  t.largest_aux_alloc_words = s.largest_aux_alloc_words;
+  t.threads_used = s.threads_used;
+  return t;
+}
+
+std::mutex g_run_mu;  // one transform per context at a time
+
+void run(const SparseAdjacency& g, const Dictionary& dict, bool lenient, int device,
+         count_t* raw, count_t* net, TransformStats* stats) {
+  const Csr32& c = g.csr32();
+  fglt_ctx* ctx = context_for(device);
+  fglt_stats st{};
+  fglt_error err{};
+  int rc;
+  {
+    std::lock_guard<std::mutex> lock(g_run_mu);
+    rc = fglt_ctx_transform(ctx, c.row_ptr.data(), c.col_idx.data(), g.num_vertices(),
+                            static_cast<std::int64_t>(c.col_idx.size()), dict.mask(), lenient ? 1 : 0,
+                            stats ? FGLT_TIMINGS : 0u, raw, net, stats ? &st : nullptr, &err);
+  }
+  if (rc) rethrow(rc, err);
+  if (stats) *stats = stats_of(st);
+}
+
+}  // namespace
+
+RawFrequencyField raw_frequencies(const SparseAdjacency& g, const Dictionary& dict,
+                                  const KernelOptions& opt, TransformStats* stats) {
+  RawFrequencyField raw(g.num_vertices(), dict);
+  TransformStats st;
+  // lenient: raw columns must not depend on whether the family is complete
+  run(g, dict, /*lenient=*/true, opt.device, raw.mutable_data(), nullptr, &st);
+  // the conversion step is not part of raw_frequencies
+  if (!st.kernel_times.empty() && st.kernel_times.back().name == "conversion")
+    st.kernel_times.pop_back();
+  if (stats) *stats = st;
+  return raw;
+}
+
+TransformResult transform(const SparseAdjacency& g, const TransformOptions& opt) {
+  TransformResult r{RawFrequencyField(g.num_vertices(), opt.dict),
+                    NetFrequencyField(g.num_vertices(), opt.dict), {}};
+  run(g, opt.dict, opt.lenient, opt.device, r.raw.mutable_data(), r.net.mutable_data(), &r.stats);
+  return r;
+}
+
+NetFrequencyField net_from_raw(const RawFrequencyField& raw, const ConversionMatrix& U,
+                               bool lenient, int /*threads*/) {
+  if (raw.dictionary().ids() != U.ids())
+    throw Error("conversion matrix does not match the field's dictionary");
+  NetFrequencyField net(raw.num_vertices(), raw.dictionary());
+  if (raw.num_vertices() == 0) return net;
+  fglt_ctx* ctx = context_for(0);
+  fglt_error err{};
+  int rc;
+  {
+    std::lock_guard<std::mutex> lock(g_run_mu);
+    rc = fglt_net_from_raw(ctx, raw.data().data(), raw.num_vertices(), raw.dictionary().mask(),
+                           lenient ? 1 : 0, net.mutable_data(), &err);
+  }
+  if (rc) rethrow(rc, err);
+  return net;
+}
+
+}  // namespace graphlet

@@ -246,3 +246,89 @@ def test_repeat_determinism_at_scale():
         np.testing.assert_array_equal(raw, base[0])
         np.testing.assert_array_equal(net, base[1])
     c.close()
+
+
+def test_reference_golden_fixtures(ctx):
+    """Tables produced by the reference itself (tests/golden/make_golden.py)."""
+    import hashlib
+    import json
+    import os
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    cfg = json.load(open(os.path.join(gold, "config1.json")))
+    rp, ci = graphs.er(2000, 0.004, 1)
+    raw, net, _ = ctx.transform_host(rp, ci)
+    assert hashlib.sha256(raw.tobytes()).hexdigest() == cfg["raw_sha256"]
+    assert hashlib.sha256(net.tobytes()).hexdigest() == cfg["net_sha256"]
+    z = np.load(os.path.join(gold, "small_tables.npz"))
+    for name in sorted({k[:-3] for k in z.files if k.endswith("_rp")}):
+        raw, net, _ = ctx.transform_host(z[name + "_rp"], z[name + "_ci"])
+        np.testing.assert_array_equal(raw, z[name + "_raw"], err_msg=name)
+        np.testing.assert_array_equal(net, z[name + "_net"], err_msg=name)
+    rp, ci = z["rmat10_rp"], z["rmat10_ci"]
+    for key in z.files:
+        if not key.startswith("rmat10_m"):
+            continue
+        mask, lenient = int(key[8:12], 16), bool(int(key[14]))
+        if key.endswith("_err"):
+            with pytest.raises(_capi.TransformFailed) as ei:
+                ctx.transform_host(rp, ci, mask, lenient)
+            assert [ei.value.code, ei.value.graphlet_id, ei.value.vertex] == z[key].tolist()
+        elif key.endswith("_raw"):
+            raw, net, _ = ctx.transform_host(rp, ci, mask, lenient)
+            np.testing.assert_array_equal(raw, z[key])
+            np.testing.assert_array_equal(net, z[key[:-4] + "_net"])
+
+
+def test_stats_contract(ctx):
+    """Step names in reference plan order (test_pipeline.cpp:78-94) and the
+    touch identity / bound (test_pipeline.cpp:96-108)."""
+    rp, ci = gu.demo()
+    _, _, st = ctx.transform_host(rp, ci, _capi.dict_mask([]), timings=True)
+    assert [k for k, _ in st["kernel_times"]] == ["degrees", "column fill", "conversion"]
+    _, _, st = ctx.transform_host(rp, ci, _capi.dict_mask([12]), timings=True)
+    assert [k for k, _ in st["kernel_times"]] == ["degrees", "four-cycle rows", "column fill",
+                                                  "conversion"]
+    _, _, st = ctx.transform_host(rp, ci, 0xFFFF, timings=True)
+    assert [k for k, _ in st["kernel_times"]] == [
+        "degrees", "triangles", "two-paths", "three-paths", "four-cycle rows", "diamond rows",
+        "tetrahedra", "column fill", "conversion"]
+    rp, ci = gu.regular(400, 4, 11)
+    _, _, st = ctx.transform_host(rp, ci)
+    assert 0 < st["p2_row_touches"] <= st["p2_touch_bound"]
+    assert st["p2_row_touches"] == st["W"] - len(ci)
+
+
+def test_sharded_stages_byte_identical(ctx):
+    """The staged (multi-rank) decomposition run rank by rank on one GPU:
+    partial edge counts and root vectors summed across 'ranks' give the same
+    bytes as the single-call path (the NCCL exchange is a plain integer sum)."""
+    import torch
+    from paper_2007_11111_b200.dist import CudaStages
+    rp, ci = graphs.rmat(14, 16, seed=4)
+    n, nnz = len(rp) - 1, len(ci)
+    want_raw, want_net, _ = ctx.transform_host(rp, ci)
+    dev = torch.device("cuda", 0)
+    rp_d, ci_d = torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev)
+    for world in (2, 3, 8):
+        st = CudaStages(dev)
+        st.prepare(rp_d, ci_d, n, nnz, 0xFFFF, False)
+        b = st.bounds(world)
+        assert b[0] == 0 and b[-1] == n and (np.diff(b) >= 0).all()
+        c3 = None
+        for r in range(world):
+            part = st.triangles(int(b[r]), int(b[r + 1])).clone()
+            c3 = part if c3 is None else c3 + part
+        st.triangles(0, 0).copy_(c3)
+        st.local()
+        vec = None
+        for r in range(world):
+            part = st.roots(int(b[r]), int(b[r + 1])).clone()
+            st.roots(0, 0).zero_()
+            vec = part if vec is None else vec + part
+        st.roots(0, 0).copy_(vec)
+        raw = torch.empty((n, 16), dtype=torch.int64, device=dev)
+        net = torch.empty((n, 16), dtype=torch.int64, device=dev)
+        rc, err = st.epilogue(0, n, raw, net)
+        assert rc == 0, err
+        np.testing.assert_array_equal(raw.cpu().numpy().view(np.uint64), want_raw)
+        np.testing.assert_array_equal(net.cpu().numpy().view(np.uint64), want_net)
