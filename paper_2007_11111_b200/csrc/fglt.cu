@@ -60,7 +60,7 @@ constexpr int kWarpHashLog = 9;   // 512-slot table per warp
 enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
-  B_CUB, B_CURSOR, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_COUNT
+  B_CUB, B_CURSOR, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY, B_COUNT
 };
 
 struct DevBuf {
@@ -198,6 +198,11 @@ struct fglt_ctx {
   bool have_stats = false;
   uint64_t W = 0, dmax = 0, maxout = 0;
 
+  // root bins by |N+(u)| (shared by the triangle and diamond passes)
+  int64_t rb_u0 = -1, rb_u1 = -1;
+  std::vector<int> rb_cnt;
+  int* rb_lists[8] = {};
+
   // test hooks (fglt_ctx_set_debug): force one code path for every root
   int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1;
 
@@ -327,6 +332,8 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   c->vec = c->ensure<u64>(B_VEC, (size_t)V_COUNT * std::max<int64_t>(n, 1));
   CK(cudaMemsetAsync(c->vec, 0, (size_t)V_COUNT * std::max<int64_t>(n, 1) * 8, c->stream));
   c->perm = c->inv = nullptr;
+  c->rb_u0 = c->rb_u1 = -1;  // graph changed: root bins are stale
+  c->rb_cnt.clear();
   c->rp = d_rp;
   c->ci = d_ci;
   c->have_stats = false;
@@ -424,16 +431,6 @@ void sweep_a(fglt_ctx* c) {
   DISPATCH_G(G, launch_sweep_a, c);
 }
 
-void triangles(fglt_ctx* c, int64_t e0, int64_t e1) {
-  if (!c->plan.c3 || c->n == 0) return;
-  CK(cudaMemsetAsync(c->C3f, 0, (size_t)std::max<int64_t>(c->nnz, 1) * 4, c->stream));
-  if (e1 > e0) {
-    k_triangles<<<c->grid(e1 - e0, 256), 256, 0, c->stream>>>(
-        c->rp, c->ci, c->split, c->ce_row, c->ce_pos, (int)e0, (int)e1, c->C3f);
-    check_launch();
-    c->launched();
-  }
-}
 
 void local_sweeps(fglt_ctx* c) {
   if (!c->plan.c3 || c->n == 0) return;
@@ -448,11 +445,12 @@ void local_sweeps(fglt_ctx* c) {
 
 // Bin roots [u0,u1) by key into up to 3 lists; returns counts (host sync).
 std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
-                           const std::vector<u64>& thr, int** lists, int64_t* stride) {
+                           const std::vector<u64>& thr, int** lists, int64_t* stride,
+                           Buf which = B_LISTS) {
   const int nb = (int)thr.size() + 1;
   if (nb > 8) throw CudaFail{FGLT_E_CUDA, "internal: at most 8 root bins"};
   const int64_t span = std::max<int64_t>(u1 - u0, 1);
-  int* lst = c->ensure<int>(B_LISTS, (size_t)nb * span);
+  int* lst = c->ensure<int>(which, (size_t)nb * span);
   u64* d_thr = c->d_small + 8;
   int* counts = reinterpret_cast<int*>(c->d_small + 16);
   std::vector<u64> th(thr);
@@ -474,6 +472,7 @@ std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
   return h;
 }
 
+
 __global__ void k_outdeg_key(const int* __restrict__ rp, const int* __restrict__ split, int n,
                              u64* __restrict__ key, u64 force_key) {
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
@@ -486,10 +485,90 @@ __global__ void k_outdeg_key(const int* __restrict__ rp, const int* __restrict__
   }
 }
 
+constexpr u64 kRootThr[] = {(u64)kSmallS, 128, 256, 512, (u64)kBlockS};
+
+// Bin roots [u0,u1) by |N+(u)| (>= 2) once; both root passes reuse the lists.
+void root_bins(fglt_ctx* c, int64_t u0, int64_t u1) {
+  if (c->rb_u0 == u0 && c->rb_u1 == u1 && !c->rb_cnt.empty()) return;
+  u64* key = c->ensure<u64>(B_RKEY, (size_t)std::max<int64_t>(c->n, 1));
+  static const u64 kForceKey[] = {0, 33, 129, 257, 513, 1025};
+  const u64 fk = (c->force_roots_bin > 0 && c->force_roots_bin < 6) ? kForceKey[c->force_roots_bin] : 0;
+  k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->rp, c->split, (int)c->n, key, fk);
+  check_launch();
+  c->launched();
+  int64_t stride = 0;
+  c->rb_cnt = bin_roots(c, key, u0, u1, std::vector<u64>(std::begin(kRootThr), std::end(kRootThr)),
+                        c->rb_lists, &stride, B_RLISTS);
+  c->rb_u0 = u0;
+  c->rb_u1 = u1;
+}
+
+// One root-centric pass over the binned roots: MODE 0 = triangle pass (C3
+// atomics, plus 4-cliques when requested), MODE 1 = diamond pass (needs final C3).
+template <bool kC3, bool kD13, bool kD15>
+void roots_pass(fglt_ctx* c) {
+  if (!c->have_stats)  // the bins are sized by max |N+(u)|: never guess
+    throw CudaFail{FGLT_E_CUDA, "internal: graph stats not read before a root pass"};
+  u64* d13 = c->V(V_D13);
+  u64* d15 = c->V(V_D15);
+  const std::vector<int>& cnt = c->rb_cnt;
+  int** lists = c->rb_lists;
+  if (cnt[0] > 0) {
+    const int wpb = 8;
+    const size_t sm = (size_t)wpb * (32 * 8 + 96 * 4);
+    const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
+    k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f,
+                                                                  lists[0], cnt[0], d13, d15);
+    check_launch();
+    c->launched();
+  }
+  for (int b = 1; b < (int)cnt.size(); ++b) {
+    if (cnt[b] == 0) continue;
+    const bool global = b == (int)cnt.size() - 1;  // s > kBlockS
+    RootsLayout L;
+    L.s_cap = global ? (int)c->maxout : (int)std::min<u64>(kRootThr[b], std::max<u64>(c->maxout, 33));
+    L.hlog = 6;
+    while ((1 << L.hlog) < 4 * L.s_cap) ++L.hlog;
+    L.hcap = 1 << L.hlog;
+    L.nwarps = 8;
+    L.stride_cap = ((L.s_cap + 31) / 32) | 1;
+    size_t sm = L.bytes_core();
+    unsigned char* slab = nullptr;
+    long long slab_stride = 0;
+    int g = std::min(cnt[b], c->sms * 8);
+    if (global) {
+      slab_stride = (long long)((L.bytes_aux() + 255) & ~(size_t)255);
+      const long long fit = std::max<long long>(1, (4ll << 30) / slab_stride);
+      g = (int)std::min<long long>({(long long)cnt[b], (long long)c->sms, fit});
+      slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
+      set_smem(k_roots_block<kC3, kD13, kD15, true>, sm);
+      k_roots_block<kC3, kD13, kD15, true><<<g, 256, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], L, slab, slab_stride, d13, d15);
+    } else {
+      sm += L.bytes_aux();
+      set_smem(k_roots_block<kC3, kD13, kD15, false>, sm);
+      k_roots_block<kC3, kD13, kD15, false><<<g, 256, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], L, slab, slab_stride, d13, d15);
+    }
+    check_launch();
+    c->launched();
+  }
+}
+
+// Triangle pass over roots [u0,u1): per-edge C3 (and d15 when requested).
+void triangles(fglt_ctx* c, int64_t u0, int64_t u1) {
+  const Plan& P = c->plan;
+  if (!(P.c3 || P.d15) || c->n == 0) return;
+  if (P.c3) CK(cudaMemsetAsync(c->C3f, 0, (size_t)std::max<int64_t>(c->nnz, 1) * 4, c->stream));
+  root_bins(c, u0, u1);
+  if (P.c3 && P.d15) roots_pass<true, false, true>(c);
+  else if (P.c3) roots_pass<true, false, false>(c);
+  else roots_pass<false, false, true>(c);
+}
+
 void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   const Plan& P = c->plan;
-  if (c->n == 0 || !(P.c4 || P.d13 || P.d15)) return;
-  const int N = (int)c->n;
+  if (c->n == 0 || !(P.c4 || P.d13)) return;
   u64* work = c->ensure<u64>(B_WORK, 4 * (size_t)c->n);
   u64* wc = work;
   u64* key = work + c->n;
@@ -544,70 +623,10 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     }
     c->mark("four-cycle rows:end");
   }
-  if (P.d13 || P.d15) {
-    static const u64 kForceKey[] = {0, 33, 129, 257, 513, 1025};
-    const u64 fk = (c->force_roots_bin > 0 && c->force_roots_bin < 6) ? kForceKey[c->force_roots_bin] : 0;
-    k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->rp, c->split, N, key, fk);
-    check_launch();
-    c->launched();
-    const std::vector<u64> thr = {(u64)kSmallS, 128, 256, 512, (u64)kBlockS};
-    std::vector<int> cnt = bin_roots(c, key, u0, u1, thr, lists, &stride);
+  if (P.d13) {
+    root_bins(c, u0, u1);
     c->mark("roots:start");
-    u64* d13 = c->V(V_D13);
-    u64* d15 = c->V(V_D15);
-    if (cnt[0] > 0) {
-      const int wpb = 8;
-      const size_t sm = (size_t)wpb * (32 * 8 + 96 * 4);
-      const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
-      if (P.d13 && P.d15)
-        k_roots_warp<true, true><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[0], cnt[0], d13, d15);
-      else if (P.d13)
-        k_roots_warp<true, false><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[0], cnt[0], d13, d15);
-      else
-        k_roots_warp<false, true><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f, lists[0], cnt[0], d13, d15);
-      check_launch();
-      c->launched();
-    }
-    for (int b = 1; b < (int)cnt.size(); ++b) {
-      if (cnt[b] == 0) continue;
-      const bool global = b == (int)cnt.size() - 1;  // s > kBlockS
-      RootsLayout L;
-      L.s_cap = global ? (int)c->maxout : (int)std::min<u64>(thr[b], std::max<u64>(c->maxout, 33));
-      L.hlog = 6;
-      while ((1 << L.hlog) < 4 * L.s_cap) ++L.hlog;
-      L.hcap = 1 << L.hlog;
-      L.nwarps = 8;
-      L.stride_cap = ((L.s_cap + 31) / 32) | 1;
-      size_t sm = L.bytes_core();
-      unsigned char* slab = nullptr;
-      long long slab_stride = 0;
-      int g = std::min(cnt[b], c->sms * 8);
-      if (global) {
-        slab_stride = (long long)((L.bytes_aux() + 255) & ~(size_t)255);
-        const long long fit = std::max<long long>(1, (4ll << 30) / slab_stride);
-        g = (int)std::min<long long>({(long long)cnt[b], (long long)c->sms, fit});
-        slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
-      } else {
-        sm += L.bytes_aux();
-      }
-#define LAUNCH_ROOTS(D13, D15, GL)                                                          \
-  do {                                                                                      \
-    set_smem(k_roots_block<D13, D15, GL>, sm);                                              \
-    k_roots_block<D13, D15, GL><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f,  \
-                                                           lists[b], cnt[b], L, slab,       \
-                                                           slab_stride, d13, d15);          \
-  } while (0)
-      if (P.d13 && P.d15) {
-        if (global) LAUNCH_ROOTS(true, true, true); else LAUNCH_ROOTS(true, true, false);
-      } else if (P.d13) {
-        if (global) LAUNCH_ROOTS(true, false, true); else LAUNCH_ROOTS(true, false, false);
-      } else {
-        if (global) LAUNCH_ROOTS(false, true, true); else LAUNCH_ROOTS(false, true, false);
-      }
-#undef LAUNCH_ROOTS
-      check_launch();
-      c->launched();
-    }
+    roots_pass<false, true, false>(c);
     c->mark("roots:end");
   }
 }
@@ -845,17 +864,14 @@ int fglt_ctx_transform(fglt_ctx* c, const int32_t* row_ptr, const int32_t* col_i
       d_ci = b;
     }
     prepare(c, d_rp, d_ci, n, nnz, dict_mask, lenient);
-    if (c->plan.c4 && !c->have_stats && n > 0) {
-      // the tile kernel sizes its cursor slices by d_max
-      read_graph_stats(c);
-    }
-    if ((c->plan.d13 || c->plan.d15) && !c->have_stats && n > 0) {
+    if (c->plan.enumerate && !c->have_stats && n > 0) {
+      // d_max sizes the 4-cycle cursor slices, max |N+(u)| the root bins
       read_graph_stats(c);
     }
     sweep_a(c);
     c->mark("degrees:end");
     c->mark("triangles:start");
-    triangles(c, 0, c->m);
+    triangles(c, 0, n);
     local_sweeps(c);
     c->mark("triangles:end");
     roots(c, 0, n);
@@ -1001,14 +1017,7 @@ int fglt_stage_triangles(fglt_ctx* c, int64_t u0, int64_t u1, uint32_t** d_edge_
     CK(cudaSetDevice(c->device));
     *d_edge_counts = c->C3f;
     *count = c->plan.c3 ? c->nnz : 0;
-    if (!c->plan.c3) return FGLT_OK;
-    int o[2] = {0, 0};
-    if (c->n > 0) {
-      CK(cudaMemcpyAsync(&o[0], c->orp + u0, 4, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(&o[1], c->orp + u1, 4, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
-    }
-    triangles(c, o[0], o[1]);
+    triangles(c, u0, u1);
     CK(cudaStreamSynchronize(c->stream));
     return FGLT_OK;
   } catch (const CudaFail& f) {

@@ -224,77 +224,8 @@ __global__ void k_sweep_a(const int* __restrict__ rp, const int* __restrict__ ci
   }
 }
 
-// --------------------------------------------------------- triangle pass K2
-// Edge-centric over canonical edges (u, x) of roots u in [e0, e1): every
-// triangle u < x < y is found exactly once, as y in N+(x) ∩ (N+(u) after x).
-// Per triangle: C3(x,y) += 1 and C3(u,y) += 1 by global atomics; C3(u,x) gets
-// the warp's hit count once. Values live at canonical positions of C3f.
-__global__ void __launch_bounds__(256)
-k_triangles(const int* __restrict__ rp, const int* __restrict__ ci,
-            const int* __restrict__ split, const int* __restrict__ ce_row,
-            const int* __restrict__ ce_pos, int e0, int e1, u32* __restrict__ C3f) {
-  // Warp batches of 32 canonical edges (u, x); their probe lists N+(x), cut at
-  // max N+(u), are flattened in interleaved (coalesced) order and each lane
-  // tracks its current edge through per-warp shared tables.
-  __shared__ int t_base[8][32], t_off[8][33], t_lo[8][32], t_hi[8][32];
-  __shared__ u32 t_hits[8][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int* bst = t_base[wid];
-  int* boff = t_off[wid];
-  int* blo = t_lo[wid];
-  int* bhi = t_hi[wid];
-  u32* hits = t_hits[wid];
-  hits[lane] = 0;
-  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
-  for (long long eb = e0 + gw * 32; eb < e1; eb += nwarps * 32) {
-    const long long e = eb + lane;
-    const bool valid = e < e1;
-    int pux = 0, send = 0, st = 0, se = 0;
-    if (valid) {
-      const int u = ce_row[e];
-      pux = ce_pos[e];
-      send = rp[u + 1];
-      if (pux + 1 < send) {
-        const int x = ci[pux];
-        const int smax = ci[send - 1];
-        st = split[x];
-        se = lower_bound_i32(ci, st, rp[x + 1], smax + 1);
-      }
-    }
-    int T;
-    const int off = flat_prefix(se - st, &T);
-    bst[lane] = st - off;
-    boff[lane] = off;
-    blo[lane] = pux + 1;
-    bhi[lane] = send;
-    if (lane == 0) boff[32] = T;
-    __syncwarp();
-    int r = 0;
-    u32 h = 0;
-    for (int kk = lane; kk < T; kk += 32) {
-      if (boff[r + 1] <= kk) {
-        if (h) atomicAdd(hits + r, h);
-        h = 0;
-        do { ++r; } while (boff[r + 1] <= kk);
-      }
-      const int p = bst[r] + kk;
-      const int y = __ldg(ci + p);
-      const int hi = bhi[r];
-      const int q = lower_bound_i32(ci, blo[r], hi, y);
-      if (q < hi && __ldg(ci + q) == y) {
-        atomicAdd(C3f + p, 1u);
-        atomicAdd(C3f + q, 1u);
-        ++h;
-      }
-    }
-    if (h) atomicAdd(hits + r, h);
-    __syncwarp();
-    if (valid && hits[lane]) atomicAdd(C3f + pux, hits[lane]);
-    hits[lane] = 0;
-    __syncwarp();
-  }
-}
+// The triangle pass (per-edge C3, and 4-cliques) is root-centric: see
+// k_roots_warp / k_roots_block<kC3=true> in fglt_roots.cuh.
 
 // Copy canonical C3 values into their mirror slots so rows read contiguously.
 __global__ void k_c3_mirror(const int* __restrict__ ce_pos, const int* __restrict__ mir,

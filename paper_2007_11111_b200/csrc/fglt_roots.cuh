@@ -281,6 +281,46 @@ k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
 // twice (count, attribution). Rows are split at the first one of length >=
 // kC4Long (rows of N-(u) are in ascending degree): short rows thread-per-row,
 // long rows warp-cooperative.
+// First index in [lo, hi) with a[i] >= key, found by the whole warp with a
+// 32-ary search (one coalesced probe round per factor of 32). Warp-uniform.
+__device__ __forceinline__ int warp_lower_bound(const int* __restrict__ a, int lo, int hi,
+                                                int key) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) >> 5;
+    const int pos = lo + step * (lane + 1) - 1;
+    const bool less = pos < hi && __ldg(a + pos) < key;
+    const int c = __popc(__ballot_sync(0xffffffffu, less));
+    lo += c * step;
+    hi = min(hi, lo + step);
+  }
+  const int pos = lo + lane;
+  const bool less = pos < hi && __ldg(a + pos) < key;
+  return lo + __popc(__ballot_sync(0xffffffffu, less));
+}
+
+// f(a[i]) for i in [st, se) by the whole warp: scalar head/tail, 16-byte
+// vector body (two vectors in flight per lane).
+template <class F>
+__device__ __forceinline__ void warp_for_each(const int* __restrict__ a, int st, int se, F&& f) {
+  const int lane = threadIdx.x & 31;
+  const int a0 = min(se, (st + 3) & ~3);
+  const int a1 = max(a0, se & ~3);
+  if (st + lane < a0) f(__ldg(a + st + lane));
+  int p = a0 + 4 * lane;
+  for (; p + 128 < a1; p += 256) {
+    const int4 x = __ldg(reinterpret_cast<const int4*>(a + p));
+    const int4 y = __ldg(reinterpret_cast<const int4*>(a + p + 128));
+    f(x.x); f(x.y); f(x.z); f(x.w);
+    f(y.x); f(y.y); f(y.z); f(y.w);
+  }
+  if (p < a1) {
+    const int4 x = __ldg(reinterpret_cast<const int4*>(a + p));
+    f(x.x); f(x.y); f(x.z); f(x.w);
+  }
+  if (a1 + lane < se) f(__ldg(a + a1 + lane));
+}
+
 // Block-wide flattening of one segment per thread: writes exclusive offsets
 // (g_off[0..nthreads], g_off[nthreads] = total) and per-row element bases
 // g_st[r] = start - off; returns the total. Contains __syncthreads.
@@ -336,10 +376,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   __shared__ int bst_all[32][32];
   __shared__ int boff_all[32][33];
   __shared__ int next_batch[2];
-  __shared__ int g_off[1025];
-  __shared__ int g_st[1024];
-  __shared__ u64 g_sum[1024];
-  __shared__ int wtot[32];
+  __shared__ int next_giant[2];
   constexpr int TILE = PACK ? kC4Tile16 : kC4Tile32;
   u32* L = reinterpret_cast<u32*>(smem_raw);
   int* cur = cursor + (long long)blockIdx.x * 2 * cursor_stride;
@@ -368,9 +405,9 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
       if (rp[v + 1] - rp[v] < kC4Long) lo_q = mid + 1; else hi_q = mid;
     }
     const int qs = lo_q;
-    // giant rows: expected >= 64 elements per tile -> block-wide flattening
+    // giant rows: expected >= 512 elements per tile -> warp per row
     const int ntiles = (u + TILE - 1) / TILE;
-    const int giant_deg = max(kC4Long, 64 * ntiles);
+    const int giant_deg = max(kC4Long, 512 * ntiles);
     hi_q = nq;
     while (lo_q < hi_q) {
       const int mid = (lo_q + hi_q) >> 1;
@@ -389,41 +426,24 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         const int n4 = (words + 3) >> 2;
         for (int i = threadIdx.x; i < n4; i += blockDim.x) L4[i] = make_uint4(0, 0, 0, 0);
       }
-      if (threadIdx.x == 0) { next_batch[0] = 0; next_batch[1] = 0; }
+      if (threadIdx.x == 0) {
+        next_batch[0] = next_batch[1] = 0;
+        next_giant[0] = next_giant[1] = 0;
+      }
       __syncthreads();
-      // ---- count pass: giant rows block-wide, then short and long rows
-      for (int g0 = qg; g0 < nq; g0 += blockDim.x) {
-        const int q = g0 + threadIdx.x;
-        const bool valid = q < nq;
-        int st = 0, se = 0;
-        if (valid) {
-          st = cur[q];
-          const int em = mir[b + q];
-          se = hi >= u ? em : lower_bound_i32(ci, st, em, hi);
-          segend[q] = se;
-        }
-        const int T = block_flatten(se - st, st, g_off, g_st, wtot);
-        // each warp streams a contiguous slice of the flattened elements
-        const int nwarp = blockDim.x >> 5;
-        const int per = (((T + nwarp - 1) / nwarp) + 31) & ~31;
-        const int k0 = wid * per, k1 = min(T, k0 + per);
-        int r = k0 + lane < k1 ? upper_row(g_off, k0 + lane, blockDim.x) : 0;
-        for (int kk = k0 + lane; kk < k1; kk += 128) {  // 4 independent loads in flight
-          int w[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int kj = kk + 32 * j;
-            w[j] = -1;
-            if (kj < k1) {
-              while (g_off[r + 1] <= kj) ++r;
-              w[j] = __ldg(ci + g_st[r] + kj);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (w[j] >= 0) inc(w[j] - lo);
-        }
-        __syncthreads();
+      // ---- count pass: giant rows (warp per row, 16-byte loads, largest
+      // first), then long-row batches, then short rows
+      while (true) {
+        int gi = 0;
+        if (lane == 0) gi = atomicAdd(next_giant, 1);
+        gi = __shfl_sync(0xffffffffu, gi, 0);
+        const int q = nq - 1 - gi;
+        if (q < qg) break;
+        const int st = cur[q];
+        const int em = mir[b + q];
+        const int se = hi >= u ? em : warp_lower_bound(ci, st, em, hi);
+        if (lane == 0) segend[q] = se;
+        warp_for_each(ci, st, se, [&](int w) { inc(w - lo); });
       }
       for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
@@ -494,50 +514,21 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         }
       }
       // ---- attribution pass: c4[v] += sum (L[w] - 1); cursors advance
-      __syncthreads();
-      for (int g0 = qg; g0 < nq; g0 += blockDim.x) {
-        const int q = g0 + threadIdx.x;
-        const bool valid = q < nq;
-        const int st = valid ? cur[q] : 0;
-        const int se = valid ? segend[q] : 0;
-        g_sum[threadIdx.x] = 0;
-        const int T = block_flatten(se - st, st, g_off, g_st, wtot);
-        const int nwarp = blockDim.x >> 5;
-        const int per = (((T + nwarp - 1) / nwarp) + 31) & ~31;
-        const int k0 = wid * per, k1 = min(T, k0 + per);
-        int r = k0 + lane < k1 ? upper_row(g_off, k0 + lane, blockDim.x) : 0;
-        int cr = r;  // row that `part` accumulates for
-        u64 part = 0;
-        for (int kk = k0 + lane; kk < k1; kk += 128) {  // 4 independent loads in flight
-          int w[4], rr[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int kj = kk + 32 * j;
-            w[j] = -1;
-            if (kj < k1) {
-              while (g_off[r + 1] <= kj) ++r;
-              rr[j] = r;
-              w[j] = __ldg(ci + g_st[r] + kj);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (w[j] < 0) break;
-            if (rr[j] != cr) {
-              if (part) smem_add_u64(g_sum + cr, part);
-              part = 0;
-              cr = rr[j];
-            }
-            part += get(w[j] - lo) - 1;
-          }
-        }
-        if (part) smem_add_u64(g_sum + cr, part);
-        __syncthreads();
-        if (valid) {
-          if (g_sum[threadIdx.x]) atomicAdd(c4 + ci[b + q], g_sum[threadIdx.x]);
+      while (true) {
+        int gi = 0;
+        if (lane == 0) gi = atomicAdd(next_giant + 1, 1);
+        gi = __shfl_sync(0xffffffffu, gi, 0);
+        const int q = nq - 1 - gi;
+        if (q < qg) break;
+        const int st = cur[q];
+        const int se = segend[q];
+        u64 sv = 0;
+        warp_for_each(ci, st, se, [&](int w) { sv += get(w - lo) - 1; });
+        sv = warp_sum_u64(sv);
+        if (lane == 0) {
+          if (sv) atomicAdd(c4 + ci[b + q], sv);
           cur[q] = se;
         }
-        __syncthreads();
       }
       for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
@@ -623,11 +614,13 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
 // kernels.cpp:234-288, same counts).
 
 // Warp per root, |S| <= 32: rows are single words.
-template <bool kD13, bool kD15>
+template <bool kC3, bool kD13, bool kD15>
 __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__ ci,
-                             const int* __restrict__ split, const u32* __restrict__ C3f,
+                             const int* __restrict__ split, u32* __restrict__ C3f,
                              const int* __restrict__ roots, int nroots,
                              u64* __restrict__ d13, u64* __restrict__ d15) {
+  // kC3: per-edge triangle counts (atomics into C3f) — the triangle pass.
+  // kD13: diamonds from the final C3 — a later pass (needs complete C3).
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -644,6 +637,7 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
       sS[lane] = ci[s0 + lane];
       if (kD13) sC[lane] = C3f[s0 + lane];
     }
+    if (kC3) sC[lane] = 0;
     sD[lane] = 0;
     rows[lane] = 0;
     __syncwarp();
@@ -654,6 +648,7 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
       const u32 ca = kD13 ? sC[a] : 0u;
       const int e = rp[x + 1];
       u64 da = 0;
+      u32 na = 0;
       for (int base = split[x]; base < e; base += 32) {
         const int p = base + lane;
         const int y = p < e ? ci[p] : 0x7fffffff;
@@ -664,6 +659,11 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
               atomicOr(rows + a, 1u << bi);
               atomicOr(rows + bi, 1u << a);
             }
+            if (kC3) {
+              atomicAdd(C3f + p, 1u);
+              atomicAdd(sC + bi, 1u);
+              ++na;
+            }
             if (kD13) {
               tu += (u64)C3f[p] - 1;
               da += (u64)sC[bi] - 1;
@@ -673,12 +673,18 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
         }
         if (__any_sync(0xffffffffu, y >= smax)) break;
       }
+      if (kC3) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
+        if (lane == 0 && na) atomicAdd(sC + a, na);
+      }
       if (kD13) {
         da = warp_sum_u64(da);
         if (lane == 0 && da) smem_add_u64(sD + a, da);
       }
     }
     __syncwarp();
+    if (kC3 && lane < s && sC[lane]) atomicAdd(C3f + s0 + lane, sC[lane]);
     if (kD13) {
       if (lane < s && sD[lane]) atomicAdd(d13 + sS[lane], sD[lane]);
       tu = warp_sum_u64(tu);
@@ -736,10 +742,10 @@ __device__ __forceinline__ int s_hash_find(const int* keys, const unsigned short
   }
 }
 
-template <bool kD13, bool kD15, bool kGlobal>
+template <bool kC3, bool kD13, bool kD15, bool kGlobal>
 __global__ void __launch_bounds__(256)
 k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
-              const int* __restrict__ split, const u32* __restrict__ C3f,
+              const int* __restrict__ split, u32* __restrict__ C3f,
               const int* __restrict__ roots, int nroots, RootsLayout L,
               unsigned char* __restrict__ slab, long long slab_stride,
               u64* __restrict__ d13, u64* __restrict__ d15) {
@@ -776,6 +782,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     for (int a = threadIdx.x; a < s; a += blockDim.x) {
       sS[a] = ci[s0 + a];
       if (kD13) { sC[a] = C3f[s0 + a]; sD[a] = 0; }
+      if (kC3) sC[a] = 0;  // per-(u, S[a]) triangle counts
     }
     for (int i = threadIdx.x; i < hcap; i += blockDim.x) hkeys[i] = -1;
     if (kD15)
@@ -801,6 +808,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
       const u32 ca = kD13 ? sC[a] : 0u;
       const int e = rp[x + 1];
       u64 da = 0;
+      u32 na = 0;
       for (int base = split[x]; base < e; base += 32) {
         const int p = base + lane;
         const int y = p < e ? __ldg(ci + p) : 0x7fffffff;
@@ -812,6 +820,11 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
               atomicOr(bm + (long long)a * stride + (bi >> 5), 1u << (bi & 31));
               atomicOr(bm + (long long)bi * stride + (a >> 5), 1u << (a & 31));
             }
+            if (kC3) {
+              atomicAdd(C3f + p, 1u);
+              atomicAdd(sC + bi, 1u);
+              ++na;
+            }
             if (kD13) {
               tu += (u64)__ldg(C3f + p) - 1;
               da += (u64)sC[bi] - 1;
@@ -821,12 +834,20 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         }
         if (__any_sync(0xffffffffu, y >= smax)) break;
       }
+      if (kC3) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
+        if (lane == 0 && na) atomicAdd(sC + a, na);
+      }
       if (kD13) {
         da = warp_sum_u64(da);
         if (lane == 0 && da) smem_add_u64(sD + a, da);
       }
     }
     __syncthreads();
+    if (kC3)
+      for (int a = threadIdx.x; a < s; a += blockDim.x)
+        if (sC[a]) atomicAdd(C3f + s0 + a, sC[a]);
     if (kD13) {
       for (int a = threadIdx.x; a < s; a += blockDim.x)
         if (sD[a]) atomicAdd(d13 + sS[a], sD[a]);
