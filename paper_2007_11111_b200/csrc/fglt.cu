@@ -515,7 +515,7 @@ void roots_pass(fglt_ctx* c) {
   int** lists = c->rb_lists;
   if (cnt[0] > 0) {
     const int wpb = 8;
-    const size_t sm = (size_t)wpb * (32 * 8 + 96 * 4);
+    const size_t sm = (size_t)wpb * (32 * 8 + 161 * 4);
     const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
     k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f,
                                                                   lists[0], cnt[0], d13, d15);
@@ -588,9 +588,9 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     u64* c4 = c->V(V_C4);
     if (cnt[0] > 0) {
       const int wpb = 8;
-      const size_t sm = (size_t)wpb * (1 << kWarpHashLog) * 8;
+      const size_t sm = (size_t)wpb * ((1 << kWarpHashLog) * 2 + 97) * 4;
       k_c4_warp<kWarpHashLog><<<c->grid((int64_t)cnt[0] * 32, wpb * 32), wpb * 32, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->mir, lists[0], cnt[0], c4);
+          c->rp, c->ci, c->split, c->mir, lists[0], cnt[0], wc, c4);
       check_launch();
       c->launched();
     }

@@ -87,30 +87,56 @@ __device__ __forceinline__ u32 hash_get(const int* keys, const u32* vals, int lo
 }
 
 // Warp per root; a 2^LOGCAP-slot table per warp in shared memory.
+// Warp per root (wc <= 256): a table of 2^hlog <= 2^LOGCAP slots sized to the
+// root; the rows of N-(u) are walked 32 at a time with segment flattening so
+// every lane streams one wedge per step.
 template <int LOGCAP>
 __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci,
                           const int* __restrict__ split, const int* __restrict__ mir,
-                          const int* __restrict__ roots, int nroots, u64* __restrict__ c4) {
+                          const int* __restrict__ roots, int nroots, const u64* __restrict__ wcv,
+                          u64* __restrict__ c4) {
   constexpr int CAP = 1 << LOGCAP;
+  constexpr int PER_WARP = CAP * 2 + 32 + 33 + 32;  // keys, vals, base, off, rowsum
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  int* keys = reinterpret_cast<int*>(smem_raw) + wib * CAP * 2;
+  int* keys = reinterpret_cast<int*>(smem_raw) + wib * PER_WARP;
   u32* vals = reinterpret_cast<u32*>(keys + CAP);
+  int* fbase = reinterpret_cast<int*>(vals + CAP);
+  int* foff = fbase + 32;
+  u32* rs = reinterpret_cast<u32*>(foff + 33);
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
     const int u = roots[k];
-    for (int i = lane; i < CAP; i += 32) { keys[i] = -1; vals[i] = 0; }
+    int hlog = 5;
+    while (hlog < LOGCAP && ((u64)1 << hlog) < 2 * wcv[u]) ++hlog;
+    const int cap = 1 << hlog;
+    for (int i = lane; i < cap; i += 32) { keys[i] = -1; vals[i] = 0; }
+    rs[lane] = 0;
     __syncwarp();
     const int b = rp[u], s = split[u];
-    for (int q = b; q < s; ++q) {
-      const int v = ci[q];
-      const int end = mir[q];
-      for (int p = rp[v] + lane; p < end; p += 32) hash_insert(keys, vals, LOGCAP, ci[p]);
+    for (int q0 = b; q0 < s; q0 += 32) {
+      const int q = q0 + lane;
+      int st = 0, len = 0;
+      if (q < s) {
+        st = rp[ci[q]];
+        len = mir[q] - st;
+      }
+      int T;
+      const int off = flat_prefix(len, &T);
+      fbase[lane] = st - off;
+      foff[lane] = off;
+      if (lane == 0) foff[32] = T;
+      __syncwarp();
+      int r = 0;
+      for (int kk = lane; kk < T; kk += 32) {
+        while (foff[r + 1] <= kk) ++r;
+        hash_insert(keys, vals, hlog, __ldg(ci + fbase[r] + kk));
+      }
+      __syncwarp();
     }
-    __syncwarp();
     u64 acc = 0;
-    for (int i = lane; i < CAP; i += 32) {
+    for (int i = lane; i < cap; i += 32) {
       const u32 l = vals[i];
       if (l >= 2) {
         const u64 c = (u64)l * (l - 1) / 2;
@@ -118,13 +144,35 @@ __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci
         atomicAdd(c4 + keys[i], c);
       }
     }
-    for (int q = b; q < s; ++q) {
-      const int v = ci[q];
-      const int end = mir[q];
-      u64 sv = 0;
-      for (int p = rp[v] + lane; p < end; p += 32) sv += hash_get(keys, vals, LOGCAP, ci[p]) - 1;
-      sv = warp_sum_u64(sv);
-      if (lane == 0 && sv) atomicAdd(c4 + v, sv);
+    for (int q0 = b; q0 < s; q0 += 32) {
+      const int q = q0 + lane;
+      int st = 0, len = 0;
+      if (q < s) {
+        st = rp[ci[q]];
+        len = mir[q] - st;
+      }
+      int T;
+      const int off = flat_prefix(len, &T);
+      fbase[lane] = st - off;
+      foff[lane] = off;
+      if (lane == 0) foff[32] = T;
+      __syncwarp();
+      int r = 0, cr = 0;
+      u32 part = 0;
+      for (int kk = lane; kk < T; kk += 32) {
+        while (foff[r + 1] <= kk) ++r;
+        if (r != cr) {
+          if (part) atomicAdd(rs + cr, part);
+          part = 0;
+          cr = r;
+        }
+        part += hash_get(keys, vals, hlog, __ldg(ci + fbase[r] + kk)) - 1;
+      }
+      if (part) atomicAdd(rs + cr, part);
+      __syncwarp();
+      if (q < s && rs[lane]) atomicAdd(c4 + ci[q], (u64)rs[lane]);
+      rs[lane] = 0;
+      __syncwarp();
     }
     acc = warp_sum_u64(acc);
     if (lane == 0 && acc) atomicAdd(c4 + u, acc);
@@ -625,9 +673,11 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   u64* sD = reinterpret_cast<u64*>(smem_raw) + wib * 32;
-  int* sS = reinterpret_cast<int*>(reinterpret_cast<u64*>(smem_raw) + (blockDim.x >> 5) * 32) + wib * 96;
+  int* sS = reinterpret_cast<int*>(reinterpret_cast<u64*>(smem_raw) + (blockDim.x >> 5) * 32) + wib * 161;
   u32* sC = reinterpret_cast<u32*>(sS + 32);
   u32* rows = sC + 32;
+  int* fbase = reinterpret_cast<int*>(rows + 32);  // per-warp flattening tables
+  int* foff = fbase + 32;                           // 33 entries
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
     const int u = roots[k];
@@ -643,46 +693,54 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
     __syncwarp();
     const int smax = sS[s - 1];
     u64 tu = 0;
-    for (int a = 0; a + 1 < s; ++a) {
-      const int x = sS[a];
-      const u32 ca = kD13 ? sC[a] : 0u;
-      const int e = rp[x + 1];
-      u64 da = 0;
-      u32 na = 0;
-      for (int base = split[x]; base < e; base += 32) {
-        const int p = base + lane;
-        const int y = p < e ? ci[p] : 0x7fffffff;
-        if (y <= smax) {
-          const int bi = lower_bound_smem(sS, a + 1, s, y);
-          if (bi < s && sS[bi] == y) {
-            if (kD15) {
-              atomicOr(rows + a, 1u << bi);
-              atomicOr(rows + bi, 1u << a);
-            }
-            if (kC3) {
-              atomicAdd(C3f + p, 1u);
-              atomicAdd(sC + bi, 1u);
-              ++na;
-            }
-            if (kD13) {
-              tu += (u64)C3f[p] - 1;
-              da += (u64)sC[bi] - 1;
-              smem_add_u64(sD + bi, (u64)ca - 1);
-            }
-          }
+    // Flatten the probe lists N+(S[a]) (cut at max S) of all members: lane a
+    // sets up its segment, then every lane streams one element per step.
+    int st = 0, len = 0;
+    if (lane + 1 < s) {
+      const int x = sS[lane];
+      st = split[x];
+      len = lower_bound_i32(ci, st, rp[x + 1], smax + 1) - st;
+    }
+    int T;
+    const int off = flat_prefix(len, &T);
+    fbase[lane] = st - off;
+    foff[lane] = off;
+    if (lane == 0) foff[32] = T;
+    __syncwarp();
+    int r = 0, cr = 0;
+    u64 da = 0;
+    u32 na = 0;
+    for (int kk = lane; kk < T; kk += 32) {
+      while (foff[r + 1] <= kk) ++r;
+      if (r != cr) {  // flush the per-member partials of row cr
+        if (kC3 && na) atomicAdd(sC + cr, na);
+        if (kD13 && da) smem_add_u64(sD + cr, da);
+        na = 0;
+        da = 0;
+        cr = r;
+      }
+      const int p = fbase[r] + kk;
+      const int y = __ldg(ci + p);
+      const int bi = lower_bound_smem(sS, r + 1, s, y);
+      if (bi < s && sS[bi] == y) {
+        if (kD15) {
+          atomicOr(rows + r, 1u << bi);
+          atomicOr(rows + bi, 1u << r);
         }
-        if (__any_sync(0xffffffffu, y >= smax)) break;
-      }
-      if (kC3) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
-        if (lane == 0 && na) atomicAdd(sC + a, na);
-      }
-      if (kD13) {
-        da = warp_sum_u64(da);
-        if (lane == 0 && da) smem_add_u64(sD + a, da);
+        if (kC3) {
+          atomicAdd(C3f + p, 1u);
+          atomicAdd(sC + bi, 1u);
+          ++na;
+        }
+        if (kD13) {
+          tu += (u64)__ldg(C3f + p) - 1;
+          da += (u64)sC[bi] - 1;
+          smem_add_u64(sD + bi, (u64)sC[r] - 1);
+        }
       }
     }
+    if (kC3 && na) atomicAdd(sC + cr, na);
+    if (kD13 && da) smem_add_u64(sD + cr, da);
     __syncwarp();
     if (kC3 && lane < s && sC[lane]) atomicAdd(C3f + s0 + lane, sC[lane]);
     if (kD13) {
@@ -1107,13 +1165,29 @@ __global__ void k_graph_stats(const int* __restrict__ rp, int n, u64* __restrict
 __global__ void k_bin(const u64* __restrict__ key, int u0, int u1, const u64* __restrict__ thr,
                       int nbins, int* __restrict__ counts, int* __restrict__ lists,
                       long long list_stride) {
-  for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1; u += gridDim.x * blockDim.x) {
-    const u64 x = key[u];
-    if (x == 0) continue;
-    int b = 0;
-    while (b + 1 < nbins && x > thr[b]) ++b;
-    const int slot = atomicAdd(counts + b, 1);
-    lists[(long long)b * list_stride + slot] = u;
+  // warp-aggregated: one atomic per (warp, bin) instead of one per root
+  const int lane = threadIdx.x & 31;
+  const int span = u1 - u0;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i0 = (blockIdx.x * blockDim.x + threadIdx.x) - lane; i0 < span; i0 += stride) {
+    const int i = i0 + lane;
+    int b = -1;
+    if (i < span) {
+      const u64 x = key[u0 + i];
+      if (x != 0) {
+        b = 0;
+        while (b + 1 < nbins && x > thr[b]) ++b;
+      }
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, b);
+    if (b >= 0) {
+      const int leader = __ffs(peers) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(counts + b, __popc(peers));
+      base = __shfl_sync(peers, base, leader);
+      const int rank = __popc(peers & ((1u << lane) - 1));
+      lists[(long long)b * list_stride + base + rank] = u0 + i;
+    }
   }
 }
 
