@@ -333,3 +333,15 @@ def test_sharded_stages_byte_identical(ctx):
         assert rc == 0, err
         np.testing.assert_array_equal(raw.cpu().numpy().view(np.uint64), want_raw)
         np.testing.assert_array_equal(net.cpu().numpy().view(np.uint64), want_net)
+
+
+@pytest.mark.parametrize("cfg", [2, 5, 3])
+def test_full_size_config_parity(ctx, cfg):
+    """BASELINE.json configs 2 (RGG 2M), 5 (SBM 4.2M) and 3 (R-MAT scale 20)
+    at full size, every raw and net entry against the oracle (d15 by the
+    oriented K4 counter, pinned to the reference's compute_d15)."""
+    name, rp, ci = graphs.config(cfg)
+    raw, net, _ = ctx.transform_host(rp, ci)
+    oraw, onet = ob.transform(rp, ci, FULL, False, 1)
+    assert np.array_equal(raw, oraw), name
+    assert np.array_equal(net, onet), name
