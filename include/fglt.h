@@ -110,6 +110,21 @@ int fglt_net_from_raw(fglt_ctx* ctx, const uint64_t* raw, int64_t n,
                       uint32_t dict_mask, int lenient, uint64_t* net,
                       fglt_error* err);
 
+/* ------------------------------------------------------------------ ingest
+ * Device CSR ingest replacing build_adjacency (src/graph.cpp:192-249):
+ * (eu[i], ev[i]) undirected pairs (int64, host pointers unless
+ * FGLT_INPUT_DEVICE), declared_n (0 = max id + 1), SanitizeOptions
+ * (graph.hpp:32-36). Mirrors when symmetrize, drops self-loops (else
+ * StructuralError), sorts, dedupes (else StructuralError), checks symmetry
+ * when not symmetrizing. The CSR stays in the context; fetch it with
+ * fglt_csr_fetch (n+1 and nnz int32 entries). */
+int fglt_build_csr(fglt_ctx* ctx, const int64_t* eu, const int64_t* ev, int64_t ne,
+                   int64_t declared_n, int symmetrize, int drop_self_loops, int dedupe,
+                   uint32_t flags, int64_t* n_out, int64_t* nnz_out, int64_t* self_loops,
+                   int64_t* duplicates, fglt_error* err);
+int fglt_csr_fetch(fglt_ctx* ctx, int32_t* row_ptr, int32_t* col_idx, uint32_t flags,
+                   fglt_error* err);
+
 /* ------------------------------------------------------------------ staged
  * Row-block sharding across ranks (one process per GPU; the caller owns the
  * collectives, e.g. torch.distributed over NCCL). Sequence per rank:

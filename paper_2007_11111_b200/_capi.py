@@ -24,7 +24,8 @@ EXPORTS = [
     "fglt_ctx_create", "fglt_ctx_destroy", "fglt_ctx_transform", "fglt_transform_csr32",
     "fglt_net_from_raw", "fglt_stage_prepare", "fglt_stage_bounds", "fglt_stage_triangles",
     "fglt_stage_local", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
-    "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug",
+    "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug", "fglt_build_csr",
+    "fglt_csr_fetch",
 ]
 
 DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN = 1, 2, 3
@@ -105,6 +106,12 @@ def lib():
         L.fglt_stage_epilogue.restype = ctypes.c_int
         L.fglt_stage_epilogue.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, vp, vp,
                                           ctypes.POINTER(FgltError)]
+        L.fglt_build_csr.restype = ctypes.c_int
+        L.fglt_build_csr.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_uint32, vp, vp, vp, vp,
+                                     ctypes.POINTER(FgltError)]
+        L.fglt_csr_fetch.restype = ctypes.c_int
+        L.fglt_csr_fetch.argtypes = [vp, vp, vp, ctypes.c_uint32, ctypes.POINTER(FgltError)]
         L.fglt_ctx_set_debug.restype = ctypes.c_int
         L.fglt_ctx_set_debug.argtypes = [vp, ctypes.c_int, ctypes.c_int]
         L.fglt_ctx_kernel_launches.restype = ctypes.c_uint64
@@ -151,6 +158,27 @@ class Context:
         self._h = self._L.fglt_ctx_create(device, ctypes.c_void_p(stream), ctypes.byref(err))
         if not self._h:
             _raise(err.code, err)
+
+    def build_csr(self, eu, ev, n: int = 0, symmetrize=True, drop_self_loops=True, dedupe=True):
+        """Device ingest (fglt_build_csr): undirected pairs -> sanitised int32 CSR."""
+        eu = np.ascontiguousarray(eu, dtype=np.int64)
+        ev = np.ascontiguousarray(ev, dtype=np.int64)
+        out = np.zeros(4, dtype=np.int64)
+        err = FgltError()
+        rc = self._L.fglt_build_csr(self._h, eu.ctypes.data, ev.ctypes.data, len(eu), n,
+                                    int(symmetrize), int(drop_self_loops), int(dedupe), 0,
+                                    out[0:].ctypes.data, out[1:].ctypes.data,
+                                    out[2:].ctypes.data, out[3:].ctypes.data, ctypes.byref(err))
+        if rc:
+            _raise(rc, err)
+        n_out, nnz = int(out[0]), int(out[1])
+        rp = np.empty(n_out + 1, dtype=np.int32)
+        ci = np.empty(nnz, dtype=np.int32)
+        rc = self._L.fglt_csr_fetch(self._h, rp.ctypes.data, ci.ctypes.data if nnz else None, 0,
+                                    ctypes.byref(err))
+        if rc:
+            _raise(rc, err)
+        return rp, ci, {"self_loops_dropped": int(out[2]), "duplicates_merged": int(out[3])}
 
     def set_debug(self, key: int, value: int):
         rc = self._L.fglt_ctx_set_debug(self._h, key, value)

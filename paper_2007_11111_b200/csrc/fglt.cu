@@ -27,6 +27,7 @@
 #include "../../include/fglt.h"
 #include "fglt_device.cuh"
 #include "fglt_roots.cuh"
+#include "fglt_ingest.cuh"
 
 using namespace fglt;
 
@@ -60,7 +61,8 @@ constexpr int kWarpHashLog = 9;   // 512-slot table per warp
 enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
-  B_CUB, B_CURSOR, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY, B_COUNT
+  B_CUB, B_CURSOR, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
+  B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_COUNT
 };
 
 struct DevBuf {
@@ -197,6 +199,9 @@ struct fglt_ctx {
   u64* d_small = nullptr;  // [0] err key, [1] W, [2] d_max, [3..] bin counts
   bool have_stats = false;
   uint64_t W = 0, dmax = 0, maxout = 0;
+
+  // last ingest result (fglt_build_csr), on the device
+  int64_t ing_n = 0, ing_nnz = 0;
 
   // root bins by |N+(u)| (shared by the triangle and diamond passes)
   int64_t rb_u0 = -1, rb_u1 = -1;
@@ -769,6 +774,149 @@ int validate_shape(int64_t n, int64_t nnz, fglt_error* err) {
 extern "C" {
 
 uint64_t fglt_ctx_kernel_launches(const fglt_ctx* c) { return c ? c->launches : 0; }
+
+int fglt_build_csr(fglt_ctx* c, const int64_t* eu, const int64_t* ev, int64_t ne,
+                   int64_t declared_n, int symmetrize, int drop_self_loops, int dedupe,
+                   uint32_t flags, int64_t* n_out, int64_t* nnz_out, int64_t* self_loops,
+                   int64_t* duplicates, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!c) {
+    set_err(err, FGLT_E_NO_DEVICE, -1, -1, "null context");
+    return FGLT_E_NO_DEVICE;
+  }
+  try {
+    CK(cudaSetDevice(c->device));
+    if (ne < 0 || declared_n < 0) {
+      set_err(err, FGLT_E_STRUCTURAL, -1, -1, "negative size");
+      return FGLT_E_STRUCTURAL;
+    }
+    if (2 * ne >= ((int64_t)1 << 31)) {
+      set_err(err, FGLT_E_STRUCTURAL, -1, -1, "edge sample exceeds the int32 CSR limits");
+      return FGLT_E_STRUCTURAL;
+    }
+    const bool mirror = symmetrize != 0;
+    long long* de = c->ensure<long long>(B_ING_E, 2 * (size_t)std::max<int64_t>(ne, 1));
+    const long long* du = reinterpret_cast<const long long*>(eu);
+    const long long* dv = reinterpret_cast<const long long*>(ev);
+    if (!(flags & FGLT_INPUT_DEVICE) && ne > 0) {
+      CK(cudaMemcpyAsync(de, eu, (size_t)ne * 8, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(de + ne, ev, (size_t)ne * 8, cudaMemcpyHostToDevice, c->stream));
+      du = de;
+      dv = de + ne;
+    }
+    c->d_small = c->ensure<u64>(B_SMALL, 64);
+    CK(cudaMemsetAsync(c->d_small + 40, 0, 8 * sizeof(u64), c->stream));
+    u64 h[3] = {0, 0, 0};
+    if (ne > 0) {
+      k_ingest_scan<<<c->grid(ne, 256), 256, 0, c->stream>>>(du, dv, ne, c->d_small + 40);
+      check_launch();
+      c->launched();
+      CK(cudaMemcpyAsync(h, c->d_small + 40, 24, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    if (h[0]) {
+      set_err(err, FGLT_E_STRUCTURAL, -1, -1, "negative vertex id in edge collection");
+      return FGLT_E_STRUCTURAL;
+    }
+    if (h[1] && !drop_self_loops) {
+      set_err(err, FGLT_E_STRUCTURAL, -1, -1, "self-loop present (drop_self_loops is off)");
+      return FGLT_E_STRUCTURAL;
+    }
+    const int64_t n = std::max<int64_t>(declared_n, ne > 0 ? (int64_t)h[2] + 1 : 0);
+    if (n >= ((int64_t)1 << 31)) {
+      set_err(err, FGLT_E_STRUCTURAL, -1, -1, "vertex ids exceed the int32 CSR limits");
+      return FGLT_E_STRUCTURAL;
+    }
+    const int64_t nk = 2 * ne;
+    u64* keys = c->ensure<u64>(B_ING_K, (size_t)std::max<int64_t>(nk, 1));
+    u64* sorted = c->ensure<u64>(B_ING_K2, (size_t)std::max<int64_t>(nk, 1));
+    int64_t nnz = 0;
+    u64 dups = 0;
+    if (ne > 0) {
+      k_ingest_keys<<<c->grid(ne, 256), 256, 0, c->stream>>>(du, dv, ne, mirror ? 1 : 0, keys);
+      check_launch();
+      c->launched();
+      int bits = 1;
+      while (bits < 32 && ((int64_t)1 << bits) <= n) ++bits;
+      size_t t1 = 0, t2 = 0;
+      int* d_nsel = reinterpret_cast<int*>(c->d_small + 48);
+      CK(cub::DeviceRadixSort::SortKeys(nullptr, t1, keys, sorted, (int)nk, 0, 64, c->stream));
+      CK(cub::DeviceSelect::Unique(nullptr, t2, sorted, keys, d_nsel, (int)nk, c->stream));
+      void* tmp = c->ensure<unsigned char>(B_CUB, std::max(t1, t2));
+      size_t tb = c->buf[B_CUB].cap;
+      // sentinels (~0) need the full 64 bits to sort last
+      CK(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, (int)nk, 0, 64, c->stream));
+      c->launched();
+      tb = c->buf[B_CUB].cap;
+      CK(cub::DeviceSelect::Unique(tmp, tb, sorted, keys, d_nsel, (int)nk, c->stream));
+      c->launched();
+      int nsel = 0;
+      u64 last = 0;
+      CK(cudaMemcpyAsync(&nsel, d_nsel, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (nsel > 0)
+        CK(cudaMemcpyAsync(&last, keys + nsel - 1, 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      nnz = nsel - (nsel > 0 && last == ~0ull ? 1 : 0);
+      const int64_t valid = (mirror ? 2 : 1) * (ne - (int64_t)h[1]);
+      dups = (u64)(valid - nnz);
+      if (dups && !dedupe) {
+        set_err(err, FGLT_E_STRUCTURAL, -1, -1, "duplicate edges present (dedupe is off)");
+        return FGLT_E_STRUCTURAL;
+      }
+    }
+    int* rp = c->ensure<int>(B_ING_RP, (size_t)n + 1);
+    int* ci = c->ensure<int>(B_ING_CI, (size_t)std::max<int64_t>(nnz, 1));
+    k_ingest_rows<<<c->grid(nnz + 1, 256), 256, 0, c->stream>>>(keys, nnz, (int)n, rp, ci);
+    check_launch();
+    c->launched();
+    if (!mirror && nnz > 0) {
+      u64 init = ~0ull, bad = ~0ull;
+      CK(cudaMemcpyAsync(c->d_small + 41, &init, 8, cudaMemcpyHostToDevice, c->stream));
+      k_ingest_symmetric<<<c->grid(n, 256), 256, 0, c->stream>>>(rp, ci, (int)n, c->d_small + 41);
+      check_launch();
+      c->launched();
+      CK(cudaMemcpyAsync(&bad, c->d_small + 41, 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (bad != ~0ull) {
+        set_err(err, FGLT_E_STRUCTURAL, -1, (int64_t)(bad >> 32),
+                "asymmetric input: (%lld,%lld) present without its reverse and symmetrize off",
+                (long long)(bad >> 32), (long long)(bad & 0xffffffffull));
+        return FGLT_E_STRUCTURAL;
+      }
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->ing_n = n;
+    c->ing_nnz = nnz;
+    if (n_out) *n_out = n;
+    if (nnz_out) *nnz_out = nnz;
+    if (self_loops) *self_loops = (int64_t)h[1];
+    if (duplicates) *duplicates = (int64_t)(mirror ? dups / 2 : dups);
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+int fglt_csr_fetch(fglt_ctx* c, int32_t* row_ptr, int32_t* col_idx, uint32_t flags,
+                   fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  try {
+    CK(cudaSetDevice(c->device));
+    const cudaMemcpyKind kind =
+        (flags & FGLT_OUTPUT_DEVICE) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (row_ptr)
+      CK(cudaMemcpyAsync(row_ptr, c->buf[B_ING_RP].p, (size_t)(c->ing_n + 1) * 4, kind, c->stream));
+    if (col_idx && c->ing_nnz)
+      CK(cudaMemcpyAsync(col_idx, c->buf[B_ING_CI].p, (size_t)c->ing_nnz * 4, kind, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
 
 int fglt_ctx_set_debug(fglt_ctx* c, int key, int value) {
   if (!c) return FGLT_E_NO_DEVICE;

@@ -345,7 +345,18 @@ EdgeCollection parse_matrix_market(std::istream& in) {
   return ec;
 }
 
+namespace {
+bool device_ingest(const EdgeCollection& ec, const SanitizeOptions& opt, BuildResult* out);
+}  // namespace
+
 BuildResult build_adjacency(const EdgeCollection& ec, const SanitizeOptions& opt) {
+  // Large inputs are sanitised on the device (fglt_build_csr); small ones, or a
+  // machine without a CUDA device, use the host sort below (ingest only —
+  // graphlet counting itself has no host path).
+  {
+    BuildResult dev;
+    if (device_ingest(ec, opt, &dev)) return dev;
+  }
   vertex_t n = ec.declared_n.value_or(0);
   for (const auto& [u, v] : ec.edges) {
     if (u < 0 || v < 0) throw StructuralError("negative vertex id in edge collection");
@@ -487,6 +498,7 @@ namespace {
 
 std::mutex g_ctx_mu;
 std::map<int, fglt_ctx*> g_ctx;
+std::mutex g_run_mu;  // one device call per context at a time
 
 fglt_ctx* context_for(int device) {
   std::lock_guard<std::mutex> lock(g_ctx_mu);
@@ -497,6 +509,33 @@ fglt_ctx* context_for(int device) {
   if (!c) throw Error(std::string("CUDA device unavailable: ") + err.msg);
   g_ctx[device] = c;
   return c;
+}
+
+[[noreturn]] void rethrow(int rc, const fglt_error& e);
+
+bool device_ingest(const EdgeCollection& ec, const SanitizeOptions& opt, BuildResult* out) {
+  if (ec.edges.size() < (std::size_t{1} << 16) || fglt_device_count() == 0) return false;
+  fglt_ctx* ctx = context_for(0);
+  std::vector<std::int64_t> eu(ec.edges.size()), ev(ec.edges.size());
+  for (std::size_t i = 0; i < ec.edges.size(); ++i) {
+    eu[i] = ec.edges[i].first;
+    ev[i] = ec.edges[i].second;
+  }
+  std::int64_t n = 0, nnz = 0, loops = 0, dups = 0;
+  fglt_error err{};
+  std::lock_guard<std::mutex> lock(g_run_mu);
+  int rc = fglt_build_csr(ctx, eu.data(), ev.data(), static_cast<std::int64_t>(eu.size()),
+                          ec.declared_n.value_or(0), opt.symmetrize || ec.declared_symmetric(),
+                          opt.drop_self_loops, opt.dedupe, 0, &n, &nnz, &loops, &dups, &err);
+  if (rc) rethrow(rc, err);
+  std::vector<std::int32_t> rp(static_cast<std::size_t>(n) + 1), ci(static_cast<std::size_t>(nnz));
+  rc = fglt_csr_fetch(ctx, rp.data(), ci.data(), 0, &err);
+  if (rc) rethrow(rc, err);
+  out->graph = SparseAdjacency(std::vector<std::int64_t>(rp.begin(), rp.end()),
+                               std::vector<vertex_t>(ci.begin(), ci.end()));
+  out->report.self_loops_dropped = static_cast<count_t>(loops);
+  out->report.duplicates_merged = static_cast<count_t>(dups);
+  return true;
 }
 
 [[noreturn]] void rethrow(int rc, const fglt_error& e) {
@@ -521,7 +560,6 @@ TransformStats stats_of(const fglt_stats& s) {
   return t;
 }
 
-std::mutex g_run_mu;  // one transform per context at a time
 
 void run(const SparseAdjacency& g, const Dictionary& dict, bool lenient, int device,
          count_t* raw, count_t* net, TransformStats* stats) {
