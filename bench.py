@@ -314,6 +314,23 @@ def main():
     dom = max(phases.items(), key=lambda kv: kv[1]) if phases else (None, None)
     traffic, traffic_src = ncu_traffic(args.config)
 
+    # device ingest: raw edge sample -> sanitised CSR
+    ingest = None
+    if world == 1 and args.config in (3, 4):
+        from paper_2007_11111_b200 import graphs as _g
+        scale = 20 if args.config == 3 else 23
+        eu, ev = _g._two_pass(_g._lib().fglt_gen_rmat, scale, 16, 0.57, 0.19, 0.19, 1)
+        ctx.build_csr(eu, ev, 1 << scale)  # warm-up
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            irp, ici, _rep = ctx.build_csr(eu, ev, 1 << scale)
+            ts.append(time.perf_counter() - t0)
+        assert np.array_equal(irp, rp_h) and np.array_equal(ici, ci_h)
+        ingest = {"edges_in": int(len(eu)), "ms": min(ts) * 1e3,
+                  "what": "fglt_build_csr: host int64 pairs -> H2D, mirror, radix sort, unique, "
+                          "row offsets, D2H CSR (wall clock, best of 3)"}
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_leg()
@@ -344,6 +361,7 @@ def main():
                                         "share": dom[1] / t_ms if dom[1] else None},
                      "phases_ms": phases},
         "cpu_baseline": cpu,
+        "ingest": ingest,
         "gpu_launches": launches,
         "clocks": clk,
     }
