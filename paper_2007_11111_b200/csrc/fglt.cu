@@ -62,7 +62,7 @@ enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
   B_CUB, B_CURSOR, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
-  B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_COUNT
+  B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_COUNT
 };
 
 struct DevBuf {
@@ -189,6 +189,7 @@ struct fglt_ctx {
   int* perm = nullptr;
   int* inv = nullptr;
   int* split = nullptr;
+  int* send = nullptr;  // end of the active part of N+(u)
   int* orp = nullptr;
   int* mir = nullptr;
   int* ce_row = nullptr;
@@ -198,7 +199,7 @@ struct fglt_ctx {
   DictInfo* d_dict = nullptr;
   u64* d_small = nullptr;  // [0] err key, [1] W, [2] d_max, [3..] bin counts
   bool have_stats = false;
-  uint64_t W = 0, dmax = 0, maxout = 0;
+  uint64_t W = 0, dmax = 0, maxout = 0, nact = 0;
 
   // last ingest result (fglt_build_csr), on the device
   int64_t ing_n = 0, ing_nnz = 0;
@@ -292,8 +293,8 @@ void launch_sweep_bc(fglt_ctx* c) {
 
 template <int G>
 void launch_root_work(fglt_ctx* c, u64* wc, u64* tw) {
-  k_root_work<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(c->rp, c->ci, c->split, c->mir,
-                                                                (int)c->n, wc, tw);
+  k_root_work<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(
+      c->rp, c->ci, c->split, c->send, c->mir, (int)c->n, c->d_small + 4, wc, tw);
   check_launch();
   c->launched();
 }
@@ -398,7 +399,9 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   int* outdeg = c->ensure<int>(B_OUTDEG, n + 1);
   int* orp = c->ensure<int>(B_ORP, n + 1);
   CK(cudaMemsetAsync(outdeg + n, 0, sizeof(int), c->stream));
-  k_split<<<c->grid(n, 256), 256, 0, c->stream>>>(c->rp, c->ci, N, split, outdeg, c->d_small + 3);
+  int* send = c->ensure<int>(B_SEND, n);
+  k_split<<<c->grid(n, 256), 256, 0, c->stream>>>(c->rp, c->ci, N, c->d_small + 4, split, send,
+                                                  outdeg, c->d_small + 3);
   check_launch();
   c->launched();
   tb = c->buf[B_CUB].cap;
@@ -407,11 +410,12 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   int* mir = c->ensure<int>(B_MIR, std::max<int64_t>(nnz, 1));
   int* ce_row = c->ensure<int>(B_CE_ROW, std::max<int64_t>(c->m, 1));
   int* ce_pos = c->ensure<int>(B_CE_POS, std::max<int64_t>(c->m, 1));
-  k_mirror<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, orp, N, mir, ce_row,
+  k_mirror<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, send, orp, N, mir, ce_row,
                                                         ce_pos);
   check_launch();
   c->launched();
   c->split = split;
+  c->send = send;
   c->orp = orp;
   c->mir = mir;
   c->ce_row = ce_row;
@@ -420,12 +424,13 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
 }
 
 void read_graph_stats(fglt_ctx* c) {
-  u64 h[3];
-  CK(cudaMemcpyAsync(h, c->d_small + 1, 24, cudaMemcpyDeviceToHost, c->stream));
+  u64 h[4];
+  CK(cudaMemcpyAsync(h, c->d_small + 1, 32, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->W = h[0];
   c->dmax = h[1];
   c->maxout = h[2];
+  c->nact = h[3];
   c->have_stats = true;
 }
 
@@ -440,7 +445,8 @@ void sweep_a(fglt_ctx* c) {
 void local_sweeps(fglt_ctx* c) {
   if (!c->plan.c3 || c->n == 0) return;
   if (c->m > 0) {
-    k_c3_mirror<<<c->grid(c->m, 256), 256, 0, c->stream>>>(c->ce_pos, c->mir, (int)c->m, c->C3f);
+    k_c3_mirror<<<c->grid(c->m, 256), 256, 0, c->stream>>>(c->ce_pos, c->mir, c->orp + c->n,
+                                                          c->C3f);
     check_launch();
     c->launched();
   }
@@ -478,10 +484,10 @@ std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
 }
 
 
-__global__ void k_outdeg_key(const int* __restrict__ rp, const int* __restrict__ split, int n,
+__global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict__ split, int n,
                              u64* __restrict__ key, u64 force_key) {
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
-    const int s = rp[u + 1] - split[u];
+    const int s = send[u] - split[u];
     u64 k = s >= 2 ? (u64)s : 0ull;
     // test hook: push roots into a larger bin (a bin's kernel handles any s
     // below its cap, so forcing upward is always valid)
@@ -498,7 +504,7 @@ void root_bins(fglt_ctx* c, int64_t u0, int64_t u1) {
   u64* key = c->ensure<u64>(B_RKEY, (size_t)std::max<int64_t>(c->n, 1));
   static const u64 kForceKey[] = {0, 33, 129, 257, 513, 1025};
   const u64 fk = (c->force_roots_bin > 0 && c->force_roots_bin < 6) ? kForceKey[c->force_roots_bin] : 0;
-  k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->rp, c->split, (int)c->n, key, fk);
+  k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->send, c->split, (int)c->n, key, fk);
   check_launch();
   c->launched();
   int64_t stride = 0;
@@ -522,7 +528,7 @@ void roots_pass(fglt_ctx* c) {
     const int wpb = 8;
     const size_t sm = (size_t)wpb * (32 * 8 + 161 * 4);
     const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
-    k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->C3f,
+    k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->send, c->C3f,
                                                                   lists[0], cnt[0], d13, d15);
     check_launch();
     c->launched();
@@ -548,12 +554,12 @@ void roots_pass(fglt_ctx* c) {
       slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
       set_smem(k_roots_block<kC3, kD13, kD15, true>, sm);
       k_roots_block<kC3, kD13, kD15, true><<<g, 256, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], L, slab, slab_stride, d13, d15);
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, d13, d15);
     } else {
       sm += L.bytes_aux();
       set_smem(k_roots_block<kC3, kD13, kD15, false>, sm);
       k_roots_block<kC3, kD13, kD15, false><<<g, 256, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->C3f, lists[b], cnt[b], L, slab, slab_stride, d13, d15);
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, d13, d15);
     }
     check_launch();
     c->launched();

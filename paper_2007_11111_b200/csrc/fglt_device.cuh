@@ -123,9 +123,14 @@ __device__ __forceinline__ u64 seg_sum_runs(int row, u64 v, bool* tail) {
 // ------------------------------------------------------------ preprocessing
 
 // key = degree << 32 | id : sorting these gives the relabelling order.
+// Vertices of degree <= 1 lie on no triangle or cycle: they are ranked LAST
+// (bit 31 of the degree field), so the enumeration id range [0, n_active)
+// holds only vertices of degree >= 2 and the 4-cycle tiles shrink with it.
 __global__ void k_degree_keys(const int* __restrict__ rp, int n, u64* __restrict__ keys) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    keys[i] = ((u64)(rp[i + 1] - rp[i]) << 32) | (u64)i;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u64 d = (u64)(rp[i + 1] - rp[i]);
+    keys[i] = ((d < 2 ? d | 0x80000000ull : d) << 32) | (u64)i;
+  }
 }
 
 __global__ void k_perm(const u64* __restrict__ keys, int n, int* __restrict__ perm,
@@ -135,7 +140,7 @@ __global__ void k_perm(const u64* __restrict__ keys, int n, int* __restrict__ pe
     int old = (int)(k & 0xffffffffu);
     perm[r] = old;
     inv[old] = r;
-    ndeg[r] = (int)(k >> 32);
+    ndeg[r] = (int)((k >> 32) & 0x7fffffffull);
   }
 }
 
@@ -155,14 +160,21 @@ __global__ void k_fill_rows(const int* __restrict__ rp, const int* __restrict__ 
 // split[r] = first position of row r holding a neighbour > r; row_of for the
 // canonical (upper) positions is written as a compact edge list.
 __global__ void k_split(const int* __restrict__ rp, const int* __restrict__ ci, int n,
-                        int* __restrict__ split, int* __restrict__ outdeg,
+                        const unsigned long long* __restrict__ nact_p, int* __restrict__ split,
+                        int* __restrict__ send, int* __restrict__ outdeg,
                         unsigned long long* __restrict__ maxout) {
+  // split[r]: first neighbour > r; send[r]: first neighbour >= n_active (the
+  // pendant/isolated tail). N+(r) restricted to active vertices is
+  // [split[r], send[r]); vertices >= n_active are never enumeration roots.
+  const int nact = (int)*nact_p;
   unsigned long long mo = 0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    int s = lower_bound_i32(ci, rp[r], rp[r + 1], r);
+    const int s = lower_bound_i32(ci, rp[r], rp[r + 1], r);
+    const int e = r < nact ? lower_bound_i32(ci, s, rp[r + 1], nact) : s;
     split[r] = s;
-    outdeg[r] = rp[r + 1] - s;
-    mo = max(mo, (unsigned long long)(rp[r + 1] - s));
+    send[r] = e;
+    outdeg[r] = e - s;
+    mo = max(mo, (unsigned long long)(e - s));
   }
   if (mo) atomicMax(maxout, mo);
 }
@@ -171,13 +183,15 @@ __global__ void k_split(const int* __restrict__ rp, const int* __restrict__ ci, 
 // mirror position q of r in row v (a prefix entry) and record both; also emit
 // the compact canonical edge list (row, position), index e = orp[r] + offset.
 __global__ void k_mirror(const int* __restrict__ rp, const int* __restrict__ ci,
-                         const int* __restrict__ split, const int* __restrict__ orp,
-                         int n, int* __restrict__ mir, int* __restrict__ ce_row,
-                         int* __restrict__ ce_pos) {
+                         const int* __restrict__ split, const int* __restrict__ send,
+                         const int* __restrict__ orp, int n, int* __restrict__ mir,
+                         int* __restrict__ ce_row, int* __restrict__ ce_pos) {
+  // canonical edges between active vertices only: edges to the pendant tail
+  // carry no triangles (their C3 stays 0 in both slots)
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
-    const int s = split[r], e = rp[r + 1], base = orp[r];
+    const int s = split[r], e = send[r], base = orp[r];
     for (int p = s + lane; p < e; p += 32) {
       const int v = ci[p];
       const int q = lower_bound_i32(ci, rp[v], split[v], r);
@@ -229,7 +243,9 @@ __global__ void k_sweep_a(const int* __restrict__ rp, const int* __restrict__ ci
 
 // Copy canonical C3 values into their mirror slots so rows read contiguously.
 __global__ void k_c3_mirror(const int* __restrict__ ce_pos, const int* __restrict__ mir,
-                            int m, u32* __restrict__ C3f) {
+                            const int* __restrict__ m_active, u32* __restrict__ C3f) {
+  // m_active = orp[n]: the canonical list holds active-active edges only
+  const int m = *m_active;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
     const int p = ce_pos[e];
     C3f[mir[p]] = C3f[p];

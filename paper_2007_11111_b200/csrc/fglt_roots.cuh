@@ -35,8 +35,11 @@ namespace fglt {
 // wc(u) = number of wedges rooted at u; tw(u) = triangle-probe work of u.
 template <int G>
 __global__ void k_root_work(const int* __restrict__ rp, const int* __restrict__ ci,
-                            const int* __restrict__ split, const int* __restrict__ mir, int n,
+                            const int* __restrict__ split, const int* __restrict__ send,
+                            const int* __restrict__ mir, int n,
+                            const unsigned long long* __restrict__ nact_p,
                             u64* __restrict__ wc, u64* __restrict__ tw) {
+  const int nact = (int)*nact_p;
   const int lane = threadIdx.x & (G - 1);
   const int groups = (gridDim.x * blockDim.x) / G;
   const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -44,19 +47,19 @@ __global__ void k_root_work(const int* __restrict__ rp, const int* __restrict__ 
   for (int it = 0; it < rounds; ++it) {
     const int u = g0 + it * groups;
     u64 a = 0, t = 0;
-    if (u < n) {
-      const int b = rp[u], s = split[u], e = rp[u + 1];
+    if (u < nact) {  // pendant/isolated vertices root nothing
+      const int b = rp[u], s = split[u], e = send[u];
       for (int q = b + lane; q < s; q += G) a += (u64)(mir[q] - rp[ci[q]]);
       for (int p = s + lane; p < e; p += G) {
         const int x = ci[p];
-        t += (u64)(rp[x + 1] - split[x]);
+        t += (u64)(send[x] - split[x]);
       }
     }
     a = group_sum_u64<G>(a);
     t = group_sum_u64<G>(t);
     if (u < n && lane == 0) {
       wc[u] = a;
-      tw[u] = t + (u64)(rp[u + 1] - split[u]);
+      tw[u] = u < nact ? t + (u64)(send[u] - split[u]) : 0;
     }
   }
 }
@@ -664,7 +667,8 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
 // Warp per root, |S| <= 32: rows are single words.
 template <bool kC3, bool kD13, bool kD15>
 __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__ ci,
-                             const int* __restrict__ split, u32* __restrict__ C3f,
+                             const int* __restrict__ split, const int* __restrict__ send,
+                             u32* __restrict__ C3f,
                              const int* __restrict__ roots, int nroots,
                              u64* __restrict__ d13, u64* __restrict__ d15) {
   // kC3: per-edge triangle counts (atomics into C3f) — the triangle pass.
@@ -682,7 +686,7 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
     const int u = roots[k];
     const int s0 = split[u];
-    const int s = rp[u + 1] - s0;
+    const int s = send[u] - s0;
     if (lane < s) {
       sS[lane] = ci[s0 + lane];
       if (kD13) sC[lane] = C3f[s0 + lane];
@@ -803,7 +807,8 @@ __device__ __forceinline__ int s_hash_find(const int* keys, const unsigned short
 template <bool kC3, bool kD13, bool kD15, bool kGlobal>
 __global__ void __launch_bounds__(256)
 k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
-              const int* __restrict__ split, u32* __restrict__ C3f,
+              const int* __restrict__ split, const int* __restrict__ send,
+              u32* __restrict__ C3f,
               const int* __restrict__ roots, int nroots, RootsLayout L,
               unsigned char* __restrict__ slab, long long slab_stride,
               u64* __restrict__ d13, u64* __restrict__ d15) {
@@ -828,7 +833,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
   for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
     const int u = roots[k];
     const int s0 = split[u];
-    const int s = rp[u + 1] - s0;
+    const int s = send[u] - s0;
     const int nw = (s + 31) >> 5;
     const int stride = nw | 1;
     int hlog = 6;
@@ -1142,13 +1147,16 @@ __global__ void k_net_only(const u64* __restrict__ raw, const DictInfo* __restri
 
 // W = sum d^2, d_max (stats and the roofline model).
 __global__ void k_graph_stats(const int* __restrict__ rp, int n, u64* __restrict__ out) {
-  u64 w = 0, dm = 0;
+  // out[0] W = sum d^2, out[1] d_max, out[3] n_active (#vertices of degree >= 2)
+  u64 w = 0, dm = 0, act = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const u64 d = (u64)(rp[i + 1] - rp[i]);
     w += d * d;
     dm = d > dm ? d : dm;
+    act += d >= 2;
   }
   w = warp_sum_u64(w);
+  act = warp_sum_u64(act);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const u64 x = __shfl_xor_sync(0xffffffffu, dm, o);
@@ -1157,6 +1165,7 @@ __global__ void k_graph_stats(const int* __restrict__ rp, int n, u64* __restrict
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(out, w);
     atomicMax(out + 1, dm);
+    if (act) atomicAdd(out + 3, act);
   }
 }
 
