@@ -56,7 +56,8 @@ const unsigned char kU16[16][16] = {
 
 constexpr int kSmallS = 32;       // roots with |N+(u)| <= 32: warp kernel
 constexpr int kBlockS = 1024;     // <= 1024: block kernel, bitmap in smem
-constexpr int kWarpHashLog = 9;   // 512-slot table per warp
+constexpr int kWarpHashLog = 9;   // 512-slot table per warp (wc <= 256)
+constexpr int kWarpHashLog2 = 11; // 2048-slot table per warp (wc <= 1024)
 
 enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
@@ -594,33 +595,43 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         c->rp, c->split, wc, (int)u0, (int)u1, cls, parts, c->force_c4_class, c->force_c4_parts);
     check_launch();
     c->launched();
-    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4}, lists, &stride);
+    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5}, lists, &stride);
     c->mark("four-cycle rows:start");
     u64* c4 = c->V(V_C4);
-    if (cnt[0] > 0) {
+    if (cnt[0] > 0) {  // class 1: warp tables of 512 slots
       const int wpb = 8;
-      const size_t sm = (size_t)wpb * ((1 << kWarpHashLog) * 2 + 97) * 4;
+      const size_t sm = (size_t)wpb * ((1 << kWarpHashLog) * 2 + 100) * 4;
       k_c4_warp<kWarpHashLog><<<c->grid((int64_t)cnt[0] * 32, wpb * 32), wpb * 32, sm, c->stream>>>(
           c->rp, c->ci, c->split, c->mir, lists[0], cnt[0], wc, c4);
       check_launch();
       c->launched();
     }
-    if (cnt[1] > 0) {  // small tables: 128-thread blocks, several per SM
+    if (cnt[1] > 0) {  // class 2: warp tables of 2048 slots
+      const int wpb = 4;
+      const size_t sm = (size_t)wpb * ((1 << kWarpHashLog2) * 2 + 100) * 4;
+      set_smem(k_c4_warp<kWarpHashLog2>, sm);
+      k_c4_warp<kWarpHashLog2><<<c->grid((int64_t)cnt[1] * 32, wpb * 32, 3), wpb * 32, sm,
+                                 c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[1], cnt[1], wc,
+                                              c4);
+      check_launch();
+      c->launched();
+    }
+    if (cnt[2] > 0) {  // class 3: small block tables, 128-thread blocks
       const size_t sm = (size_t)(1 << kC4SmallLog) * 8;
-      const int g = std::min(cnt[1], c->sms * 6);
-      DISPATCH_G(G, launch_c4_hashp, c, g, 128, sm, lists[1], cnt[1], wc, parts, kC4SmallLog, c4);
+      const int g = std::min(cnt[2], c->sms * 6);
+      DISPATCH_G(G, launch_c4_hashp, c, g, 128, sm, lists[2], cnt[2], wc, parts, kC4SmallLog, c4);
     }
-    if (cnt[2] > 0) {
+    if (cnt[3] > 0) {  // class 4: hash-partition passes
       const size_t sm = (size_t)(1 << kC4HashLog) * 8;
-      const int g = std::min(cnt[2], c->sms);
-      DISPATCH_G(G, launch_c4_hashp, c, g, 512, sm, lists[2], cnt[2], wc, parts, kC4HashLog, c4);
+      const int g = std::min(cnt[3], c->sms);
+      DISPATCH_G(G, launch_c4_hashp, c, g, 512, sm, lists[3], cnt[3], wc, parts, kC4HashLog, c4);
     }
-    for (int bb = 3; bb <= 4; ++bb) {
+    for (int bb = 4; bb <= 5; ++bb) {  // classes 5/6: dense tiles
       if (cnt[bb] == 0) continue;
       const size_t sm = 196608;
       const int g = std::min(cnt[bb], c->sms);
       int* cur = c->ensure<int>(B_CURSOR, 2 * (size_t)g * (size_t)(c->dmax + 1));
-      if (bb == 3) {
+      if (bb == 4) {
         set_smem(k_c4_dense<true>, sm);
         k_c4_dense<true><<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[bb],
                                                      cnt[bb], cur, (long long)(c->dmax + 1), c4);

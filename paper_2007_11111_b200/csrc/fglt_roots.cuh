@@ -90,6 +90,23 @@ __device__ __forceinline__ u32 hash_get(const int* keys, const u32* vals, int lo
 }
 
 // Warp per root; a 2^LOGCAP-slot table per warp in shared memory.
+// Lookup that also claims the slot: bit 31 of the count marks "C(L,2) already
+// emitted for this target"; *first is true for exactly one caller per slot.
+__device__ __forceinline__ u32 hash_get_claim(const int* keys, u32* vals, int logcap, int w,
+                                              bool* first) {
+  const u32 mask = (1u << logcap) - 1;
+  u32 h = hash_slot(w, logcap);
+  while (true) {
+    const int k = keys[h];
+    if (k == w) {
+      const u32 old = atomicOr(vals + h, 0x80000000u);
+      *first = !(old & 0x80000000u);
+      return old & 0x7fffffffu;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
 // Warp per root (wc <= 256): a table of 2^hlog <= 2^LOGCAP slots sized to the
 // root; the rows of N-(u) are walked 32 at a time with segment flattening so
 // every lane streams one wedge per step.
@@ -99,8 +116,8 @@ __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci
                           const int* __restrict__ roots, int nroots, const u64* __restrict__ wcv,
                           u64* __restrict__ c4) {
   constexpr int CAP = 1 << LOGCAP;
-  constexpr int PER_WARP = CAP * 2 + 32 + 33 + 32;  // keys, vals, base, off, rowsum
-  extern __shared__ unsigned char smem_raw[];
+  constexpr int PER_WARP = CAP * 2 + 100;  // keys, vals, base[32], off[33], rowsum[32], pad (16 B)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   int* keys = reinterpret_cast<int*>(smem_raw) + wib * PER_WARP;
@@ -114,7 +131,14 @@ __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci
     int hlog = 5;
     while (hlog < LOGCAP && ((u64)1 << hlog) < 2 * wcv[u]) ++hlog;
     const int cap = 1 << hlog;
-    for (int i = lane; i < cap; i += 32) { keys[i] = -1; vals[i] = 0; }
+    {
+      uint4* k4 = reinterpret_cast<uint4*>(keys);
+      uint4* v4 = reinterpret_cast<uint4*>(vals);
+      for (int i = lane; i < (cap >> 2); i += 32) {
+        k4[i] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+        v4[i] = make_uint4(0, 0, 0, 0);
+      }
+    }
     rs[lane] = 0;
     __syncwarp();
     const int b = rp[u], s = split[u];
@@ -132,21 +156,24 @@ __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci
       if (lane == 0) foff[32] = T;
       __syncwarp();
       int r = 0;
-      for (int kk = lane; kk < T; kk += 32) {
-        while (foff[r + 1] <= kk) ++r;
-        hash_insert(keys, vals, hlog, __ldg(ci + fbase[r] + kk));
+      for (int kk = lane; kk < T; kk += 128) {  // 4 independent loads in flight
+        int w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int kj = kk + 32 * j;
+          w[j] = -1;
+          if (kj < T) {
+            while (foff[r + 1] <= kj) ++r;
+            w[j] = __ldg(ci + fbase[r] + kj);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (w[j] >= 0) hash_insert(keys, vals, hlog, w[j]);
       }
       __syncwarp();
     }
-    u64 acc = 0;
-    for (int i = lane; i < cap; i += 32) {
-      const u32 l = vals[i];
-      if (l >= 2) {
-        const u64 c = (u64)l * (l - 1) / 2;
-        acc += c;
-        atomicAdd(c4 + keys[i], c);
-      }
-    }
+    u64 acc = 0;  // sum_w C(L[w],2), emitted by the first visitor of each target
     for (int q0 = b; q0 < s; q0 += 32) {
       const int q = q0 + lane;
       int st = 0, len = 0;
@@ -162,14 +189,35 @@ __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci
       __syncwarp();
       int r = 0, cr = 0;
       u32 part = 0;
-      for (int kk = lane; kk < T; kk += 32) {
-        while (foff[r + 1] <= kk) ++r;
-        if (r != cr) {
-          if (part) atomicAdd(rs + cr, part);
-          part = 0;
-          cr = r;
+      for (int kk = lane; kk < T; kk += 128) {  // 4 independent loads in flight
+        int w[4], rr[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int kj = kk + 32 * j;
+          w[j] = -1;
+          if (kj < T) {
+            while (foff[r + 1] <= kj) ++r;
+            rr[j] = r;
+            w[j] = __ldg(ci + fbase[r] + kj);
+          }
         }
-        part += hash_get(keys, vals, hlog, __ldg(ci + fbase[r] + kk)) - 1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (w[j] < 0) break;
+          if (rr[j] != cr) {
+            if (part) atomicAdd(rs + cr, part);
+            part = 0;
+            cr = rr[j];
+          }
+          bool first;
+          const u32 l = hash_get_claim(keys, vals, hlog, w[j], &first);
+          if (first && l >= 2) {
+            const u64 cc = (u64)l * (l - 1) / 2;
+            acc += cc;
+            atomicAdd(c4 + w[j], cc);
+          }
+          part += l - 1;
+        }
       }
       if (part) atomicAdd(rs + cr, part);
       __syncwarp();
@@ -198,12 +246,13 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 }
 
 // Cost-model classes for roots with wc(u) > 0 (k_c4_class):
-//   1 warp table     wc <= 256
-//   2 small block table (128 threads, <= 4096 slots), wc <= 2048
-//   3 block table, P hash-partition passes over the wedges, P = ceil(wc/12288)
-//   4 dense tiles, 16-bit packed counters (|N-(u)| < 65536), 96K ids per tile
-//   5 dense tiles, 32-bit counters, 48K ids per tile
-// Class 3 vs 4/5 is chosen per root by the cheaper of the two modelled costs.
+//   1 warp table, 512 slots              wc <= 256
+//   2 warp table, 2048 slots             wc <= 1024
+//   3 small block table (128 threads, <= 4096 slots), wc <= 2048
+//   4 block table, P hash-partition passes over the wedges, P = ceil(wc/12288)
+//   5 dense tiles, 16-bit packed counters (|N-(u)| < 65536), 96K ids per tile
+//   6 dense tiles, 32-bit counters, 48K ids per tile
+// Class 4 vs 5/6 is chosen per root by the cheaper of the two modelled costs.
 constexpr int kC4HashLog = 14;              // 16384 slots (keys + counts = 128 KB)
 constexpr int kC4SmallLog = 12;             // 4096 slots (32 KB)
 constexpr u64 kC4HashFill = 12288;          // distinct targets per pass (LF 0.75)
@@ -222,8 +271,10 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       c = 0;
     } else if (w <= 256) {
       c = 1;
-    } else if (w <= 2048) {
+    } else if (w <= 1024) {
       c = 2;
+    } else if (w <= 2048) {
+      c = 3;
     } else {
       const u64 nq = (u64)(split[u] - rp[u]);
       P = (w + kC4HashFill - 1) / kC4HashFill;
@@ -232,15 +283,15 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       const u64 tile = pack ? kC4Tile16 : kC4Tile32;
       const u64 tiles = ((u64)u + tile - 1) / tile;
       const u64 cost_dense = tiles * (2 * 49152 / 4 + nq) + 2 * w;
-      if (cost_hash <= cost_dense) c = 3;
-      else c = pack ? 4 : 5;
+      if (cost_hash <= cost_dense) c = 4;
+      else c = pack ? 5 : 6;
     }
     if (force_cls > 0 && w > 0) {  // test hook: route every root to one path
       const u64 nq = (u64)(split[u] - rp[u]);
       // external numbering: 2 hash passes, 3 packed tiles, 4 32-bit tiles
-      c = (u64)force_cls + 1;
-      if (c == 4 && nq >= 65536) c = 5;
-      if (c == 3) {
+      c = (u64)force_cls + 2;
+      if (c == 5 && nq >= 65536) c = 6;
+      if (c == 4) {
         P = (w + kC4HashFill - 1) / kC4HashFill;
         if (force_parts > 0) P = (u64)force_parts;
       }
