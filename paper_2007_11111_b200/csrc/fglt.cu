@@ -63,7 +63,7 @@ enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
   B_CUB, B_CURSOR, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
-  B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_COUNT
+  B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV, B_COUNT
 };
 
 struct DevBuf {
@@ -302,10 +302,10 @@ void launch_root_work(fglt_ctx* c, u64* wc, u64* tw) {
 
 template <int G>
 void launch_c4_hashp(fglt_ctx* c, int g, int block, size_t sm, const int* roots, int nroots,
-                     const u64* wc, const u64* parts, int max_log, u64* c4) {
+                     const u64* wc, const u64* parts, int max_log, int* queue, u64* c4) {
   set_smem(k_c4_hashp<G>, sm);
   k_c4_hashp<G><<<g, block, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, roots, nroots, wc,
-                                             parts, max_log, c4);
+                                             parts, max_log, queue, c4);
   check_launch();
   c->launched();
 }
@@ -499,6 +499,31 @@ __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict
 
 constexpr u64 kRootThr[] = {(u64)kSmallS, 128, 256, 512, (u64)kBlockS};
 
+__global__ void k_gather_keys(const int* __restrict__ list, int cnt, const u64* __restrict__ w,
+                              u64* __restrict__ keys) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+    keys[i] = w[list[i]];
+}
+
+// Order a root list by work, largest first (LPT for the dynamic queues).
+void sort_by_work_desc(fglt_ctx* c, int* list, int cnt, const u64* w) {
+  if (cnt < 2) return;
+  u64* k = c->ensure<u64>(B_SORTK, 2 * (size_t)cnt);
+  int* v = c->ensure<int>(B_SORTV, (size_t)cnt);
+  k_gather_keys<<<c->grid(cnt, 256), 256, 0, c->stream>>>(list, cnt, w, k);
+  check_launch();
+  c->launched();
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, k, k + cnt, list, v, cnt, 0, 64,
+                                               c->stream));
+  void* tmp = c->ensure<unsigned char>(B_CUB, tb);
+  tb = c->buf[B_CUB].cap;
+  CK(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, k, k + cnt, list, v, cnt, 0, 64,
+                                               c->stream));
+  c->launched();
+  CK(cudaMemcpyAsync(list, v, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, c->stream));
+}
+
 // Bin roots [u0,u1) by |N+(u)| (>= 2) once; both root passes reuse the lists.
 void root_bins(fglt_ctx* c, int64_t u0, int64_t u1) {
   if (c->rb_u0 == u0 && c->rb_u1 == u1 && !c->rb_cnt.empty()) return;
@@ -596,6 +621,9 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     check_launch();
     c->launched();
     std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5}, lists, &stride);
+    for (int bb = 3; bb <= 5; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc);
+    int* queues = reinterpret_cast<int*>(c->d_small + 56);  // dynamic root queues
+    CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
     c->mark("four-cycle rows:start");
     u64* c4 = c->V(V_C4);
     if (cnt[0] > 0) {  // class 1: warp tables of 512 slots
@@ -619,12 +647,14 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     if (cnt[2] > 0) {  // class 3: small block tables, 128-thread blocks
       const size_t sm = (size_t)(1 << kC4SmallLog) * 8;
       const int g = std::min(cnt[2], c->sms * 6);
-      DISPATCH_G(G, launch_c4_hashp, c, g, 128, sm, lists[2], cnt[2], wc, parts, kC4SmallLog, c4);
+      DISPATCH_G(G, launch_c4_hashp, c, g, 128, sm, lists[2], cnt[2], wc, parts, kC4SmallLog,
+                 queues + 0, c4);
     }
     if (cnt[3] > 0) {  // class 4: hash-partition passes
       const size_t sm = (size_t)(1 << kC4HashLog) * 8;
       const int g = std::min(cnt[3], c->sms);
-      DISPATCH_G(G, launch_c4_hashp, c, g, 512, sm, lists[3], cnt[3], wc, parts, kC4HashLog, c4);
+      DISPATCH_G(G, launch_c4_hashp, c, g, 512, sm, lists[3], cnt[3], wc, parts, kC4HashLog,
+                 queues + 1, c4);
     }
     for (int bb = 4; bb <= 5; ++bb) {  // classes 5/6: dense tiles
       if (cnt[bb] == 0) continue;
@@ -634,11 +664,13 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       if (bb == 4) {
         set_smem(k_c4_dense<true>, sm);
         k_c4_dense<true><<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[bb],
-                                                     cnt[bb], cur, (long long)(c->dmax + 1), c4);
+                                                     cnt[bb], cur, (long long)(c->dmax + 1),
+                                                     queues + 2, c4);
       } else {
         set_smem(k_c4_dense<false>, sm);
         k_c4_dense<false><<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[bb],
-                                                      cnt[bb], cur, (long long)(c->dmax + 1), c4);
+                                                      cnt[bb], cur, (long long)(c->dmax + 1),
+                                                      queues + 3, c4);
       }
       check_launch();
       c->launched();

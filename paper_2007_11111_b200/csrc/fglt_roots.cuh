@@ -316,7 +316,9 @@ __global__ void
 k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, const u64* __restrict__ wcv,
-           const u64* __restrict__ parts, int max_log, u64* __restrict__ c4) {
+           const u64* __restrict__ parts, int max_log, int* __restrict__ next_root,
+           u64* __restrict__ c4) {
+  // roots are sorted by work (largest first) and handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
   const int maxcap = 1 << max_log;
@@ -324,7 +326,12 @@ k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
   u32* vals = reinterpret_cast<u32*>(keys + maxcap);
   const int gl = threadIdx.x & (G - 1);
   const int gid = threadIdx.x / G, ngroups = blockDim.x / G;
-  for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
+  __shared__ int s_root;
+  while (true) {
+    if (threadIdx.x == 0) s_root = atomicAdd(next_root, 1);
+    __syncthreads();
+    const int k = s_root;
+    if (k >= nroots) break;
     const int u = roots[k];
     const u32 P = (u32)parts[u];
     const u64 per_pass = (wcv[u] + P - 1) / P;
@@ -471,7 +478,8 @@ __global__ void __launch_bounds__(1024)
 k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, int* __restrict__ cursor,
-           long long cursor_stride, u64* __restrict__ c4) {
+           long long cursor_stride, int* __restrict__ next_root, u64* __restrict__ c4) {
+  // roots are sorted by work (largest first) and handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
   __shared__ u64 rsum[32][32];
@@ -496,7 +504,12 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     return L[off];
   };
   rs[lane] = 0;
-  for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
+  __shared__ int s_root;
+  while (true) {
+    if (threadIdx.x == 0) s_root = atomicAdd(next_root, 1);
+    __syncthreads();
+    const int k = s_root;
+    if (k >= nroots) break;
     const int u = roots[k];
     const int b = rp[u], nq = split[u] - b;
     // first long row (rows in N-(u) have nondecreasing degree)
