@@ -536,6 +536,8 @@ void root_bins(fglt_ctx* c, int64_t u0, int64_t u1) {
   int64_t stride = 0;
   c->rb_cnt = bin_roots(c, key, u0, u1, std::vector<u64>(std::begin(kRootThr), std::end(kRootThr)),
                         c->rb_lists, &stride, B_RLISTS);
+  for (int b = 1; b < (int)c->rb_cnt.size(); ++b)
+    sort_by_work_desc(c, c->rb_lists[b], c->rb_cnt[b], key);
   c->rb_u0 = u0;
   c->rb_u1 = u1;
 }
@@ -550,6 +552,8 @@ void roots_pass(fglt_ctx* c) {
   u64* d15 = c->V(V_D15);
   const std::vector<int>& cnt = c->rb_cnt;
   int** lists = c->rb_lists;
+  int* queues = reinterpret_cast<int*>(c->d_small + 60);  // one dynamic queue per bin
+  CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
   if (cnt[0] > 0) {
     const int wpb = 8;
     const size_t sm = (size_t)wpb * (32 * 8 + 161 * 4);
@@ -580,12 +584,12 @@ void roots_pass(fglt_ctx* c) {
       slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
       set_smem(k_roots_block<kC3, kD13, kD15, true>, sm);
       k_roots_block<kC3, kD13, kD15, true><<<g, 256, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, d13, d15);
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15);
     } else {
       sm += L.bytes_aux();
       set_smem(k_roots_block<kC3, kD13, kD15, false>, sm);
       k_roots_block<kC3, kD13, kD15, false><<<g, 256, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, d13, d15);
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15);
     }
     check_launch();
     c->launched();

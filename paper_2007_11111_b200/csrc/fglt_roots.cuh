@@ -875,7 +875,8 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
               u32* __restrict__ C3f,
               const int* __restrict__ roots, int nroots, RootsLayout L,
               unsigned char* __restrict__ slab, long long slab_stride,
-              u64* __restrict__ d13, u64* __restrict__ d15) {
+              int* __restrict__ next_root, u64* __restrict__ d13, u64* __restrict__ d15) {
+  // roots sorted by |S| (largest first), handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
   __shared__ int next_item[2];
@@ -894,7 +895,12 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
       ((((size_t)L.nwarps * L.s_cap * 2) + 15) & ~(size_t)15));
   unsigned short* mylist = lists + (size_t)wid * L.s_cap;
 
-  for (int k = blockIdx.x; k < nroots; k += gridDim.x) {
+  __shared__ int s_root;
+  while (true) {
+    if (threadIdx.x == 0) s_root = atomicAdd(next_root, 1);
+    __syncthreads();
+    const int k = s_root;
+    if (k >= nroots) break;
     const int u = roots[k];
     const int s0 = split[u];
     const int s = send[u] - s0;
