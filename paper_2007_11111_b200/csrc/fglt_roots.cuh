@@ -608,24 +608,37 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         __syncwarp();
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < words; i += blockDim.x) {
-        const u32 x = L[i];
-        if (PACK) {
-          const u32 l0 = x & 0xffffu, l1 = x >> 16;
-          if (l0 >= 2) {
-            const u64 c = (u64)l0 * (l0 - 1) / 2;
-            acc += c;
-            atomicAdd(c4 + lo + 2 * i, c);
+      {
+        // 16-byte sweep; words past the tile end were zeroed with the tile
+        const uint4* L4 = reinterpret_cast<const uint4*>(L);
+        const int n4 = (words + 3) >> 2;
+        const u32 ge2 = PACK ? 0xfffefffeu : 0xfffffffeu;  // some counter >= 2
+        for (int i4 = threadIdx.x; i4 < n4; i4 += blockDim.x) {
+          const uint4 v = L4[i4];
+          if (((v.x | v.y | v.z | v.w) & ge2) == 0) continue;
+          const u32 xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const u32 x = xs[j];
+            const int i = 4 * i4 + j;
+            if (PACK) {
+              const u32 l0 = x & 0xffffu, l1 = x >> 16;
+              if (l0 >= 2) {
+                const u64 c = (u64)l0 * (l0 - 1) / 2;
+                acc += c;
+                atomicAdd(c4 + lo + 2 * i, c);
+              }
+              if (l1 >= 2) {
+                const u64 c = (u64)l1 * (l1 - 1) / 2;
+                acc += c;
+                atomicAdd(c4 + lo + 2 * i + 1, c);
+              }
+            } else if (x >= 2) {
+              const u64 c = (u64)x * (x - 1) / 2;
+              acc += c;
+              atomicAdd(c4 + lo + i, c);
+            }
           }
-          if (l1 >= 2) {
-            const u64 c = (u64)l1 * (l1 - 1) / 2;
-            acc += c;
-            atomicAdd(c4 + lo + 2 * i + 1, c);
-          }
-        } else if (x >= 2) {
-          const u64 c = (u64)x * (x - 1) / 2;
-          acc += c;
-          atomicAdd(c4 + lo + i, c);
         }
       }
       // ---- attribution pass: c4[v] += sum (L[w] - 1); cursors advance
@@ -760,6 +773,7 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
     rows[lane] = 0;
     __syncwarp();
     const int smax = sS[s - 1];
+    const bool narrow = (u64)s * (u64)(rp[u + 1] - rp[u]) < (1ull << 32);
     u64 tu = 0;
     // Flatten the probe lists N+(S[a]) (cut at max S) of all members: lane a
     // sets up its segment, then every lane streams one element per step.
@@ -803,7 +817,8 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
         if (kD13) {
           tu += (u64)__ldg(C3f + p) - 1;
           da += (u64)sC[bi] - 1;
-          smem_add_u64(sD + bi, (u64)sC[r] - 1);
+          if (narrow) atomicAdd(reinterpret_cast<u32*>(sD + bi), sC[r] - 1);
+          else smem_add_u64(sD + bi, (u64)sC[r] - 1);
         }
       }
     }
@@ -915,6 +930,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     for (int a = threadIdx.x; a < s; a += blockDim.x) {
       sS[a] = ci[s0 + a];
       if (kD13) { sC[a] = C3f[s0 + a]; sD[a] = 0; }
+      if (kD15) sD[a] = 0;  // sK (u32 view), see below
       if (kC3) sC[a] = 0;  // per-(u, S[a]) triangle counts
     }
     for (int i = threadIdx.x; i < hcap; i += blockDim.x) hkeys[i] = -1;
@@ -930,6 +946,9 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     }
     __syncthreads();
     const int smax = sS[s - 1];
+    // sD[b] sums C3(u, .) - 1 < deg(u) over < s triangles: 32 bits suffice
+    // (no carry) when s * deg(u) < 2^32
+    const bool narrow = (u64)s * (u64)(rp[u + 1] - rp[u]) < (1ull << 32);
     u64 tu = 0;
     // ---- probe: every triangle {u, S[a], S[b]} with a < b, once
     while (true) {
@@ -942,9 +961,14 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
       const int e = rp[x + 1];
       u64 da = 0;
       u32 na = 0;
+      // software-pipelined: the next chunk's load is in flight while this
+      // chunk's lookups run
+      int p = split[x] + lane;
+      int y = p < e ? __ldg(ci + p) : 0x7fffffff;
       for (int base = split[x]; base < e; base += 32) {
-        const int p = base + lane;
-        const int y = p < e ? __ldg(ci + p) : 0x7fffffff;
+        const int pn = p + 32;
+        const int ylast = __shfl_sync(0xffffffffu, y, 31);  // chunk max (rows are sorted)
+        const int yn = (pn < e && ylast < smax) ? __ldg(ci + pn) : 0x7fffffff;
         if (y <= smax) {
           const int bi = s_hash_find(hkeys, hidx, hlog, y);
           FGLT_BOUNDS(bi < s && (bi < 0 || bi > a), "bi", bi, a);
@@ -961,11 +985,14 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
             if (kD13) {
               tu += (u64)__ldg(C3f + p) - 1;
               da += (u64)sC[bi] - 1;
-              smem_add_u64(sD + bi, (u64)ca - 1);
+              if (narrow) atomicAdd(reinterpret_cast<u32*>(sD + bi), ca - 1);
+              else smem_add_u64(sD + bi, (u64)ca - 1);
             }
           }
         }
-        if (__any_sync(0xffffffffu, y >= smax)) break;
+        if (ylast >= smax) break;
+        p = pn;
+        y = yn;
       }
       if (kC3) {
 #pragma unroll
@@ -988,28 +1015,41 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
       if (threadIdx.x == 0 && tu) atomicAdd(d13 + u, tu);
     }
     if (kD15) {
-      // t_a = sum_{b in row a} popc(row_a & row_b) = 2 x (#G[S]-triangles at a)
-      u64 tot = 0;
+      // Each G[S] edge (a, b), a < b, once: c_ab = popc(row_a & row_b) is the
+      // number of G[S]-triangles on it and is credited to both ends, so
+      // sK[a] = sum_{b in row a} c_ab = 2 t_a (t_a = G[S]-triangles through a).
+      u32* sK = reinterpret_cast<u32*>(sD);
       while (true) {
         int a = 0;
         if (lane == 0) a = atomicAdd(next_item + 1, 1);
         a = __shfl_sync(0xffffffffu, a, 0);
-        if (a >= s) break;
+        if (a + 1 >= s) break;
         const u32* ra = bm + (long long)a * stride;
-        u64 acc = 0;
-        // row degree decides the lane mapping
-        int deg = 0;
-        for (int j = lane; j < nw; j += 32) deg += __popc(ra[j]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
-        if (deg == 0) continue;
-        if (deg >= 24 && deg <= L.s_cap) {
-          // lanes over pairs: extract the neighbour list of a, then each lane
-          // ANDs whole rows
+        const int j0 = (a + 1) >> 5;
+        const u32 m0 = ~0u << ((a + 1) & 31);  // bits > a in word j0
+        u32 acc = 0;
+        if (nw <= 8) {
+          // lane l takes bit l of each nonzero word
+          for (int j = j0; j < nw; ++j) {
+            const u32 w = ra[j] & (j == j0 ? m0 : ~0u);
+            if (w == 0) continue;
+            if ((w >> lane) & 1u) {
+              const int bb = (j << 5) + lane;
+              const u32* rb = bm + (long long)bb * stride;
+              u32 c = 0;
+              for (int t = 0; t < nw; ++t) c += __popc(ra[t] & rb[t]);
+              if (c) {
+                acc += c;
+                atomicAdd(sK + bb, c);
+              }
+            }
+          }
+        } else {
+          // extract the neighbours b > a of a, then lanes over them
           int written = 0;
-          for (int j0 = 0; j0 < nw; j0 += 32) {
-            const int j = j0 + lane;
-            u32 w = j < nw ? ra[j] : 0u;
+          for (int jb = j0; jb < nw; jb += 32) {
+            const int j = jb + lane;
+            u32 w = j < nw ? ra[j] & (j == j0 ? m0 : ~0u) : 0u;
             const int c = __popc(w);
             int incl = c;
 #pragma unroll
@@ -1025,33 +1065,34 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
             written += __shfl_sync(0xffffffffu, incl, 31);
           }
           __syncwarp();
-          FGLT_BOUNDS(written == deg, "written", written, deg);
-          for (int i = lane; i < deg; i += 32) {
-            FGLT_BOUNDS(mylist[i] < s, "list", mylist[i], s);
-            const u32* rb = bm + (long long)mylist[i] * stride;
+          FGLT_BOUNDS(written <= s, "written", written, s);
+          for (int i = lane; i < written; i += 32) {
+            const int bb = mylist[i];
+            FGLT_BOUNDS(bb > a && bb < s, "list", bb, s);
+            const u32* rb = bm + (long long)bb * stride;
             u32 c = 0;
-            for (int j = 0; j < nw; ++j) c += __popc(ra[j] & rb[j]);
-            acc += c;
-          }
-          __syncwarp();
-        } else {
-          // lanes over words
-          for (int w0 = 0; w0 < nw; ++w0) {
-            u32 bits = ra[w0];
-            while (bits) {
-              const int bb = (w0 << 5) + __ffs(bits) - 1;
-              bits &= bits - 1;
-              const u32* rb = bm + (long long)bb * stride;
-              for (int j = lane; j < nw; j += 32) acc += __popc(ra[j] & rb[j]);
+            for (int t = 0; t < nw; ++t) c += __popc(ra[t] & rb[t]);
+            if (c) {
+              acc += c;
+              atomicAdd(sK + bb, c);
             }
           }
+          __syncwarp();
         }
-        acc = warp_sum_u64(acc);
-        const u64 ta = acc / 2;
-        if (lane == 0 && ta) atomicAdd(d15 + sS[a], ta);
-        tot += ta;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0 && acc) atomicAdd(sK + a, acc);
       }
-      tot = block_sum_u64(lane == 0 ? tot : 0ull, red);
+      __syncthreads();
+      u64 tot = 0;
+      for (int a = threadIdx.x; a < s; a += blockDim.x) {
+        const u32 ta = sK[a] >> 1;
+        if (ta) {
+          atomicAdd(d15 + sS[a], (u64)ta);
+          tot += ta;
+        }
+      }
+      tot = block_sum_u64(tot, red);
       if (threadIdx.x == 0 && tot) atomicAdd(d15 + u, tot / 3);
     }
     __syncthreads();
