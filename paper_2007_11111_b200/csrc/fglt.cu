@@ -367,7 +367,7 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   tmp_bytes = std::max(tmp_bytes, t2);
   size_t t3 = 0;
   int* tmp = c->ensure<int>(B_TMP, std::max<int64_t>(nnz, 1));
-  int* nci = c->ensure<int>(B_NCI, std::max<int64_t>(nnz, 1));
+  int* nci = c->ensure<int>(B_NCI, std::max<int64_t>(nnz, 1) + 4);  // +4: 16-byte tail reads
   CK(cub::DeviceSegmentedSort::SortKeys(nullptr, t3, tmp, nci, (int)nnz, N, nrp, nrp + 1, c->stream));
   tmp_bytes = std::max(tmp_bytes, t3);
   void* cub_tmp = c->ensure<unsigned char>(B_CUB, tmp_bytes);

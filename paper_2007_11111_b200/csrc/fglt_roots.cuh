@@ -7,6 +7,7 @@
 
 #ifdef FGLT_DEBUG_BOUNDS
 #include <cstdio>
+#include <type_traits>
 #define FGLT_BOUNDS(cond, tag, a, b)                                                   \
   do {                                                                                 \
     if (!(cond)) {                                                                     \
@@ -259,6 +260,7 @@ constexpr u64 kC4HashFill = 12288;          // distinct targets per pass (LF 0.7
 constexpr int kC4Tile16 = 98304;            // ids per packed tile (192 KB)
 constexpr int kC4Tile32 = 49152;            // ids per 32-bit tile (192 KB)
 constexpr int kC4Long = 48;                 // rows at least this long: flattened batches
+constexpr int kQuadsInFlight = 2;          // 16-byte loads in flight per lane (dense batches)
 
 __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
                            const u64* __restrict__ wc, int u0, int u1, u64* __restrict__ cls,
@@ -485,6 +487,8 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   __shared__ u64 rsum[32][32];
   __shared__ int bst_all[32][32];
   __shared__ int boff_all[32][33];
+  __shared__ int bsa_all[32][32];  // per-batch row [start, end) in ci
+  __shared__ int bsb_all[32][32];
   __shared__ int next_batch[2];
   __shared__ int next_giant[2];
   constexpr int TILE = PACK ? kC4Tile16 : kC4Tile32;
@@ -495,6 +499,8 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   u64* rs = rsum[wid];
   int* bst = bst_all[wid];
   int* boff = boff_all[wid];
+  int* bsa = bsa_all[wid];
+  int* bsb = bsb_all[wid];
   auto inc = [&](int off) {
     if (PACK) atomicAdd(L + (off >> 1), 1u << ((off & 1) << 4));
     else atomicAdd(L + off, 1u);
@@ -583,27 +589,42 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
           se = hi >= u ? em : lower_bound_i32(ci, st, em, hi);
           segend[q] = se;
         }
+        // flattened over 16-byte quads of ci: quad k of row r is ci[4 (bst[r] + k)]
+        // + 0..3, elements outside [st, se) masked
+        const int qa = st >> 2;
+        const int nqd = se > st ? ((se + 3) >> 2) - qa : 0;
         int T;
-        const int off = flat_prefix(se - st, &T);
-        bst[lane] = st - off;  // element k of row r lives at bst[r] + k
+        const int off = flat_prefix(nqd, &T);
+        bst[lane] = qa - off;
         boff[lane] = off;
+        bsa[lane] = st;
+        bsb[lane] = se;
         if (lane == 0) boff[32] = T;
         __syncwarp();
         int r = 0;
-        for (int kk = lane; kk < T; kk += 128) {  // 4 independent loads in flight
-          int w[4];
+        for (int kk = lane; kk < T; kk += 32 * kQuadsInFlight) {
+          int4 v[kQuadsInFlight];
+          int lt[kQuadsInFlight], ht[kQuadsInFlight];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < kQuadsInFlight; ++j) {
             const int kj = kk + 32 * j;
-            w[j] = -1;
+            lt[j] = 4;
+            ht[j] = 0;
             if (kj < T) {
               while (boff[r + 1] <= kj) ++r;
-              w[j] = __ldg(ci + bst[r] + kj);
+              const int e0 = (bst[r] + kj) << 2;
+              v[j] = __ldg(reinterpret_cast<const int4*>(ci + e0));
+              lt[j] = bsa[r] - e0;
+              ht[j] = bsb[r] - e0;
             }
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (w[j] >= 0) inc(w[j] - lo);
+          for (int j = 0; j < kQuadsInFlight; ++j) {
+            if (lt[j] <= 0 && ht[j] > 0) inc(v[j].x - lo);
+            if (lt[j] <= 1 && ht[j] > 1) inc(v[j].y - lo);
+            if (lt[j] <= 2 && ht[j] > 2) inc(v[j].z - lo);
+            if (lt[j] <= 3 && ht[j] > 3) inc(v[j].w - lo);
+          }
         }
         __syncwarp();
       }
@@ -680,35 +701,51 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         const bool valid = q < qg;
         const int st = valid ? cur[q] : 0;
         const int se = valid ? segend[q] : 0;
+        const int qa = st >> 2;
+        const int nqd = se > st ? ((se + 3) >> 2) - qa : 0;
         int T;
-        const int off = flat_prefix(se - st, &T);
-        bst[lane] = st - off;
+        const int off = flat_prefix(nqd, &T);
+        bst[lane] = qa - off;
         boff[lane] = off;
+        bsa[lane] = st;
+        bsb[lane] = se;
         if (lane == 0) boff[32] = T;
         __syncwarp();
         int r = 0, cr = 0;
         u64 part = 0;
-        for (int kk = lane; kk < T; kk += 128) {
-          int w[4], rr[4];
+        for (int kk = lane; kk < T; kk += 32 * kQuadsInFlight) {
+          int4 v[kQuadsInFlight];
+          int lt[kQuadsInFlight], ht[kQuadsInFlight], rr[kQuadsInFlight];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < kQuadsInFlight; ++j) {
             const int kj = kk + 32 * j;
-            w[j] = -1;
+            lt[j] = 4;
+            ht[j] = 0;
+            rr[j] = r;
             if (kj < T) {
               while (boff[r + 1] <= kj) ++r;
               rr[j] = r;
-              w[j] = __ldg(ci + bst[r] + kj);
+              const int e0 = (bst[r] + kj) << 2;
+              v[j] = __ldg(reinterpret_cast<const int4*>(ci + e0));
+              lt[j] = bsa[r] - e0;
+              ht[j] = bsb[r] - e0;
             }
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (w[j] < 0) break;
+          for (int j = 0; j < kQuadsInFlight; ++j) {
+            if (ht[j] <= 0) break;
+            // PACK counters are < 2^16, so four of them fit 32 bits
+            typename std::conditional<PACK, u32, u64>::type ps = 0;
+            if (lt[j] <= 0) ps += get(v[j].x - lo) - 1;
+            if (lt[j] <= 1 && ht[j] > 1) ps += get(v[j].y - lo) - 1;
+            if (lt[j] <= 2 && ht[j] > 2) ps += get(v[j].z - lo) - 1;
+            if (ht[j] > 3) ps += get(v[j].w - lo) - 1;
             if (rr[j] != cr) {
               if (part) smem_add_u64(rs + cr, part);
               part = 0;
               cr = rr[j];
             }
-            part += get(w[j] - lo) - 1;
+            part += ps;
           }
         }
         if (part) smem_add_u64(rs + cr, part);
