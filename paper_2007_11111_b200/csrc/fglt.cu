@@ -62,7 +62,7 @@ constexpr int kWarpHashLog2 = 11; // 2048-slot table per warp (wc <= 1024)
 enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
-  B_CUB, B_CURSOR, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
+  B_CUB, B_CURSOR, B_TBND, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV, B_COUNT
 };
 
@@ -660,21 +660,31 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       DISPATCH_G(G, launch_c4_hashp, c, g, 512, sm, lists[3], cnt[3], wc, parts, kC4HashLog,
                  queues + 1, c4);
     }
+    int* bnd = nullptr;  // absolute tile boundaries of the active rows
+    const long long nact = (long long)c->nact;
+    const long long kb = nact > 0 ? (nact - 1) / kC4Tile32 + 1 : 0;
+    if ((cnt[4] > 0 || cnt[5] > 0) && kb * nact <= (1ll << 28)) {
+      bnd = c->ensure<int>(B_TBND, (size_t)(kb * nact));
+      k_tile_bounds<<<c->grid(kb * nact, 256), 256, 0, c->stream>>>(c->rp, c->ci, (int)nact,
+                                                                     (int)kb, bnd);
+      check_launch();
+      c->launched();
+    }
     for (int bb = 4; bb <= 5; ++bb) {  // classes 5/6: dense tiles
       if (cnt[bb] == 0) continue;
-      const size_t sm = 196608;
-      const int g = std::min(cnt[bb], c->sms);
+      const size_t sm = kC4TileBytes;
+      const int g = std::min(cnt[bb], c->sms * (1024 / kC4DenseThreads));
       int* cur = c->ensure<int>(B_CURSOR, 2 * (size_t)g * (size_t)(c->dmax + 1));
       if (bb == 4) {
         set_smem(k_c4_dense<true>, sm);
-        k_c4_dense<true><<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[bb],
-                                                     cnt[bb], cur, (long long)(c->dmax + 1),
-                                                     queues + 2, c4);
+        k_c4_dense<true><<<g, kC4DenseThreads, sm, c->stream>>>(
+            c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
+            bnd, nact, queues + 2, c4);
       } else {
         set_smem(k_c4_dense<false>, sm);
-        k_c4_dense<false><<<g, 1024, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[bb],
-                                                      cnt[bb], cur, (long long)(c->dmax + 1),
-                                                      queues + 3, c4);
+        k_c4_dense<false><<<g, kC4DenseThreads, sm, c->stream>>>(
+            c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
+            bnd, nact, queues + 3, c4);
       }
       check_launch();
       c->launched();

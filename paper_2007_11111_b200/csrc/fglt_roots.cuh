@@ -257,8 +257,10 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 constexpr int kC4HashLog = 14;              // 16384 slots (keys + counts = 128 KB)
 constexpr int kC4SmallLog = 12;             // 4096 slots (32 KB)
 constexpr u64 kC4HashFill = 12288;          // distinct targets per pass (LF 0.75)
-constexpr int kC4Tile16 = 98304;            // ids per packed tile (192 KB)
-constexpr int kC4Tile32 = 49152;            // ids per 32-bit tile (192 KB)
+constexpr int kC4DenseThreads = 1024;       // one dense block per SM (the tile takes the smem)
+constexpr int kC4TileBytes = 196608;        // counter tile per block (192 KB)
+constexpr int kC4Tile16 = kC4TileBytes / 2; // ids per packed tile
+constexpr int kC4Tile32 = kC4TileBytes / 4; // ids per 32-bit tile
 constexpr int kC4Long = 48;                 // rows at least this long: flattened batches
 constexpr int kQuadsInFlight = 2;          // 16-byte loads in flight per lane (dense batches)
 
@@ -284,7 +286,7 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       const bool pack = nq < 65536;
       const u64 tile = pack ? kC4Tile16 : kC4Tile32;
       const u64 tiles = ((u64)u + tile - 1) / tile;
-      const u64 cost_dense = tiles * (2 * 49152 / 4 + nq) + 2 * w;
+      const u64 cost_dense = tiles * (kC4TileBytes / 8 + nq) + 2 * w;
       if (cost_hash <= cost_dense) c = 4;
       else c = pack ? 5 : 6;
     }
@@ -475,20 +477,37 @@ __device__ __forceinline__ int upper_row(const int* g_off, int k, int n) {
   return lo;
 }
 
+// Absolute tile boundaries of the active rows, shared by every dense root:
+// bnd[k * nact + v] = first position in N(v) with id >= k * kC4Tile32
+// (k = 0..K-1). A row's segment in a tile is then two independent loads
+// instead of a dependent binary search per (root, row, tile).
+__global__ void k_tile_bounds(const int* __restrict__ rp, const int* __restrict__ ci, int nact,
+                              int K, int* __restrict__ bnd) {
+  const long long total = (long long)K * nact;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i / nact);
+    const int v = (int)(i - (long long)k * nact);
+    bnd[i] = k == 0 ? rp[v] : lower_bound_i32(ci, rp[v], rp[v + 1], k * kC4Tile32);
+  }
+}
+
 template <bool PACK>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(kC4DenseThreads, 1024 / kC4DenseThreads)
 k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, int* __restrict__ cursor,
-           long long cursor_stride, int* __restrict__ next_root, u64* __restrict__ c4) {
+           long long cursor_stride, const int* __restrict__ bnd, long long bnd_stride,
+           int* __restrict__ next_root, u64* __restrict__ c4) {
   // roots are sorted by work (largest first) and handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
-  __shared__ u64 rsum[32][32];
-  __shared__ int bst_all[32][32];
-  __shared__ int boff_all[32][33];
-  __shared__ int bsa_all[32][32];  // per-batch row [start, end) in ci
-  __shared__ int bsb_all[32][32];
+  constexpr int NW = kC4DenseThreads / 32;
+  __shared__ u64 rsum[NW][32];
+  __shared__ int bst_all[NW][32];
+  __shared__ int boff_all[NW][33];
+  __shared__ int bsa_all[NW][32];  // per-batch row [start, end) in ci
+  __shared__ int bsb_all[NW][32];
   __shared__ int next_batch[2];
   __shared__ int next_giant[2];
   constexpr int TILE = PACK ? kC4Tile16 : kC4Tile32;
@@ -542,6 +561,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     for (int lo = 0; lo < u; lo += TILE) {
       const int hi = min(lo + TILE, u);
       const int words = PACK ? (hi - lo + 1) >> 1 : hi - lo;
+      const long long kb_lo = lo / kC4Tile32, kb_hi = kb_lo + TILE / kC4Tile32;
       {
         uint4* L4 = reinterpret_cast<uint4*>(L);
         const int n4 = (words + 3) >> 2;
@@ -560,9 +580,17 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         gi = __shfl_sync(0xffffffffu, gi, 0);
         const int q = nq - 1 - gi;
         if (q < qg) break;
-        const int st = cur[q];
         const int em = mir[b + q];
-        const int se = hi >= u ? em : warp_lower_bound(ci, st, em, hi);
+        int st, se;
+        if (bnd) {
+          const int v = ci[b + q];
+          st = bnd[kb_lo * bnd_stride + v];
+          se = hi >= u ? em : min(em, bnd[kb_hi * bnd_stride + v]);
+          if (lane == 0) cur[q] = st;
+        } else {
+          st = cur[q];
+          se = hi >= u ? em : warp_lower_bound(ci, st, em, hi);
+        }
         if (lane == 0) segend[q] = se;
         warp_for_each(ci, st, se, [&](int w) { inc(w - lo); });
       }
@@ -584,9 +612,16 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         const bool valid = q < qg;
         int st = 0, se = 0;
         if (valid) {
-          st = cur[q];
           const int em = mir[b + q];
-          se = hi >= u ? em : lower_bound_i32(ci, st, em, hi);
+          if (bnd) {
+            const int v = ci[b + q];
+            st = bnd[kb_lo * bnd_stride + v];
+            se = hi >= u ? em : min(em, bnd[kb_hi * bnd_stride + v]);
+            cur[q] = st;
+          } else {
+            st = cur[q];
+            se = hi >= u ? em : lower_bound_i32(ci, st, em, hi);
+          }
           segend[q] = se;
         }
         // flattened over 16-byte quads of ci: quad k of row r is ci[4 (bst[r] + k)]
