@@ -654,11 +654,14 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       DISPATCH_G(G, launch_c4_hashp, c, g, 128, sm, lists[2], cnt[2], wc, parts, kC4SmallLog,
                  queues + 0, c4);
     }
-    if (cnt[3] > 0) {  // class 4: hash-partition passes
+    if (cnt[3] > 0) {  // class 4: block-flattened hash-partition passes
       const size_t sm = (size_t)(1 << kC4HashLog) * 8;
       const int g = std::min(cnt[3], c->sms);
-      DISPATCH_G(G, launch_c4_hashp, c, g, 512, sm, lists[3], cnt[3], wc, parts, kC4HashLog,
-                 queues + 1, c4);
+      set_smem(k_c4_block<kC4BlockThreads>, sm);
+      k_c4_block<kC4BlockThreads><<<g, kC4BlockThreads, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->mir, lists[3], cnt[3], wc, parts, kC4HashLog, queues + 1, c4);
+      check_launch();
+      c->launched();
     }
     int* bnd = nullptr;  // absolute tile boundaries of the active rows
     const long long nact = (long long)c->nact;

@@ -263,6 +263,7 @@ constexpr int kC4Tile16 = kC4TileBytes / 2; // ids per packed tile
 constexpr int kC4Tile32 = kC4TileBytes / 4; // ids per 32-bit tile
 constexpr int kC4Long = 48;                 // rows at least this long: flattened batches
 constexpr int kQuadsInFlight = 2;          // 16-byte loads in flight per lane (dense batches)
+constexpr int kC4BlockThreads = 1024;      // class-4 block (one 128 KB table per SM)
 
 __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
                            const u64* __restrict__ wc, int u0, int u1, u64* __restrict__ cls,
@@ -475,6 +476,146 @@ __device__ __forceinline__ int upper_row(const int* g_off, int k, int n) {
     if (g_off[mid] <= k) lo = mid; else hi = mid;
   }
   return lo;
+}
+
+// Block per root, hash table in shared memory, P hash-partition passes.
+// The rows of N-(u) are flattened block-wide over 16-byte quads of ci, in
+// chunks of NT rows; each warp owns an equal contiguous share of the quads
+// (one binary search per lane to find its first row, then a forward walk), so
+// a root's work is balanced across all warps with no per-row serial loops.
+template <int NT>
+__global__ void __launch_bounds__(NT)
+k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
+           const int* __restrict__ split, const int* __restrict__ mir,
+           const int* __restrict__ roots, int nroots, const u64* __restrict__ wcv,
+           const u64* __restrict__ parts, int max_log, int* __restrict__ next_root,
+           u64* __restrict__ c4) {
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ u64 red[32];
+  __shared__ int g_off[NT + 1];  // quad offsets of the chunk's rows
+  __shared__ int g_st[NT];       // quad k of row r is ci quad g_st[r] + k
+  __shared__ int g_sa[NT], g_sb[NT];  // row element range [sa, sb)
+  __shared__ u64 rowsum[NT];
+  __shared__ int wtot[32];
+  __shared__ int s_root;
+  const int maxcap = 1 << max_log;
+  int* keys = reinterpret_cast<int*>(smem_raw);
+  u32* vals = reinterpret_cast<u32*>(keys + maxcap);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  rowsum[threadIdx.x] = 0;
+  while (true) {
+    if (threadIdx.x == 0) s_root = atomicAdd(next_root, 1);
+    __syncthreads();
+    const int k = s_root;
+    if (k >= nroots) break;
+    const int u = roots[k];
+    const u32 P = (u32)parts[u];
+    const u64 per_pass = (wcv[u] + P - 1) / P;
+    int hlog = 6;
+    while (hlog < max_log && ((u64)1 << hlog) < 2 * per_pass) ++hlog;
+    const int cap = 1 << hlog;
+    const int b = rp[u], s = split[u];
+    u64 acc = 0;
+    // flatten rows [c0, c0 + NT) of N-(u); returns the quad count
+    auto flatten = [&](int c0) -> int {
+      const int q = c0 + threadIdx.x;
+      int st = 0, se = 0;
+      if (q < s) {
+        st = rp[ci[q]];
+        se = mir[q];
+      }
+      const int qa = st >> 2;
+      const int nqd = se > st ? ((se + 3) >> 2) - qa : 0;
+      g_sa[threadIdx.x] = st;
+      g_sb[threadIdx.x] = se;
+      return block_flatten(nqd, qa, g_off, g_st, wtot);  // g_st = qa - off
+    };
+    // visit every wedge target of the chunk: f(row, w)
+    auto sweep_quads = [&](int T, auto&& f) {
+      const int per = (T + NW - 1) / NW;
+      const int k0 = wid * per, k1 = min(T, k0 + per);
+      if (k0 + lane >= k1) return;
+      int r = upper_row(g_off, k0 + lane, NT);
+      for (int kk = k0 + lane; kk < k1; kk += 32 * kQuadsInFlight) {
+        int4 v[kQuadsInFlight];
+        int lt[kQuadsInFlight], ht[kQuadsInFlight], rr[kQuadsInFlight];
+#pragma unroll
+        for (int j = 0; j < kQuadsInFlight; ++j) {
+          const int kj = kk + 32 * j;
+          lt[j] = 4;
+          ht[j] = 0;
+          rr[j] = r;
+          if (kj < k1) {
+            while (g_off[r + 1] <= kj) ++r;
+            rr[j] = r;
+            const int e0 = (g_st[r] + kj) << 2;
+            v[j] = __ldg(reinterpret_cast<const int4*>(ci + e0));
+            lt[j] = g_sa[r] - e0;
+            ht[j] = g_sb[r] - e0;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kQuadsInFlight; ++j) {
+          if (lt[j] <= 0 && ht[j] > 0) f(rr[j], v[j].x);
+          if (lt[j] <= 1 && ht[j] > 1) f(rr[j], v[j].y);
+          if (lt[j] <= 2 && ht[j] > 2) f(rr[j], v[j].z);
+          if (lt[j] <= 3 && ht[j] > 3) f(rr[j], v[j].w);
+        }
+      }
+    };
+    for (u32 part = 0; part < P; ++part) {
+      {
+        uint4* k4 = reinterpret_cast<uint4*>(keys);
+        uint4* v4 = reinterpret_cast<uint4*>(vals);
+        for (int i = threadIdx.x; i < (cap >> 2); i += NT) {
+          k4[i] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+          v4[i] = make_uint4(0, 0, 0, 0);
+        }
+      }
+      // count pass (block_flatten's barriers order the clear before inserts)
+      for (int c0 = b; c0 < s; c0 += NT) {
+        const int T = flatten(c0);
+        sweep_quads(T, [&](int, int w) {
+          if (P == 1 || part_of(w, P) == part) hash_insert(keys, vals, hlog, w);
+        });
+        __syncthreads();
+      }
+      for (int i = threadIdx.x; i < cap; i += NT) {
+        const u32 l = vals[i];
+        if (l >= 2) {
+          const u64 c = (u64)l * (l - 1) / 2;
+          acc += c;
+          atomicAdd(c4 + keys[i], c);
+        }
+      }
+      // attribution pass: c4[v] += sum_w (L[w] - 1)
+      for (int c0 = b; c0 < s; c0 += NT) {
+        const int T = flatten(c0);
+        int cr = -1;
+        u64 part_sum = 0;
+        sweep_quads(T, [&](int r, int w) {
+          if (P == 1 || part_of(w, P) == part) {
+            if (r != cr) {
+              if (part_sum) smem_add_u64(rowsum + cr, part_sum);
+              part_sum = 0;
+              cr = r;
+            }
+            part_sum += hash_get(keys, vals, hlog, w) - 1;
+          }
+        });
+        if (part_sum) smem_add_u64(rowsum + cr, part_sum);
+        __syncthreads();
+        const int q = c0 + threadIdx.x;
+        if (q < s && rowsum[threadIdx.x]) atomicAdd(c4 + ci[q], rowsum[threadIdx.x]);
+        rowsum[threadIdx.x] = 0;
+      }
+      __syncthreads();
+    }
+    acc = block_sum_u64(acc, red);
+    if (threadIdx.x == 0 && acc) atomicAdd(c4 + u, acc);
+    __syncthreads();
+  }
 }
 
 // Absolute tile boundaries of the active rows, shared by every dense root:
