@@ -62,7 +62,7 @@ constexpr int kWarpHashLog2 = 11; // 2048-slot table per warp (wc <= 1024)
 enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
-  B_CUB, B_CURSOR, B_TBND, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
+  B_CUB, B_CURSOR, B_TBND, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV, B_COUNT
 };
 
@@ -366,9 +366,14 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, ndeg, nrp, N + 1, c->stream));
   tmp_bytes = std::max(tmp_bytes, t2);
   size_t t3 = 0;
+  int id_bits = 1;
+  while (id_bits < 31 && ((int64_t)1 << id_bits) < n) ++id_bits;
   int* tmp = c->ensure<int>(B_TMP, std::max<int64_t>(nnz, 1));
+  int* row_of = c->ensure<int>(B_ROWOF, std::max<int64_t>(nnz, 1));
+  int* keys_out = c->ensure<int>(B_KEYSOUT, std::max<int64_t>(nnz, 1));
   int* nci = c->ensure<int>(B_NCI, std::max<int64_t>(nnz, 1) + 4);  // +4: 16-byte tail reads
-  CK(cub::DeviceSegmentedSort::SortKeys(nullptr, t3, tmp, nci, (int)nnz, N, nrp, nrp + 1, c->stream));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, tmp, keys_out, row_of, nci, (int)nnz, 0, id_bits,
+                                     c->stream));
   tmp_bytes = std::max(tmp_bytes, t3);
   void* cub_tmp = c->ensure<unsigned char>(B_CUB, tmp_bytes);
   size_t tb = c->buf[B_CUB].cap;
@@ -381,13 +386,14 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   tb = c->buf[B_CUB].cap;
   CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ndeg, nrp, N + 1, c->stream));
   c->launched();
-  k_fill_rows<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(d_rp, d_ci, perm, inv, nrp, N, tmp);
+  k_fill_rows<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(d_rp, d_ci, perm, inv, nrp, N, tmp,
+                                                           row_of);
   check_launch();
   c->launched();
   tb = c->buf[B_CUB].cap;
-  if (nnz > 0) {
-    CK(cub::DeviceSegmentedSort::SortKeys(cub_tmp, tb, tmp, nci, (int)nnz, N, nrp, nrp + 1,
-                                          c->stream));
+  if (nnz > 0) {  // stable sort by neighbour id: rows come out sorted (see k_fill_rows)
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, tmp, keys_out, row_of, nci, (int)nnz, 0,
+                                       id_bits, c->stream));
     c->launched();
   }
   c->perm = perm;

@@ -144,16 +144,25 @@ __global__ void k_perm(const u64* __restrict__ keys, int n, int* __restrict__ pe
   }
 }
 
-// Warp per new row: copy the relabelled neighbours of the old row.
+// Warp per new row r: the relabelled neighbours of the old row (unsorted) and
+// the row id of each. The array is r-major, so a STABLE sort of these pairs
+// by neighbour id lists, for every vertex y, its neighbours r in ascending
+// order: the transpose of a symmetric graph is the graph itself, so that sort
+// yields the sorted relabelled CSR (a 20-bit key sort instead of a sort of
+// every row).
 __global__ void k_fill_rows(const int* __restrict__ rp, const int* __restrict__ ci,
                             const int* __restrict__ perm, const int* __restrict__ inv,
-                            const int* __restrict__ nrp, int n, int* __restrict__ out) {
+                            const int* __restrict__ nrp, int n, int* __restrict__ out,
+                            int* __restrict__ row_of) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
     const int o = perm[r];
     const int b = rp[o], e = rp[o + 1], w = nrp[r];
-    for (int p = b + lane; p < e; p += 32) out[w + (p - b)] = inv[ci[p]];
+    for (int p = b + lane; p < e; p += 32) {
+      out[w + (p - b)] = inv[ci[p]];
+      row_of[w + (p - b)] = r;
+    }
   }
 }
 

@@ -1096,8 +1096,11 @@ __device__ __forceinline__ int s_hash_find(const int* keys, const unsigned short
   }
 }
 
+constexpr int kRootsThreads = 256;
+constexpr int kRootsWarps = kRootsThreads / 32;
+
 template <bool kC3, bool kD13, bool kD15, bool kGlobal>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kRootsThreads)
 k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
               const int* __restrict__ split, const int* __restrict__ send,
               u32* __restrict__ C3f,
@@ -1108,6 +1111,9 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
   __shared__ int next_item[2];
+  __shared__ int f_off[kRootsThreads + 1], f_st[kRootsThreads];  // probe flattening
+  __shared__ int f_sa[kRootsThreads], f_sb[kRootsThreads];
+  __shared__ int f_wtot[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u64* sD = reinterpret_cast<u64*>(smem_raw);
   int* sS = reinterpret_cast<int*>(sD + L.s_cap);
@@ -1163,59 +1169,97 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     // (no carry) when s * deg(u) < 2^32
     const bool narrow = (u64)s * (u64)(rp[u + 1] - rp[u]) < (1ull << 32);
     u64 tu = 0;
-    // ---- probe: every triangle {u, S[a], S[b]} with a < b, once
-    while (true) {
-      int a = 0;
-      if (lane == 0) a = atomicAdd(next_item, 1);
-      a = __shfl_sync(0xffffffffu, a, 0);
-      if (a + 1 >= s) break;
-      const int x = sS[a];
-      const u32 ca = kD13 ? sC[a] : 0u;
-      const int e = rp[x + 1];
-      u64 da = 0;
-      u32 na = 0;
-      // software-pipelined: the next chunk's load is in flight while this
-      // chunk's lookups run
-      int p = split[x] + lane;
-      int y = p < e ? __ldg(ci + p) : 0x7fffffff;
-      for (int base = split[x]; base < e; base += 32) {
-        const int pn = p + 32;
-        const int ylast = __shfl_sync(0xffffffffu, y, 31);  // chunk max (rows are sorted)
-        const int yn = (pn < e && ylast < smax) ? __ldg(ci + pn) : 0x7fffffff;
-        if (y <= smax) {
-          const int bi = s_hash_find(hkeys, hidx, hlog, y);
-          FGLT_BOUNDS(bi < s && (bi < 0 || bi > a), "bi", bi, a);
-          if (bi >= 0) {
-            if (kD15) {
-              atomicOr(bm + (long long)a * stride + (bi >> 5), 1u << (bi & 31));
-              atomicOr(bm + (long long)bi * stride + (a >> 5), 1u << (a & 31));
+    // ---- probe: every triangle {u, S[a], S[b]} with a < b, once. The
+    // probe lists N+(S[a]) cut at max S are flattened block-wide over 16-byte
+    // quads, NT members per chunk; each warp owns an equal share of quads.
+    for (int c0 = 0; c0 + 1 < s; c0 += kRootsThreads) {
+      {
+        const int a = c0 + threadIdx.x;
+        int st = 0, se = 0;
+        if (a + 1 < s) {
+          const int x = sS[a];
+          st = split[x];
+          se = lower_bound_i32(ci, st, rp[x + 1], smax + 1);
+        }
+        const int qa = st >> 2;
+        const int nqd = se > st ? ((se + 3) >> 2) - qa : 0;
+        f_sa[threadIdx.x] = st;
+        f_sb[threadIdx.x] = se;
+        block_flatten(nqd, qa, f_off, f_st, f_wtot);
+      }
+      const int T = f_off[kRootsThreads];
+      const int per = (T + kRootsWarps - 1) / kRootsWarps;
+      const int k0 = wid * per, k1 = min(T, k0 + per);
+      if (k0 + lane < k1) {
+        int r = upper_row(f_off, k0 + lane, kRootsThreads);
+        int cr = -1;
+        u32 ca = 0, na = 0;
+        u64 da = 0;
+        auto flush = [&]() {
+          if (cr < 0) return;
+          if (kC3 && na) atomicAdd(sC + c0 + cr, na);
+          if (kD13 && da) smem_add_u64(sD + c0 + cr, da);
+        };
+        for (int kk = k0 + lane; kk < k1; kk += 32 * kQuadsInFlight) {
+          int4 v[kQuadsInFlight];
+          int lt[kQuadsInFlight], ht[kQuadsInFlight], rr[kQuadsInFlight], e0[kQuadsInFlight];
+#pragma unroll
+          for (int j = 0; j < kQuadsInFlight; ++j) {
+            const int kj = kk + 32 * j;
+            lt[j] = 4;
+            ht[j] = 0;
+            rr[j] = r;
+            e0[j] = 0;
+            if (kj < k1) {
+              while (f_off[r + 1] <= kj) ++r;
+              rr[j] = r;
+              e0[j] = (f_st[r] + kj) << 2;
+              v[j] = __ldg(reinterpret_cast<const int4*>(ci + e0[j]));
+              lt[j] = f_sa[r] - e0[j];
+              ht[j] = f_sb[r] - e0[j];
             }
-            if (kC3) {
-              atomicAdd(C3f + p, 1u);
-              atomicAdd(sC + bi, 1u);
-              ++na;
+          }
+#pragma unroll
+          for (int j = 0; j < kQuadsInFlight; ++j) {
+            if (ht[j] <= 0) break;
+            if (rr[j] != cr) {
+              flush();
+              cr = rr[j];
+              na = 0;
+              da = 0;
+              if (kD13) ca = sC[c0 + cr];
             }
-            if (kD13) {
-              tu += (u64)__ldg(C3f + p) - 1;
-              da += (u64)sC[bi] - 1;
-              if (narrow) atomicAdd(reinterpret_cast<u32*>(sD + bi), ca - 1);
-              else smem_add_u64(sD + bi, (u64)ca - 1);
+            const int a = c0 + cr;
+            const int ys[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              if (t < lt[j] || t >= ht[j]) continue;
+              const int y = ys[t];
+              const int bi = s_hash_find(hkeys, hidx, hlog, y);
+              FGLT_BOUNDS(bi < s && (bi < 0 || bi > a), "bi", bi, a);
+              if (bi < 0) continue;
+              const int p = e0[j] + t;
+              if (kD15) {
+                atomicOr(bm + (long long)a * stride + (bi >> 5), 1u << (bi & 31));
+                atomicOr(bm + (long long)bi * stride + (a >> 5), 1u << (a & 31));
+              }
+              if (kC3) {
+                atomicAdd(C3f + p, 1u);
+                atomicAdd(sC + bi, 1u);
+                ++na;
+              }
+              if (kD13) {
+                tu += (u64)__ldg(C3f + p) - 1;
+                da += (u64)sC[bi] - 1;
+                if (narrow) atomicAdd(reinterpret_cast<u32*>(sD + bi), ca - 1);
+                else smem_add_u64(sD + bi, (u64)ca - 1);
+              }
             }
           }
         }
-        if (ylast >= smax) break;
-        p = pn;
-        y = yn;
+        flush();
       }
-      if (kC3) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) na += __shfl_xor_sync(0xffffffffu, na, o);
-        if (lane == 0 && na) atomicAdd(sC + a, na);
-      }
-      if (kD13) {
-        da = warp_sum_u64(da);
-        if (lane == 0 && da) smem_add_u64(sD + a, da);
-      }
+      __syncthreads();  // f_* are rewritten by the next chunk
     }
     __syncthreads();
     if (kC3)
