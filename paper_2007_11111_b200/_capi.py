@@ -28,7 +28,7 @@ EXPORTS = [
     "fglt_csr_fetch",
 ]
 
-DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN = 1, 2, 3
+DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB = 1, 2, 3, 4
 
 
 class FgltError(ctypes.Structure):

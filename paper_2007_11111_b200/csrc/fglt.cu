@@ -62,7 +62,7 @@ constexpr int kWarpHashLog2 = 11; // 2048-slot table per warp (wc <= 1024)
 enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
-  B_CUB, B_CURSOR, B_TBND, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
+  B_CUB, B_CURSOR, B_TBND, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV, B_COUNT
 };
 
@@ -211,7 +211,12 @@ struct fglt_ctx {
   int* rb_lists[8] = {};
 
   // test hooks (fglt_ctx_set_debug): force one code path for every root
-  int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1;
+  int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1, force_hub = 0;
+  // hub rows (k_hub_rows): built once per graph by the first root pass
+  bool hub_built = false;
+  unsigned long long* hub = nullptr;
+  int* hub_base = nullptr;
+  int hub_hb = 0;
 
   // timing
   bool timing = false;
@@ -340,6 +345,7 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   CK(cudaMemsetAsync(c->vec, 0, (size_t)V_COUNT * std::max<int64_t>(n, 1) * 8, c->stream));
   c->perm = c->inv = nullptr;
   c->rb_u0 = c->rb_u1 = -1;  // graph changed: root bins are stale
+  c->hub_built = false;
   c->rb_cnt.clear();
   c->rp = d_rp;
   c->ci = d_ci;
@@ -531,7 +537,38 @@ void sort_by_work_desc(fglt_ctx* c, int* list, int cnt, const u64* w) {
 }
 
 // Bin roots [u0,u1) by |N+(u)| (>= 2) once; both root passes reuse the lists.
+void build_hubs(fglt_ctx* c) {
+  if (c->hub_built) return;
+  c->hub_built = true;
+  c->hub = nullptr;
+  const int64_t nact = (int64_t)c->nact;
+  if (c->force_hub == 1 || nact < 2) return;
+  const int R = (int)std::min<int64_t>(nact, kHubMax);
+  c->hub_hb = (int)(nact - R);
+  int* hw = c->ensure<int>(B_HUBBASE, 2 * (size_t)(R + 1));
+  int* base = hw + (R + 1);
+  k_hub_words<<<c->grid(R + 1, 256), 256, 0, c->stream>>>(R, hw);
+  check_launch();
+  c->launched();
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, hw, base, R + 1, c->stream));
+  void* tmp = c->ensure<unsigned char>(B_CUB, tb);
+  tb = c->buf[B_CUB].cap;
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tb, hw, base, R + 1, c->stream));
+  c->launched();
+  // words = sum_i ceil((R-1-i)/32), computed on the host
+  size_t words = 0;
+  for (int i = 0; i < R; ++i) words += (size_t)((R - 1 - i + 31) >> 5);
+  c->hub = c->ensure<unsigned long long>(B_HUB, std::max<size_t>(words, 1));
+  k_hub_rows<<<c->grid((int64_t)R * 32, 256), 256, 0, c->stream>>>(c->ci, c->split, c->send,
+                                                                  c->hub_hb, R, base, c->hub);
+  check_launch();
+  c->launched();
+  c->hub_base = base;
+}
+
 void root_bins(fglt_ctx* c, int64_t u0, int64_t u1) {
+  build_hubs(c);
   if (c->rb_u0 == u0 && c->rb_u1 == u1 && !c->rb_cnt.empty()) return;
   u64* key = c->ensure<u64>(B_RKEY, (size_t)std::max<int64_t>(c->n, 1));
   static const u64 kForceKey[] = {0, 33, 129, 257, 513, 1025};
@@ -577,7 +614,7 @@ void roots_pass(fglt_ctx* c) {
     L.hlog = 6;
     while ((1 << L.hlog) < 4 * L.s_cap) ++L.hlog;
     L.hcap = 1 << L.hlog;
-    L.nwarps = 8;
+    L.nwarps = kRootsWarps;
     L.stride_cap = ((L.s_cap + 31) / 32) | 1;
     size_t sm = L.bytes_core();
     unsigned char* slab = nullptr;
@@ -589,13 +626,15 @@ void roots_pass(fglt_ctx* c) {
       g = (int)std::min<long long>({(long long)cnt[b], (long long)c->sms, fit});
       slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
       set_smem(k_roots_block<kC3, kD13, kD15, true>, sm);
-      k_roots_block<kC3, kD13, kD15, true><<<g, 256, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15);
+      k_roots_block<kC3, kD13, kD15, true><<<g, kRootsThreads, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15,
+          c->hub, c->hub_base, c->hub_hb, c->force_hub == 2);
     } else {
       sm += L.bytes_aux();
       set_smem(k_roots_block<kC3, kD13, kD15, false>, sm);
-      k_roots_block<kC3, kD13, kD15, false><<<g, 256, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15);
+      k_roots_block<kC3, kD13, kD15, false><<<g, kRootsThreads, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15,
+          c->hub, c->hub_base, c->hub_hb, c->force_hub == 2);
     }
     check_launch();
     c->launched();
@@ -996,6 +1035,7 @@ int fglt_ctx_set_debug(fglt_ctx* c, int key, int value) {
     case FGLT_DEBUG_C4_CLASS: c->force_c4_class = value; return FGLT_OK;
     case FGLT_DEBUG_C4_PARTS: c->force_c4_parts = value; return FGLT_OK;
     case FGLT_DEBUG_ROOTS_BIN: c->force_roots_bin = value; return FGLT_OK;
+    case FGLT_DEBUG_HUB: c->force_hub = value; c->hub_built = false; return FGLT_OK;
     default: return FGLT_E_PARSE;
   }
 }

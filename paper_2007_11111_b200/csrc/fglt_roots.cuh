@@ -1096,7 +1096,43 @@ __device__ __forceinline__ int s_hash_find(const int* keys, const unsigned short
   }
 }
 
+// ---- hub rows. The R highest-ranked active vertices [hb, n_active) (the
+// highest-degree ones, after the relabel) get a packed adjacency row over the
+// ids above them: for x = hb + i, word k of row i covers ids x+1+32k ..
+// x+32+32k; low 32 bits = adjacency, high 32 bits = number of N+(x) entries
+// before the word (so the CSR position of (x, y) is split[x] + high +
+// popc(low below y)). Rows are ceil((R-1-i)/32) words, packed back to back.
+constexpr int kHubMax = 16384;  // R cap: R^2/8 bytes of rows (32 MB), L2-resident
+
+__global__ void k_hub_words(int R, int* __restrict__ w) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= R; i += gridDim.x * blockDim.x)
+    w[i] = i < R ? (R - 1 - i + 31) >> 5 : 0;
+}
+
+// Warp per hub row (hub_base = exclusive scan of k_hub_words).
+__global__ void k_hub_rows(const int* __restrict__ ci, const int* __restrict__ split,
+                           const int* __restrict__ send, int hb, int R,
+                           const int* __restrict__ hub_base, unsigned long long* __restrict__ hub) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < R; i += warps) {
+    const int x = hb + i;
+    const int base = hub_base[i], nw = hub_base[i + 1] - base;
+    const int st = split[x], en = send[x];  // N+(x): ids in (x, n_active)
+    for (int k = lane; k < nw; k += 32) {
+      const int before = lower_bound_i32(ci, st, en, x + 1 + 32 * k) - st;
+      hub[base + k] = (unsigned long long)before << 32;
+    }
+    __syncwarp();
+    for (int j = st + lane; j < en; j += 32) {
+      const int o = ci[j] - x - 1;
+      atomicOr(reinterpret_cast<unsigned*>(hub + base + (o >> 5)), 1u << (o & 31));
+    }
+  }
+}
+
 constexpr int kRootsThreads = 256;
+constexpr int kPairsInFlight = 4;  // hub-row words in flight per lane
 constexpr int kRootsWarps = kRootsThreads / 32;
 
 template <bool kC3, bool kD13, bool kD15, bool kGlobal>
@@ -1106,13 +1142,15 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
               u32* __restrict__ C3f,
               const int* __restrict__ roots, int nroots, RootsLayout L,
               unsigned char* __restrict__ slab, long long slab_stride,
-              int* __restrict__ next_root, u64* __restrict__ d13, u64* __restrict__ d15) {
+              int* __restrict__ next_root, u64* __restrict__ d13, u64* __restrict__ d15,
+              const unsigned long long* __restrict__ hub, const int* __restrict__ hub_base,
+              int hb, int hub_force) {
   // roots sorted by |S| (largest first), handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
   __shared__ int next_item[2];
   __shared__ int f_off[kRootsThreads + 1], f_st[kRootsThreads];  // probe flattening
-  __shared__ int f_sa[kRootsThreads], f_sb[kRootsThreads];
+  __shared__ int f_sa[kRootsThreads], f_sb[kRootsThreads], f_hb[kRootsThreads];
   __shared__ int f_wtot[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u64* sD = reinterpret_cast<u64*>(smem_raw);
@@ -1169,97 +1207,155 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     // (no carry) when s * deg(u) < 2^32
     const bool narrow = (u64)s * (u64)(rp[u + 1] - rp[u]) < (1ull << 32);
     u64 tu = 0;
-    // ---- probe: every triangle {u, S[a], S[b]} with a < b, once. The
-    // probe lists N+(S[a]) cut at max S are flattened block-wide over 16-byte
-    // quads, NT members per chunk; each warp owns an equal share of quads.
+    // ---- every triangle {u, S[a], S[b]} with a < b, once, found from
+    // member a by one of two means, chosen per member:
+    //   probe: N+(S[a]) cut at max S, flattened block-wide over 16-byte quads
+    //          of ci and looked up in the hash of S;
+    //   pairs: S[a] is a hub (id >= hb): test S[b], b > a, against the
+    //          packed adjacency row of S[a] (k_hub_rows), which also gives the
+    //          CSR position of (S[a], S[b]) by a popcount rank.
+    // Per-row partials (na, da) are flushed when a lane's row changes.
+    int cr = -1;
+    u32 ca = 0, na = 0;
+    u64 da = 0;
+    auto flush = [&](int c0) {
+      if (cr < 0) return;
+      if (kC3 && na) atomicAdd(sC + c0 + cr, na);
+      if (kD13 && da) smem_add_u64(sD + c0 + cr, da);
+      cr = -1;
+    };
+    auto to_row = [&](int c0, int r) {
+      if (r != cr) {
+        flush(c0);
+        cr = r;
+        na = 0;
+        da = 0;
+        if (kD13) ca = sC[c0 + r];
+      }
+    };
+    auto hit = [&](int a, int bi, int p) {
+      if (kD15) {
+        atomicOr(bm + (long long)a * stride + (bi >> 5), 1u << (bi & 31));
+        atomicOr(bm + (long long)bi * stride + (a >> 5), 1u << (a & 31));
+      }
+      if (kC3) {
+        atomicAdd(C3f + p, 1u);
+        atomicAdd(sC + bi, 1u);
+        ++na;
+      }
+      if (kD13) {
+        tu += (u64)__ldg(C3f + p) - 1;
+        da += (u64)sC[bi] - 1;
+        if (narrow) atomicAdd(reinterpret_cast<u32*>(sD + bi), ca - 1);
+        else smem_add_u64(sD + bi, (u64)ca - 1);
+      }
+    };
     for (int c0 = 0; c0 + 1 < s; c0 += kRootsThreads) {
+      const int a_me = c0 + threadIdx.x;
+      int x = 0, st = 0, se = 0;
+      bool pairs = false;
+      if (a_me + 1 < s) {
+        x = sS[a_me];
+        st = split[x];
+        se = lower_bound_i32(ci, st, rp[x + 1], smax + 1);
+        pairs = hub != nullptr && x >= hb && (hub_force || 2 * (s - 1 - a_me) < se - st);
+      }
+      // probe rows
       {
-        const int a = c0 + threadIdx.x;
-        int st = 0, se = 0;
-        if (a + 1 < s) {
-          const int x = sS[a];
-          st = split[x];
-          se = lower_bound_i32(ci, st, rp[x + 1], smax + 1);
-        }
         const int qa = st >> 2;
-        const int nqd = se > st ? ((se + 3) >> 2) - qa : 0;
+        const int nqd = (!pairs && se > st) ? ((se + 3) >> 2) - qa : 0;
         f_sa[threadIdx.x] = st;
         f_sb[threadIdx.x] = se;
         block_flatten(nqd, qa, f_off, f_st, f_wtot);
       }
-      const int T = f_off[kRootsThreads];
-      const int per = (T + kRootsWarps - 1) / kRootsWarps;
-      const int k0 = wid * per, k1 = min(T, k0 + per);
-      if (k0 + lane < k1) {
-        int r = upper_row(f_off, k0 + lane, kRootsThreads);
-        int cr = -1;
-        u32 ca = 0, na = 0;
-        u64 da = 0;
-        auto flush = [&]() {
-          if (cr < 0) return;
-          if (kC3 && na) atomicAdd(sC + c0 + cr, na);
-          if (kD13 && da) smem_add_u64(sD + c0 + cr, da);
-        };
-        for (int kk = k0 + lane; kk < k1; kk += 32 * kQuadsInFlight) {
-          int4 v[kQuadsInFlight];
-          int lt[kQuadsInFlight], ht[kQuadsInFlight], rr[kQuadsInFlight], e0[kQuadsInFlight];
+      {
+        const int T = f_off[kRootsThreads];
+        const int per = (T + kRootsWarps - 1) / kRootsWarps;
+        const int k0 = wid * per, k1 = min(T, k0 + per);
+        if (k0 + lane < k1) {
+          int r = upper_row(f_off, k0 + lane, kRootsThreads);
+          for (int kk = k0 + lane; kk < k1; kk += 32 * kQuadsInFlight) {
+            int4 v[kQuadsInFlight];
+            int lt[kQuadsInFlight], ht[kQuadsInFlight], rr[kQuadsInFlight], e0[kQuadsInFlight];
 #pragma unroll
-          for (int j = 0; j < kQuadsInFlight; ++j) {
-            const int kj = kk + 32 * j;
-            lt[j] = 4;
-            ht[j] = 0;
-            rr[j] = r;
-            e0[j] = 0;
-            if (kj < k1) {
-              while (f_off[r + 1] <= kj) ++r;
+            for (int j = 0; j < kQuadsInFlight; ++j) {
+              const int kj = kk + 32 * j;
+              lt[j] = 4;
+              ht[j] = 0;
               rr[j] = r;
-              e0[j] = (f_st[r] + kj) << 2;
-              v[j] = __ldg(reinterpret_cast<const int4*>(ci + e0[j]));
-              lt[j] = f_sa[r] - e0[j];
-              ht[j] = f_sb[r] - e0[j];
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < kQuadsInFlight; ++j) {
-            if (ht[j] <= 0) break;
-            if (rr[j] != cr) {
-              flush();
-              cr = rr[j];
-              na = 0;
-              da = 0;
-              if (kD13) ca = sC[c0 + cr];
-            }
-            const int a = c0 + cr;
-            const int ys[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              if (t < lt[j] || t >= ht[j]) continue;
-              const int y = ys[t];
-              const int bi = s_hash_find(hkeys, hidx, hlog, y);
-              FGLT_BOUNDS(bi < s && (bi < 0 || bi > a), "bi", bi, a);
-              if (bi < 0) continue;
-              const int p = e0[j] + t;
-              if (kD15) {
-                atomicOr(bm + (long long)a * stride + (bi >> 5), 1u << (bi & 31));
-                atomicOr(bm + (long long)bi * stride + (a >> 5), 1u << (a & 31));
+              e0[j] = 0;
+              if (kj < k1) {
+                while (f_off[r + 1] <= kj) ++r;
+                rr[j] = r;
+                e0[j] = (f_st[r] + kj) << 2;
+                v[j] = __ldg(reinterpret_cast<const int4*>(ci + e0[j]));
+                lt[j] = f_sa[r] - e0[j];
+                ht[j] = f_sb[r] - e0[j];
               }
-              if (kC3) {
-                atomicAdd(C3f + p, 1u);
-                atomicAdd(sC + bi, 1u);
-                ++na;
-              }
-              if (kD13) {
-                tu += (u64)__ldg(C3f + p) - 1;
-                da += (u64)sC[bi] - 1;
-                if (narrow) atomicAdd(reinterpret_cast<u32*>(sD + bi), ca - 1);
-                else smem_add_u64(sD + bi, (u64)ca - 1);
+            }
+#pragma unroll
+            for (int j = 0; j < kQuadsInFlight; ++j) {
+              if (ht[j] <= 0) break;
+              to_row(c0, rr[j]);
+              const int a = c0 + rr[j];
+              const int ys[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                if (t < lt[j] || t >= ht[j]) continue;
+                const int bi = s_hash_find(hkeys, hidx, hlog, ys[t]);
+                FGLT_BOUNDS(bi < s && (bi < 0 || bi > a), "bi", bi, a);
+                if (bi >= 0) hit(a, bi, e0[j] + t);
               }
             }
           }
+          flush(c0);
         }
-        flush();
       }
-      __syncthreads();  // f_* are rewritten by the next chunk
+      __syncthreads();  // f_* are rewritten below
+      if (hub == nullptr) continue;
+      // pair rows
+      {
+        f_sa[threadIdx.x] = x;
+        f_sb[threadIdx.x] = st;
+        f_hb[threadIdx.x] = pairs ? hub_base[x - hb] : 0;
+        block_flatten(pairs ? s - 1 - a_me : 0, 0, f_off, f_st, f_wtot);
+      }
+      {
+        const int T = f_off[kRootsThreads];
+        const int per = (T + kRootsWarps - 1) / kRootsWarps;
+        const int k0 = wid * per, k1 = min(T, k0 + per);
+        if (k0 + lane < k1) {
+          int r = upper_row(f_off, k0 + lane, kRootsThreads);
+          for (int kk = k0 + lane; kk < k1; kk += 32 * kPairsInFlight) {
+            unsigned long long wv[kPairsInFlight];
+            int rr[kPairsInFlight], bb[kPairsInFlight], ob[kPairsInFlight];
+#pragma unroll
+            for (int j = 0; j < kPairsInFlight; ++j) {
+              const int kj = kk + 32 * j;
+              rr[j] = -1;
+              if (kj < k1) {
+                while (f_off[r + 1] <= kj) ++r;
+                rr[j] = r;
+                bb[j] = c0 + r + 1 + (kj - f_off[r]);
+                const int o = sS[bb[j]] - f_sa[r] - 1;
+                ob[j] = o & 31;
+                wv[j] = __ldg(hub + f_hb[r] + (o >> 5));
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < kPairsInFlight; ++j) {
+              if (rr[j] < 0) break;
+              const u32 bits = (u32)wv[j];
+              if (!((bits >> ob[j]) & 1u)) continue;
+              to_row(c0, rr[j]);
+              const int pos = f_sb[rr[j]] + (int)(wv[j] >> 32) + __popc(bits & ((1u << ob[j]) - 1u));
+              hit(c0 + rr[j], bb[j], pos);
+            }
+          }
+          flush(c0);
+        }
+      }
+      __syncthreads();
     }
     __syncthreads();
     if (kC3)

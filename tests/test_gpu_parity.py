@@ -234,6 +234,21 @@ def test_forced_code_paths(label, key, value, parts):
     c.close()
 
 
+@pytest.mark.parametrize("hub", [1, 2])
+@pytest.mark.parametrize("rbin", [1, 3, 5])
+def test_hub_rows_paths(hub, rbin):
+    """Hub-row pair checks (forced for every hub member) and the pure probe
+    path (hub rows off) must give the same bits, in every block bin."""
+    c = _capi.Context(0)
+    c.set_debug(_capi.DEBUG_HUB, hub)
+    c.set_debug(_capi.DEBUG_ROOTS_BIN, rbin)
+    cases = [gu.er(300, 0.15, 11), gu.complete(48), graphs.rmat(12, 16, seed=6),
+             graphs.sbm(64, 64, 0.3, 3.0, 4), gu.star(90), gu.demo()]
+    for rp, ci in cases:
+        check_same(c, rp, ci, d15_mode=1)
+    c.close()
+
+
 def test_repeat_determinism_at_scale():
     """Bit-identical results across repeated runs at a size where every
     root bin and 4-cycle class is populated (guards against lost updates;
