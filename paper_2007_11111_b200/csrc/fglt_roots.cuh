@@ -1131,12 +1131,12 @@ __global__ void k_hub_rows(const int* __restrict__ ci, const int* __restrict__ s
   }
 }
 
-constexpr int kRootsThreads = 256;
+constexpr int kRootsThreads = 256;     // block threads, bins with |S| > 128
+constexpr int kRootsThreadsSmall = 128;  // bin |S| <= 128
 constexpr int kPairsInFlight = 4;  // hub-row words in flight per lane
-constexpr int kRootsWarps = kRootsThreads / 32;
 
-template <bool kC3, bool kD13, bool kD15, bool kGlobal>
-__global__ void __launch_bounds__(kRootsThreads)
+template <bool kC3, bool kD13, bool kD15, bool kGlobal, int NT>
+__global__ void __launch_bounds__(NT)
 k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
               const int* __restrict__ split, const int* __restrict__ send,
               u32* __restrict__ C3f,
@@ -1149,8 +1149,9 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
   __shared__ int next_item[2];
-  __shared__ int f_off[kRootsThreads + 1], f_st[kRootsThreads];  // probe flattening
-  __shared__ int f_sa[kRootsThreads], f_sb[kRootsThreads], f_hb[kRootsThreads];
+  constexpr int NWB = NT / 32;
+  __shared__ int f_off[NT + 1], f_st[NT];  // probe / pair flattening
+  __shared__ int f_sa[NT], f_sb[NT], f_hb[NT];
   __shared__ int f_wtot[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   u64* sD = reinterpret_cast<u64*>(smem_raw);
@@ -1250,7 +1251,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         else smem_add_u64(sD + bi, (u64)ca - 1);
       }
     };
-    for (int c0 = 0; c0 + 1 < s; c0 += kRootsThreads) {
+    for (int c0 = 0; c0 + 1 < s; c0 += NT) {
       const int a_me = c0 + threadIdx.x;
       int x = 0, st = 0, se = 0;
       bool pairs = false;
@@ -1258,7 +1259,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         x = sS[a_me];
         st = split[x];
         se = lower_bound_i32(ci, st, rp[x + 1], smax + 1);
-        pairs = hub != nullptr && x >= hb && (hub_force || 2 * (s - 1 - a_me) < se - st);
+        pairs = hub != nullptr && x >= hb && (hub_force || (s - 1 - a_me) < se - st);
       }
       // probe rows
       {
@@ -1269,11 +1270,11 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         block_flatten(nqd, qa, f_off, f_st, f_wtot);
       }
       {
-        const int T = f_off[kRootsThreads];
-        const int per = (T + kRootsWarps - 1) / kRootsWarps;
+        const int T = f_off[NT];
+        const int per = (T + NWB - 1) / NWB;
         const int k0 = wid * per, k1 = min(T, k0 + per);
         if (k0 + lane < k1) {
-          int r = upper_row(f_off, k0 + lane, kRootsThreads);
+          int r = upper_row(f_off, k0 + lane, NT);
           for (int kk = k0 + lane; kk < k1; kk += 32 * kQuadsInFlight) {
             int4 v[kQuadsInFlight];
             int lt[kQuadsInFlight], ht[kQuadsInFlight], rr[kQuadsInFlight], e0[kQuadsInFlight];
@@ -1321,11 +1322,11 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         block_flatten(pairs ? s - 1 - a_me : 0, 0, f_off, f_st, f_wtot);
       }
       {
-        const int T = f_off[kRootsThreads];
-        const int per = (T + kRootsWarps - 1) / kRootsWarps;
+        const int T = f_off[NT];
+        const int per = (T + NWB - 1) / NWB;
         const int k0 = wid * per, k1 = min(T, k0 + per);
         if (k0 + lane < k1) {
-          int r = upper_row(f_off, k0 + lane, kRootsThreads);
+          int r = upper_row(f_off, k0 + lane, NT);
           for (int kk = k0 + lane; kk < k1; kk += 32 * kPairsInFlight) {
             unsigned long long wv[kPairsInFlight];
             int rr[kPairsInFlight], bb[kPairsInFlight], ob[kPairsInFlight];
