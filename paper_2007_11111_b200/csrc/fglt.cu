@@ -621,7 +621,7 @@ void roots_pass(fglt_ctx* c) {
     size_t sm = L.bytes_core();
     unsigned char* slab = nullptr;
     long long slab_stride = 0;
-    int g = std::min(cnt[b], c->sms * (small ? 16 : 8));
+    int g = std::min(cnt[b], c->sms * (small ? 32 : 8));
     if (global) {
       slab_stride = (long long)((L.bytes_aux() + 255) & ~(size_t)255);
       const long long fit = std::max<long long>(1, (4ll << 30) / slab_stride);
