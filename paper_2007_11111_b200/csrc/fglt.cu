@@ -614,36 +614,34 @@ void roots_pass(fglt_ctx* c) {
     L.hlog = 6;
     while ((1 << L.hlog) < 4 * L.s_cap) ++L.hlog;
     L.hcap = 1 << L.hlog;
-    const bool small = b == 1 && !global;  // |S| <= 128: 128-thread blocks
-    const int nt = small ? kRootsThreadsSmall : kRootsThreads;
+    // block size follows |S|: 64 threads for |S| <= 128, 128 for <= 256, else 256
+    const int nt = global ? kRootsThreads : (b == 1 ? 64 : b == 2 ? 128 : kRootsThreads);
     L.nwarps = nt / 32;
     L.stride_cap = ((L.s_cap + 31) / 32) | 1;
     size_t sm = L.bytes_core();
     unsigned char* slab = nullptr;
     long long slab_stride = 0;
-    int g = std::min(cnt[b], c->sms * (small ? 32 : 8));
+    int g = std::min(cnt[b], c->sms * 8 * (kRootsThreads / nt));
+#define FGLT_ROOTS_LAUNCH(GLOBAL, NT)                                                              \
+  do {                                                                                             \
+    set_smem(k_roots_block<kC3, kD13, kD15, GLOBAL, NT>, sm);                                      \
+    k_roots_block<kC3, kD13, kD15, GLOBAL, NT><<<g, NT, sm, c->stream>>>(                         \
+        c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride,           \
+        queues + b, d13, d15, c->hub, c->hub_base, c->hub_hb, c->force_hub == 2);                  \
+  } while (0)
     if (global) {
       slab_stride = (long long)((L.bytes_aux() + 255) & ~(size_t)255);
       const long long fit = std::max<long long>(1, (4ll << 30) / slab_stride);
       g = (int)std::min<long long>({(long long)cnt[b], (long long)c->sms, fit});
       slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
-      set_smem(k_roots_block<kC3, kD13, kD15, true, kRootsThreads>, sm);
-      k_roots_block<kC3, kD13, kD15, true, kRootsThreads><<<g, kRootsThreads, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15,
-          c->hub, c->hub_base, c->hub_hb, c->force_hub == 2);
-    } else if (small) {
-      sm += L.bytes_aux();
-      set_smem(k_roots_block<kC3, kD13, kD15, false, kRootsThreadsSmall>, sm);
-      k_roots_block<kC3, kD13, kD15, false, kRootsThreadsSmall><<<g, kRootsThreadsSmall, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15,
-          c->hub, c->hub_base, c->hub_hb, c->force_hub == 2);
+      FGLT_ROOTS_LAUNCH(true, kRootsThreads);
     } else {
       sm += L.bytes_aux();
-      set_smem(k_roots_block<kC3, kD13, kD15, false, kRootsThreads>, sm);
-      k_roots_block<kC3, kD13, kD15, false, kRootsThreads><<<g, kRootsThreads, sm, c->stream>>>(
-          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride, queues + b, d13, d15,
-          c->hub, c->hub_base, c->hub_hb, c->force_hub == 2);
+      if (nt == 64) FGLT_ROOTS_LAUNCH(false, 64);
+      else if (nt == 128) FGLT_ROOTS_LAUNCH(false, 128);
+      else FGLT_ROOTS_LAUNCH(false, kRootsThreads);
     }
+#undef FGLT_ROOTS_LAUNCH
     check_launch();
     c->launched();
   }

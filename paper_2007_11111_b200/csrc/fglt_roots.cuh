@@ -1131,8 +1131,7 @@ __global__ void k_hub_rows(const int* __restrict__ ci, const int* __restrict__ s
   }
 }
 
-constexpr int kRootsThreads = 256;     // block threads, bins with |S| > 128
-constexpr int kRootsThreadsSmall = 64;  // bin |S| <= 128
+constexpr int kRootsThreads = 256;  // block threads for |S| > 256 (smaller bins: 64, 128)
 constexpr int kPairsInFlight = 4;  // hub-row words in flight per lane
 
 template <bool kC3, bool kD13, bool kD15, bool kGlobal, int NT>
