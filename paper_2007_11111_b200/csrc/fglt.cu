@@ -62,7 +62,7 @@ constexpr int kWarpHashLog2 = 11; // 2048-slot table per warp (wc <= 1024)
 enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
-  B_CUB, B_CURSOR, B_TBND, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
+  B_CUB, B_CURSOR, B_TBND, B_BIGROWS, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV, B_COUNT
 };
 
@@ -214,6 +214,8 @@ struct fglt_ctx {
   int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1, force_hub = 0;
   // hub rows (k_hub_rows): built once per graph by the first root pass
   bool hub_built = false;
+  bool big_rows_listed = false;  // list_big_rows
+  int* big_rows = nullptr;
   unsigned long long* hub = nullptr;
   int* hub_base = nullptr;
   int hub_hb = 0;
@@ -272,35 +274,62 @@ void set_smem(K kernel, size_t bytes) {
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-template <int G>
-void launch_sweep_a(fglt_ctx* c) {
-  k_sweep_a<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(
-      c->rp, c->ci, (int)c->n, c->plan.p2 || c->plan.p3 ? c->V(V_P2) : nullptr,
-      c->plan.d7 ? c->V(V_D7) : nullptr);
+// Long rows (degree > kSweepBig) are listed once per graph for the
+// block-per-row sweeps.
+void list_big_rows(fglt_ctx* c) {
+  if (c->big_rows_listed) return;
+  c->big_rows_listed = true;
+  int* count = reinterpret_cast<int*>(c->d_small + 5);
+  CK(cudaMemsetAsync(count, 0, sizeof(int), c->stream));
+  c->big_rows = c->ensure<int>(B_BIGROWS, std::max<int64_t>(c->nnz / (kSweepBig + 1), 1));
+  k_list_big_rows<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->rp, (int)c->n, c->big_rows, count);
   check_launch();
   c->launched();
+}
+
+template <int G, class F>
+void run_rows(fglt_ctx* c, const F& f) {
+  list_big_rows(c);
+  k_rows_group<G, F><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(f, c->rp, (int)c->n);
+  check_launch();
+  c->launched();
+  k_rows_block<F><<<c->sms * 4, kSweepBlock, 0, c->stream>>>(
+      f, c->rp, c->big_rows, reinterpret_cast<const int*>(c->d_small + 5));
+  check_launch();
+  c->launched();
+}
+
+template <int G>
+void launch_sweep_a(fglt_ctx* c) {
+  SweepA f{c->rp, c->ci, c->plan.p2 || c->plan.p3 ? c->V(V_P2) : nullptr,
+           c->plan.d7 ? c->V(V_D7) : nullptr};
+  run_rows<G>(c, f);
 }
 
 template <int G>
 void launch_sweep_bc(fglt_ctx* c) {
-  k_sweep_b<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(
-      c->rp, c->ci, (int)c->n, c->C3f, c->plan.p3 ? c->V(V_P2) : nullptr, c->V(V_C3),
-      c->plan.d14 ? c->V(V_D14) : nullptr, c->plan.d10 ? c->V(V_D10) : nullptr,
-      c->plan.p3 ? c->V(V_P3) : nullptr);
-  check_launch();
-  c->launched();
+  SweepB fb{c->rp, c->ci, c->C3f, c->plan.p3 ? c->V(V_P2) : nullptr, c->V(V_C3),
+            c->plan.d14 ? c->V(V_D14) : nullptr, c->plan.d10 ? c->V(V_D10) : nullptr,
+            c->plan.p3 ? c->V(V_P3) : nullptr};
+  run_rows<G>(c, fb);
   if (c->plan.d9) {
-    k_sweep_c<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(c->rp, c->ci, (int)c->n,
-                                                                c->V(V_C3), c->V(V_D9));
-    check_launch();
-    c->launched();
+    SweepC fc{c->ci, c->V(V_C3), c->V(V_D9)};
+    run_rows<G>(c, fc);
   }
 }
 
 template <int G>
-void launch_root_work(fglt_ctx* c, u64* wc, u64* tw) {
+void launch_root_work(fglt_ctx* c, u64* wc) {
   k_root_work<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(
-      c->rp, c->ci, c->split, c->send, c->mir, (int)c->n, c->d_small + 4, wc, tw);
+      c->rp, c->ci, c->split, c->mir, (int)c->n, c->d_small + 4, wc);
+  check_launch();
+  c->launched();
+}
+
+template <int G>
+void launch_probe_work(fglt_ctx* c, u64* tw) {
+  k_probe_work<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(c->split, c->send, c->ci,
+                                                                  (int)c->n, c->d_small + 4, tw);
   check_launch();
   c->launched();
 }
@@ -346,6 +375,7 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   c->perm = c->inv = nullptr;
   c->rb_u0 = c->rb_u1 = -1;  // graph changed: root bins are stale
   c->hub_built = false;
+  c->big_rows_listed = false;
   c->rb_cnt.clear();
   c->rp = d_rp;
   c->ci = d_ci;
@@ -661,16 +691,15 @@ void triangles(fglt_ctx* c, int64_t u0, int64_t u1) {
 void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   const Plan& P = c->plan;
   if (c->n == 0 || !(P.c4 || P.d13)) return;
-  u64* work = c->ensure<u64>(B_WORK, 4 * (size_t)c->n);
+  u64* work = c->ensure<u64>(B_WORK, 3 * (size_t)c->n);
   u64* wc = work;
-  u64* key = work + c->n;
-  u64* cls = work + 2 * c->n;
-  u64* parts = work + 3 * c->n;
+  u64* cls = work + c->n;
+  u64* parts = work + 2 * c->n;
   int* lists[8];
   int64_t stride = 0;
   if (P.c4) {
     const int G = group_for((double)c->nnz / (double)c->n);
-    DISPATCH_G(G, launch_root_work, c, wc, key);
+    DISPATCH_G(G, launch_root_work, c, wc);
     k_c4_class<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(
         c->rp, c->split, wc, (int)u0, (int)u1, cls, parts, c->force_c4_class, c->force_c4_parts);
     check_launch();
@@ -1255,7 +1284,8 @@ int fglt_stage_bounds(fglt_ctx* c, int world, int64_t* bounds, fglt_error* err) 
     }
     u64* work = c->ensure<u64>(B_WORK, 2 * (size_t)n);
     const int G = group_for((double)c->nnz / (double)n);
-    DISPATCH_G(G, launch_root_work, c, work, work + n);
+    DISPATCH_G(G, launch_root_work, c, work);
+    DISPATCH_G(G, launch_probe_work, c, work + n);
     std::vector<u64> wc(n), tw(n);
     CK(cudaMemcpyAsync(wc.data(), work, n * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(tw.data(), work + n, n * 8, cudaMemcpyDeviceToHost, c->stream));

@@ -212,40 +212,93 @@ __global__ void k_mirror(const int* __restrict__ rp, const int* __restrict__ ci,
   }
 }
 
-// ------------------------------------------------------------------ sweep A
-// p2 = sum_j d_j - d  (compute_p2, kernels.cpp:26-39)
-// d7 = sum_j C(d_j - 1, 2) (compute_d7, kernels.cpp:149-163)
-// Group of G lanes per row.
-template <int G>
-__global__ void k_sweep_a(const int* __restrict__ rp, const int* __restrict__ ci, int n,
-                          u64* __restrict__ p2, u64* __restrict__ d7) {
+// ------------------------------------------------------------------ sweeps
+// Per-row sweeps. Each is a functor: elem() folds one CSR entry into NV
+// accumulators, fin() writes the row. Rows of degree <= kSweepBig go G lanes
+// per row (k_rows_group); longer rows, listed once by k_list_big_rows, get a
+// whole block each (k_rows_block), so one hub row never serialises a group.
+constexpr int kSweepBig = 1024;
+constexpr int kSweepBlock = 256;
+
+__global__ void k_list_big_rows(const int* __restrict__ rp, int n, int* __restrict__ list,
+                                int* __restrict__ count) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    if (rp[r + 1] - rp[r] > kSweepBig) list[atomicAdd(count, 1)] = r;
+}
+
+template <int G, class F>
+__global__ void k_rows_group(F f, const int* __restrict__ rp, int n) {
   const int lane = threadIdx.x & (G - 1);
   const int groups = (gridDim.x * blockDim.x) / G;
   const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
   const int rounds = (n + groups - 1) / groups;
-  for (int it = 0; it < rounds; ++it) {
+  for (int it = 0; it < rounds; ++it) {  // warp-uniform trip count (group shuffles)
     const int r = g0 + it * groups;
-    u64 sd = 0, s7 = 0;
-    u64 d = 0;
+    u64 acc[F::NV] = {};
+    bool mine = false;
     if (r < n) {
       const int b = rp[r], e = rp[r + 1];
-      d = (u64)(e - b);
-      for (int p = b + lane; p < e; p += G) {
-        const int j = ci[p];
-        const u64 dj = (u64)(rp[j + 1] - rp[j]);
-        sd += dj;
-        const u64 t = dj - 1;  // dj >= 1 for a neighbour
-        s7 += t < 2 ? 0ull : t * (t - 1) / 2;
-      }
+      mine = e - b <= kSweepBig;
+      if (mine)
+        for (int p = b + lane; p < e; p += G) f.elem(r, p, acc);
     }
-    sd = group_sum_u64<G>(sd);
-    s7 = group_sum_u64<G>(s7);
-    if (r < n && lane == 0) {
-      if (p2) p2[r] = sat_sub(sd, d);
-      if (d7) d7[r] = s7;
-    }
+#pragma unroll
+    for (int k = 0; k < F::NV; ++k) acc[k] = group_sum_u64<G>(acc[k]);
+    if (mine && lane == 0) f.fin(r, acc);
   }
 }
+
+template <class F>
+__global__ void __launch_bounds__(kSweepBlock)
+k_rows_block(F f, const int* __restrict__ rp, const int* __restrict__ list,
+             const int* __restrict__ count) {
+  __shared__ u64 part[F::NV][kSweepBlock / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nb = *count;
+  for (int i = blockIdx.x; i < nb; i += gridDim.x) {
+    const int r = list[i];
+    u64 acc[F::NV] = {};
+    for (int p = rp[r] + threadIdx.x; p < rp[r + 1]; p += kSweepBlock) f.elem(r, p, acc);
+#pragma unroll
+    for (int k = 0; k < F::NV; ++k) {
+      const u64 v = warp_sum_u64(acc[k]);
+      if (lane == 0) part[k][wid] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int k = 0; k < F::NV; ++k) {
+        u64 t = 0;
+        for (int w = 0; w < kSweepBlock / 32; ++w) t += part[k][w];
+        acc[k] = t;
+      }
+      f.fin(r, acc);
+    }
+    __syncthreads();
+  }
+}
+
+// Sweep A: p2 = sum_j d_j - d  (compute_p2, kernels.cpp:26-39);
+// d7 = sum_j C(d_j - 1, 2) (compute_d7, kernels.cpp:149-163).
+struct SweepA {
+  static constexpr int NV = 2;
+  const int* rp;
+  const int* ci;
+  u64* p2;
+  u64* d7;
+  __device__ void elem(int, int p, u64 (&acc)[NV]) const {
+    const int j = ci[p];
+    const u64 dj = (u64)(rp[j + 1] - rp[j]);
+    acc[0] += dj;
+    const u64 t = dj - 1;  // dj >= 1 for a neighbour
+    acc[1] += t < 2 ? 0ull : t * (t - 1) / 2;
+  }
+  __device__ void fin(int r, const u64 (&acc)[NV]) const {
+    const u64 d = (u64)(rp[r + 1] - rp[r]);
+    if (p2) p2[r] = sat_sub(acc[0], d);
+    if (d7) d7[r] = acc[1];
+  }
+};
 
 // The triangle pass (per-edge C3, and 4-cliques) is root-centric: see
 // k_roots_warp / k_roots_block<kC3=true> in fglt_roots.cuh.
@@ -261,65 +314,47 @@ __global__ void k_c3_mirror(const int* __restrict__ ce_pos, const int* __restric
   }
 }
 
-// ------------------------------------------------------------------ sweep B
 // c3 = sum C3 / 2; d14 = sum C(C3,2); d10 = sum C3 * (d_j - 2)+;
 // p3 = sum p2_j - (d(d-1) + 2 c3) rectified   (kernels.cpp:91-107, :176-205)
-template <int G>
-__global__ void k_sweep_b(const int* __restrict__ rp, const int* __restrict__ ci, int n,
-                          const u32* __restrict__ C3f, const u64* __restrict__ p2,
-                          u64* __restrict__ c3, u64* __restrict__ d14,
-                          u64* __restrict__ d10, u64* __restrict__ p3) {
-  const int lane = threadIdx.x & (G - 1);
-  const int groups = (gridDim.x * blockDim.x) / G;
-  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int rounds = (n + groups - 1) / groups;
-  for (int it = 0; it < rounds; ++it) {
-    const int r = g0 + it * groups;
-    u64 sc = 0, s14 = 0, s10 = 0, sp2 = 0;
-    u64 d = 0;
-    if (r < n) {
-      const int b = rp[r], e = rp[r + 1];
-      d = (u64)(e - b);
-      for (int p = b + lane; p < e; p += G) {
-        const int j = ci[p];
-        const u64 c = C3f[p];
-        sc += c;
-        s14 += c * (c - (c > 0)) / 2;
-        const u64 dj = (u64)(rp[j + 1] - rp[j]);
-        s10 += c * (dj > 2 ? dj - 2 : 0ull);
-        if (p2) sp2 += p2[j];
-      }
-    }
-    sc = group_sum_u64<G>(sc);
-    s14 = group_sum_u64<G>(s14);
-    s10 = group_sum_u64<G>(s10);
-    sp2 = group_sum_u64<G>(sp2);
-    if (r < n && lane == 0) {
-      const u64 c3v = sc / 2;
-      c3[r] = c3v;
-      if (d14) d14[r] = s14;
-      if (d10) d10[r] = s10;
-      if (p3) p3[r] = sat_sub(sp2, d * (d > 0 ? d - 1 : 0ull) + 2 * c3v);
-    }
+// Sweep B: c3 = sum C3 / 2; d14 = sum C(C3,2); d10 = sum C3 * (d_j - 2)+;
+// p3 = sum p2_j - (d(d-1) + 2 c3) rectified   (kernels.cpp:91-107, :176-205)
+struct SweepB {
+  static constexpr int NV = 4;
+  const int* rp;
+  const int* ci;
+  const u32* C3f;
+  const u64* p2;
+  u64* c3;
+  u64* d14;
+  u64* d10;
+  u64* p3;
+  __device__ void elem(int, int p, u64 (&acc)[NV]) const {
+    const int j = ci[p];
+    const u64 c = C3f[p];
+    acc[0] += c;
+    acc[1] += c * (c - (c > 0)) / 2;
+    const u64 dj = (u64)(rp[j + 1] - rp[j]);
+    acc[2] += c * (dj > 2 ? dj - 2 : 0ull);
+    if (p2) acc[3] += p2[j];
   }
-}
+  __device__ void fin(int r, const u64 (&acc)[NV]) const {
+    const u64 d = (u64)(rp[r + 1] - rp[r]);
+    const u64 c3v = acc[0] / 2;
+    c3[r] = c3v;
+    if (d14) d14[r] = acc[1];
+    if (d10) d10[r] = acc[2];
+    if (p3) p3[r] = sat_sub(acc[3], d * (d > 0 ? d - 1 : 0ull) + 2 * c3v);
+  }
+};
 
-// d9 = sum_j c3_j - 2 c3, rectified (kernels.cpp:194-199)
-template <int G>
-__global__ void k_sweep_c(const int* __restrict__ rp, const int* __restrict__ ci, int n,
-                          const u64* __restrict__ c3, u64* __restrict__ d9) {
-  const int lane = threadIdx.x & (G - 1);
-  const int groups = (gridDim.x * blockDim.x) / G;
-  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int rounds = (n + groups - 1) / groups;
-  for (int it = 0; it < rounds; ++it) {
-    const int r = g0 + it * groups;
-    u64 s = 0;
-    if (r < n)
-      for (int p = rp[r] + lane; p < rp[r + 1]; p += G) s += c3[ci[p]];
-    s = group_sum_u64<G>(s);
-    if (r < n && lane == 0) d9[r] = sat_sub(s, 2 * c3[r]);
-  }
-}
+// Sweep C: d9 = sum_j c3_j - 2 c3, rectified (kernels.cpp:194-199)
+struct SweepC {
+  static constexpr int NV = 1;
+  const int* ci;
+  const u64* c3;
+  u64* d9;
+  __device__ void elem(int, int p, u64 (&acc)[NV]) const { acc[0] += c3[ci[p]]; }
+  __device__ void fin(int r, const u64 (&acc)[NV]) const { d9[r] = sat_sub(acc[0], 2 * c3[r]); }
+};
 
 }  // namespace fglt

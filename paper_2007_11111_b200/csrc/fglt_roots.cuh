@@ -33,13 +33,13 @@ namespace fglt {
 // addressing table for light roots, dense 48K-entry tiles of the w range for
 // heavy roots.
 
-// wc(u) = number of wedges rooted at u; tw(u) = triangle-probe work of u.
+// wc(u) = number of wedges rooted at u (sum over v in N-(u) of the prefix of
+// row v below u, whose end is the mirror position of u).
 template <int G>
 __global__ void k_root_work(const int* __restrict__ rp, const int* __restrict__ ci,
-                            const int* __restrict__ split, const int* __restrict__ send,
-                            const int* __restrict__ mir, int n,
+                            const int* __restrict__ split, const int* __restrict__ mir, int n,
                             const unsigned long long* __restrict__ nact_p,
-                            u64* __restrict__ wc, u64* __restrict__ tw) {
+                            u64* __restrict__ wc) {
   const int nact = (int)*nact_p;
   const int lane = threadIdx.x & (G - 1);
   const int groups = (gridDim.x * blockDim.x) / G;
@@ -47,21 +47,38 @@ __global__ void k_root_work(const int* __restrict__ rp, const int* __restrict__ 
   const int rounds = (n + groups - 1) / groups;
   for (int it = 0; it < rounds; ++it) {
     const int u = g0 + it * groups;
-    u64 a = 0, t = 0;
+    u64 a = 0;
     if (u < nact) {  // pendant/isolated vertices root nothing
-      const int b = rp[u], s = split[u], e = send[u];
+      const int b = rp[u], s = split[u];
       for (int q = b + lane; q < s; q += G) a += (u64)(mir[q] - rp[ci[q]]);
-      for (int p = s + lane; p < e; p += G) {
+    }
+    a = group_sum_u64<G>(a);
+    if (u < n && lane == 0) wc[u] = a;
+  }
+}
+
+// tw(u) = triangle-probe work of u (sum of |N+(x)| over x in N+(u), plus
+// |N+(u)|); used only to cut root ranges of equal work across ranks.
+template <int G>
+__global__ void k_probe_work(const int* __restrict__ split, const int* __restrict__ send,
+                             const int* __restrict__ ci, int n,
+                             const unsigned long long* __restrict__ nact_p,
+                             u64* __restrict__ tw) {
+  const int nact = (int)*nact_p;
+  const int lane = threadIdx.x & (G - 1);
+  const int groups = (gridDim.x * blockDim.x) / G;
+  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int rounds = (n + groups - 1) / groups;
+  for (int it = 0; it < rounds; ++it) {
+    const int u = g0 + it * groups;
+    u64 t = 0;
+    if (u < nact)
+      for (int p = split[u] + lane; p < send[u]; p += G) {
         const int x = ci[p];
         t += (u64)(send[x] - split[x]);
       }
-    }
-    a = group_sum_u64<G>(a);
     t = group_sum_u64<G>(t);
-    if (u < n && lane == 0) {
-      wc[u] = a;
-      tw[u] = u < nact ? t + (u64)(send[u] - split[u]) : 0;
-    }
+    if (u < n && lane == 0) tw[u] = u < nact ? t + (u64)(send[u] - split[u]) : 0;
   }
 }
 
