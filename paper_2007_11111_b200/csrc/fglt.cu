@@ -300,6 +300,12 @@ void run_rows(fglt_ctx* c, const F& f) {
 }
 
 template <int G>
+void launch_root_work(fglt_ctx* c, u64* wc) {
+  RootWork f{c->rp, c->ci, c->split, c->mir, (int)c->nact, wc};
+  run_rows<G>(c, f);
+}
+
+template <int G>
 void launch_sweep_a(fglt_ctx* c) {
   SweepA f{c->rp, c->ci, c->plan.p2 || c->plan.p3 ? c->V(V_P2) : nullptr,
            c->plan.d7 ? c->V(V_D7) : nullptr};
@@ -316,14 +322,6 @@ void launch_sweep_bc(fglt_ctx* c) {
     SweepC fc{c->ci, c->V(V_C3), c->V(V_D9)};
     run_rows<G>(c, fc);
   }
-}
-
-template <int G>
-void launch_root_work(fglt_ctx* c, u64* wc) {
-  k_root_work<G><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(
-      c->rp, c->ci, c->split, c->mir, (int)c->n, c->d_small + 4, wc);
-  check_launch();
-  c->launched();
 }
 
 template <int G>
@@ -422,8 +420,8 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   tb = c->buf[B_CUB].cap;
   CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ndeg, nrp, N + 1, c->stream));
   c->launched();
-  k_fill_rows<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(d_rp, d_ci, perm, inv, nrp, N, tmp,
-                                                           row_of);
+  k_fill_rows<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(d_rp, d_ci, perm, inv, nrp, N,
+                                                           c->d_small + 4, tmp, row_of);
   check_launch();
   c->launched();
   tb = c->buf[B_CUB].cap;

@@ -150,13 +150,38 @@ __global__ void k_perm(const u64* __restrict__ keys, int n, int* __restrict__ pe
 // order: the transpose of a symmetric graph is the graph itself, so that sort
 // yields the sorted relabelled CSR (a 20-bit key sort instead of a sort of
 // every row).
+// Active rows [0, n_active) have non-decreasing degree after the relabel, so
+// the long ones are the contiguous range [first_long_row, n_active).
+__device__ __forceinline__ int first_long_row(const int* __restrict__ nrp, int nact, int thr) {
+  int lo = 0, hi = nact;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (nrp[mid + 1] - nrp[mid] > thr) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+constexpr int kLongRow = 1024;  // rows longer than this get a whole block
+
 __global__ void k_fill_rows(const int* __restrict__ rp, const int* __restrict__ ci,
                             const int* __restrict__ perm, const int* __restrict__ inv,
-                            const int* __restrict__ nrp, int n, int* __restrict__ out,
-                            int* __restrict__ row_of) {
+                            const int* __restrict__ nrp, int n,
+                            const unsigned long long* __restrict__ nact_p,
+                            int* __restrict__ out, int* __restrict__ row_of) {
+  const int nact = (int)*nact_p;
+  const int fl = first_long_row(nrp, nact, kLongRow);
+  for (int r = fl + blockIdx.x; r < nact; r += gridDim.x) {  // block per long row
+    const int o = perm[r];
+    const int b = rp[o], e = rp[o + 1], w = nrp[r];
+    for (int p = b + threadIdx.x; p < e; p += blockDim.x) {
+      out[w + (p - b)] = inv[ci[p]];
+      row_of[w + (p - b)] = r;
+    }
+  }
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+    if (r >= fl && r < nact) continue;
     const int o = perm[r];
     const int b = rp[o], e = rp[o + 1], w = nrp[r];
     for (int p = b + lane; p < e; p += 32) {

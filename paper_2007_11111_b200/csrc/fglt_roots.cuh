@@ -33,29 +33,22 @@ namespace fglt {
 // addressing table for light roots, dense 48K-entry tiles of the w range for
 // heavy roots.
 
-// wc(u) = number of wedges rooted at u (sum over v in N-(u) of the prefix of
-// row v below u, whose end is the mirror position of u).
-template <int G>
-__global__ void k_root_work(const int* __restrict__ rp, const int* __restrict__ ci,
-                            const int* __restrict__ split, const int* __restrict__ mir, int n,
-                            const unsigned long long* __restrict__ nact_p,
-                            u64* __restrict__ wc) {
-  const int nact = (int)*nact_p;
-  const int lane = threadIdx.x & (G - 1);
-  const int groups = (gridDim.x * blockDim.x) / G;
-  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int rounds = (n + groups - 1) / groups;
-  for (int it = 0; it < rounds; ++it) {
-    const int u = g0 + it * groups;
-    u64 a = 0;
-    if (u < nact) {  // pendant/isolated vertices root nothing
-      const int b = rp[u], s = split[u];
-      for (int q = b + lane; q < s; q += G) a += (u64)(mir[q] - rp[ci[q]]);
-    }
-    a = group_sum_u64<G>(a);
-    if (u < n && lane == 0) wc[u] = a;
+// wc(u) = number of wedges rooted at u: sum over v in N-(u) of the prefix of
+// row v below u, whose end is the mirror position of u. A row functor
+// (k_rows_group / k_rows_block); pendant/isolated vertices root nothing.
+struct RootWork {
+  static constexpr int NV = 1;
+  const int* rp;
+  const int* ci;
+  const int* split;
+  const int* mir;
+  int nact;
+  u64* wc;
+  __device__ void elem(int r, int p, u64 (&acc)[NV]) const {
+    if (r < nact && p < split[r]) acc[0] += (u64)(mir[p] - rp[ci[p]]);
   }
-}
+  __device__ void fin(int r, const u64 (&acc)[NV]) const { wc[r] = acc[0]; }
+};
 
 // tw(u) = triangle-probe work of u (sum of |N+(x)| over x in N+(u), plus
 // |N+(u)|); used only to cut root ranges of equal work across ranks.
