@@ -573,6 +573,12 @@ void build_hubs(fglt_ctx* c) {
   if (c->force_hub == 1 || nact < 2) return;
   const int R = (int)std::min<int64_t>(nact, kHubMax);
   c->hub_hb = (int)(nact - R);
+  if (c->force_hub != 2) {  // only graphs with real hubs: the smallest hub's degree
+    int h[2];
+    CK(cudaMemcpyAsync(h, c->rp + c->hub_hb, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h[1] - h[0] < kHubMinDegree) return;
+  }
   int* hw = c->ensure<int>(B_HUBBASE, 2 * (size_t)(R + 1));
   int* base = hw + (R + 1);
   k_hub_words<<<c->grid(R + 1, 256), 256, 0, c->stream>>>(R, hw);
@@ -627,10 +633,11 @@ void roots_pass(fglt_ctx* c) {
   CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
   if (cnt[0] > 0) {
     const int wpb = 8;
-    const size_t sm = (size_t)wpb * (32 * 8 + 161 * 4);
+    const size_t sm = (size_t)wpb * (32 * 8 + kRootsWarpInts * 4);
     const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
-    k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(c->rp, c->ci, c->split, c->send, c->C3f,
-                                                                  lists[0], cnt[0], d13, d15);
+    k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(
+        c->rp, c->ci, c->split, c->send, c->C3f, lists[0], cnt[0], d13, d15, c->hub, c->hub_base,
+        c->hub_hb, c->force_hub == 2);
     check_launch();
     c->launched();
   }

@@ -965,23 +965,30 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
 // kernels.cpp:234-288, same counts).
 
 // Warp per root, |S| <= 32: rows are single words.
+constexpr int kRootsWarpInts = 32 * 5 + 33;  // sS, sC, rows, fbase, foff(33), fsplit per warp
 template <bool kC3, bool kD13, bool kD15>
-__global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__ ci,
+__global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ rp, const int* __restrict__ ci,
                              const int* __restrict__ split, const int* __restrict__ send,
                              u32* __restrict__ C3f,
                              const int* __restrict__ roots, int nroots,
-                             u64* __restrict__ d13, u64* __restrict__ d15) {
+                             u64* __restrict__ d13, u64* __restrict__ d15,
+                             const unsigned long long* __restrict__ hub,
+                             const int* __restrict__ hub_base, int hb, int hub_force) {
   // kC3: per-edge triangle counts (atomics into C3f) — the triangle pass.
   // kD13: diamonds from the final C3 — a later pass (needs complete C3).
+  // Members that are hubs may test their pairs against the hub rows instead
+  // of probing (see k_roots_block).
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   u64* sD = reinterpret_cast<u64*>(smem_raw) + wib * 32;
-  int* sS = reinterpret_cast<int*>(reinterpret_cast<u64*>(smem_raw) + (blockDim.x >> 5) * 32) + wib * 161;
+  int* sS = reinterpret_cast<int*>(reinterpret_cast<u64*>(smem_raw) + (blockDim.x >> 5) * 32) +
+            wib * kRootsWarpInts;
   u32* sC = reinterpret_cast<u32*>(sS + 32);
   u32* rows = sC + 32;
   int* fbase = reinterpret_cast<int*>(rows + 32);  // per-warp flattening tables
   int* foff = fbase + 32;                           // 33 entries
+  int* fsplit = foff + 33;                          // pair rows: split[S[a]]
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
     const int u = roots[k];
@@ -1000,11 +1007,14 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
     u64 tu = 0;
     // Flatten the probe lists N+(S[a]) (cut at max S) of all members: lane a
     // sets up its segment, then every lane streams one element per step.
-    int st = 0, len = 0;
+    int st = 0, len = 0, x = 0;
+    bool pairs = false;
     if (lane + 1 < s) {
-      const int x = sS[lane];
+      x = sS[lane];
       st = split[x];
       len = lower_bound_i32(ci, st, rp[x + 1], smax + 1) - st;
+      pairs = hub != nullptr && x >= hb && (hub_force || s - 1 - lane < len);
+      if (pairs) len = 0;
     }
     int T;
     const int off = flat_prefix(len, &T);
@@ -1048,6 +1058,55 @@ __global__ void k_roots_warp(const int* __restrict__ rp, const int* __restrict__
     if (kC3 && na) atomicAdd(sC + cr, na);
     if (kD13 && da) smem_add_u64(sD + cr, da);
     __syncwarp();
+    if (hub != nullptr && __any_sync(0xffffffffu, pairs)) {
+      // pair rows: member a tests S[a+1..s) against its hub row
+      int T2;
+      const int off2 = flat_prefix(pairs ? s - 1 - lane : 0, &T2);
+      fbase[lane] = pairs ? hub_base[x - hb] : 0;
+      foff[lane] = off2;
+      fsplit[lane] = st;
+      if (lane == 0) foff[32] = T2;
+      __syncwarp();
+      r = 0;
+      cr = 0;
+      na = 0;
+      da = 0;
+      for (int kk = lane; kk < T2; kk += 32) {
+        while (foff[r + 1] <= kk) ++r;
+        if (r != cr) {
+          if (kC3 && na) atomicAdd(sC + cr, na);
+          if (kD13 && da) smem_add_u64(sD + cr, da);
+          na = 0;
+          da = 0;
+          cr = r;
+        }
+        const int bi = r + 1 + (kk - foff[r]);
+        const int o = sS[bi] - sS[r] - 1;
+        const unsigned long long wv = __ldg(hub + fbase[r] + (o >> 5));
+        const u32 bits = (u32)wv;
+        if ((bits >> (o & 31)) & 1u) {
+          const int p = fsplit[r] + (int)(wv >> 32) + __popc(bits & ((1u << (o & 31)) - 1u));
+          if (kD15) {
+            atomicOr(rows + r, 1u << bi);
+            atomicOr(rows + bi, 1u << r);
+          }
+          if (kC3) {
+            atomicAdd(C3f + p, 1u);
+            atomicAdd(sC + bi, 1u);
+            ++na;
+          }
+          if (kD13) {
+            tu += (u64)__ldg(C3f + p) - 1;
+            da += (u64)sC[bi] - 1;
+            if (narrow) atomicAdd(reinterpret_cast<u32*>(sD + bi), sC[r] - 1);
+            else smem_add_u64(sD + bi, (u64)sC[r] - 1);
+          }
+        }
+      }
+      if (kC3 && na) atomicAdd(sC + cr, na);
+      if (kD13 && da) smem_add_u64(sD + cr, da);
+      __syncwarp();
+    }
     if (kC3 && lane < s && sC[lane]) atomicAdd(C3f + s0 + lane, sC[lane]);
     if (kD13) {
       if (lane < s && sD[lane]) atomicAdd(d13 + sS[lane], sD[lane]);
@@ -1113,6 +1172,7 @@ __device__ __forceinline__ int s_hash_find(const int* keys, const unsigned short
 // before the word (so the CSR position of (x, y) is split[x] + high +
 // popc(low below y)). Rows are ceil((R-1-i)/32) words, packed back to back.
 constexpr int kHubMax = 16384;  // R cap: R^2/8 bytes of rows (32 MB), L2-resident
+constexpr int kHubMinDegree = 128;  // hub rows only when the R-th largest degree reaches this
 
 __global__ void k_hub_words(int R, int* __restrict__ w) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= R; i += gridDim.x * blockDim.x)

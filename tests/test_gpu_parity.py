@@ -235,7 +235,7 @@ def test_forced_code_paths(label, key, value, parts):
 
 
 @pytest.mark.parametrize("hub", [1, 2])
-@pytest.mark.parametrize("rbin", [1, 3, 5])
+@pytest.mark.parametrize("rbin", [0, 1, 3, 5])
 def test_hub_rows_paths(hub, rbin):
     """Hub-row pair checks (forced for every hub member) and the pure probe
     path (hub rows off) must give the same bits, in every block bin."""
