@@ -451,10 +451,28 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   int* mir = c->ensure<int>(B_MIR, std::max<int64_t>(nnz, 1));
   int* ce_row = c->ensure<int>(B_CE_ROW, std::max<int64_t>(c->m, 1));
   int* ce_pos = c->ensure<int>(B_CE_POS, std::max<int64_t>(c->m, 1));
-  k_mirror<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, send, orp, N, mir, ce_row,
-                                                        ce_pos);
-  check_launch();
-  c->launched();
+  const bool sort_mirror = nnz >= 8 * n;  // else per-edge binary searches are cheaper
+  if (nnz > 0 && !sort_mirror) {
+    k_mirror<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, send, orp, N, mir,
+                                                          ce_row, ce_pos);
+    check_launch();
+    c->launched();
+  } else if (nnz > 0) {
+    // mirror positions by a second stable transpose: the sorted CSR read
+    // r-major as (key = neighbour y, value = own position j) sorts into
+    // y-major order with r ascending, i.e. the value landing at j' (the slot
+    // of (y, r)) is j, the slot of (r, y).
+    k_iota<<<c->grid(nnz, 256), 256, 0, c->stream>>>(row_of, nnz);
+    check_launch();
+    c->launched();
+    tb = c->buf[B_CUB].cap;
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, nci, keys_out, row_of, mir, (int)nnz, 0,
+                                       id_bits, c->stream));
+    c->launched();
+    k_canon<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(split, send, orp, N, ce_row, ce_pos);
+    check_launch();
+    c->launched();
+  }
   c->split = split;
   c->send = send;
   c->orp = orp;

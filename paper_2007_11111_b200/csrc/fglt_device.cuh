@@ -213,9 +213,10 @@ __global__ void k_split(const int* __restrict__ rp, const int* __restrict__ ci, 
   if (mo) atomicMax(maxout, mo);
 }
 
-// Warp per row: for each canonical position p (row r, v = ci[p] > r) find the
-// mirror position q of r in row v (a prefix entry) and record both; also emit
-// the compact canonical edge list (row, position), index e = orp[r] + offset.
+// Low-degree graphs (binary searches are short): warp per row; for each
+// canonical position p (row r, v = ci[p] > r) find the mirror position q of
+// r in row v (a prefix entry) and record both; also emit the compact
+// canonical edge list (row, position), index e = orp[r] + offset.
 __global__ void k_mirror(const int* __restrict__ rp, const int* __restrict__ ci,
                          const int* __restrict__ split, const int* __restrict__ send,
                          const int* __restrict__ orp, int n, int* __restrict__ mir,
@@ -235,6 +236,29 @@ __global__ void k_mirror(const int* __restrict__ rp, const int* __restrict__ ci,
       ce_pos[base + (p - s)] = p;
     }
   }
+}
+
+// Compact canonical edge list of the active-active upper entries: for row r,
+// positions [split[r], send[r]) go to e = orp[r] + offset as (row, position).
+// (The mirror positions come from a second stable transpose sort, prepare().)
+__global__ void k_canon(const int* __restrict__ split, const int* __restrict__ send,
+                        const int* __restrict__ orp, int n, int* __restrict__ ce_row,
+                        int* __restrict__ ce_pos) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+    const int s = split[r], e = send[r], base = orp[r];
+    for (int p = s + lane; p < e; p += 32) {
+      ce_row[base + (p - s)] = r;
+      ce_pos[base + (p - s)] = p;
+    }
+  }
+}
+
+__global__ void k_iota(int* __restrict__ a, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = (int)i;
 }
 
 // ------------------------------------------------------------------ sweeps
