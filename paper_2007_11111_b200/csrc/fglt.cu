@@ -741,21 +741,23 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       check_launch();
       c->launched();
     }
-    if (cnt[1] > 0) {  // class 2: warp tables of 2048 slots
-      const int wpb = 4;
-      const size_t sm = (size_t)wpb * ((1 << kWarpHashLog2) * 2 + 100) * 4;
-      set_smem(k_c4_warp<kWarpHashLog2>, sm);
-      k_c4_warp<kWarpHashLog2><<<c->grid((int64_t)cnt[1] * 32, wpb * 32, 3), wpb * 32, sm,
-                                 c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[1], cnt[1], wc,
-                                              c4);
+    if (cnt[1] > 0) {  // class 2: 128-thread block-flattened tables of <= 2048 slots
+      const size_t sm = (size_t)(1 << kWarpHashLog2) * 8;
+      const int g = std::min(cnt[1], c->sms * 10);
+      set_smem(k_c4_block<128>, sm);
+      k_c4_block<128><<<g, 128, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[1], cnt[1],
+                                                wc, parts, kWarpHashLog2, queues + 4, c4);
       check_launch();
       c->launched();
     }
-    if (cnt[2] > 0) {  // class 3: small block tables, 128-thread blocks
+    if (cnt[2] > 0) {  // class 3: 256-thread block-flattened tables of <= 4096 slots
       const size_t sm = (size_t)(1 << kC4SmallLog) * 8;
       const int g = std::min(cnt[2], c->sms * 6);
-      DISPATCH_G(G, launch_c4_hashp, c, g, 128, sm, lists[2], cnt[2], wc, parts, kC4SmallLog,
-                 queues + 0, c4);
+      set_smem(k_c4_block<256>, sm);
+      k_c4_block<256><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[2], cnt[2],
+                                                wc, parts, kC4SmallLog, queues + 0, c4);
+      check_launch();
+      c->launched();
     }
     if (cnt[3] > 0) {  // class 4: block-flattened hash-partition passes
       const size_t sm = (size_t)(1 << kC4HashLog) * 8;
