@@ -267,11 +267,19 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 constexpr int kC4HashLog = 14;              // 16384 slots (keys + counts = 128 KB)
 constexpr int kC4SmallLog = 12;             // 4096 slots (32 KB)
 constexpr u64 kC4HashFill = 12288;          // distinct targets per pass (LF 0.75)
-constexpr int kC4DenseThreads = 1024;       // one dense block per SM (the tile takes the smem)
-constexpr int kC4TileBytes = 196608;        // counter tile per block (192 KB)
+#ifndef FGLT_DENSE_THREADS
+#define FGLT_DENSE_THREADS 1024
+#define FGLT_DENSE_TILE_BYTES 196608
+#endif
+constexpr int kC4DenseThreads = FGLT_DENSE_THREADS;     // one dense block per SM by default
+constexpr int kC4TileBytes = FGLT_DENSE_TILE_BYTES;     // counter tile per block (192 KB)
 constexpr int kC4Tile16 = kC4TileBytes / 2; // ids per packed tile
 constexpr int kC4Tile32 = kC4TileBytes / 4; // ids per 32-bit tile
 constexpr int kC4Long = 48;                 // rows at least this long: flattened batches
+#ifndef FGLT_GIANT
+#define FGLT_GIANT 512
+#endif
+constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many wedges in a tile: warp per row
 constexpr int kQuadsInFlight = 2;          // 16-byte loads in flight per lane (dense batches)
 constexpr int kC4BlockThreads = 1024;      // class-4 block (one 128 KB table per SM)
 
@@ -643,6 +651,23 @@ __global__ void k_tile_bounds(const int* __restrict__ rp, const int* __restrict_
   }
 }
 
+// Optional phase timers for the dense kernel (profiling builds only,
+// -DFGLT_DENSE_PROF): per-warp clock deltas summed over the grid and printed
+// by the last block. Phases: 0 zero, 1 count work, 2 count barrier, 3 sweep,
+// 4 attribution work, 5 attribution barrier, 6 root setup.
+#ifdef FGLT_DENSE_PROF
+__device__ unsigned long long g_dense_prof[8];
+__device__ unsigned int g_dense_done;
+#define DPROF_MARK(k)                                                       \
+  do {                                                                      \
+    const long long _t = clock64();                                         \
+    if (lane == 0) atomicAdd(g_dense_prof + (k), (unsigned long long)(_t - _pt)); \
+    _pt = _t;                                                               \
+  } while (0)
+#else
+#define DPROF_MARK(k) do {} while (0)
+#endif
+
 template <bool PACK>
 __global__ void __launch_bounds__(kC4DenseThreads, 1024 / kC4DenseThreads)
 k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
@@ -680,6 +705,9 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     return L[off];
   };
   rs[lane] = 0;
+#ifdef FGLT_DENSE_PROF
+  long long _pt = clock64();
+#endif
   __shared__ int s_root;
   while (true) {
     if (threadIdx.x == 0) s_root = atomicAdd(next_root, 1);
@@ -698,7 +726,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     const int qs = lo_q;
     // giant rows: expected >= 512 elements per tile -> warp per row
     const int ntiles = (u + TILE - 1) / TILE;
-    const int giant_deg = max(kC4Long, 512 * ntiles);
+    const int giant_deg = max(kC4Long, kC4GiantPerTile * ntiles);
     hi_q = nq;
     while (lo_q < hi_q) {
       const int mid = (lo_q + hi_q) >> 1;
@@ -716,6 +744,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
       {
         uint4* L4 = reinterpret_cast<uint4*>(L);
         const int n4 = (words + 3) >> 2;
+        DPROF_MARK(6);
         for (int i = threadIdx.x; i < n4; i += blockDim.x) L4[i] = make_uint4(0, 0, 0, 0);
       }
       if (threadIdx.x == 0) {
@@ -723,6 +752,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         next_giant[0] = next_giant[1] = 0;
       }
       __syncthreads();
+      DPROF_MARK(0);
       // ---- count pass: giant rows (warp per row, 16-byte loads, largest
       // first), then long-row batches, then short rows
       while (true) {
@@ -814,7 +844,9 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         }
         __syncwarp();
       }
+      DPROF_MARK(1);
       __syncthreads();
+      DPROF_MARK(2);
       {
         // 16-byte sweep; words past the tile end were zeroed with the tile
         const uint4* L4 = reinterpret_cast<const uint4*>(L);
@@ -848,6 +880,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
           }
         }
       }
+      DPROF_MARK(3);
       // ---- attribution pass: c4[v] += sum (L[w] - 1); cursors advance
       while (true) {
         int gi = 0;
@@ -943,12 +976,27 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         rs[lane] = 0;
         __syncwarp();
       }
+      DPROF_MARK(4);
       __syncthreads();
+      DPROF_MARK(5);
     }
     acc = block_sum_u64(acc, red);
     if (threadIdx.x == 0 && acc) atomicAdd(c4 + u, acc);
     __syncthreads();
   }
+#ifdef FGLT_DENSE_PROF
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&g_dense_done, 1u) == gridDim.x - 1) {
+    unsigned long long t = 0;
+    for (int k = 0; k < 7; ++k) t += g_dense_prof[k];
+    printf("dense phases (warp-cycles %%): zero %.1f count %.1f cbar %.1f sweep %.1f attr %.1f abar %.1f setup %.1f\n",
+           100.0 * g_dense_prof[0] / t, 100.0 * g_dense_prof[1] / t, 100.0 * g_dense_prof[2] / t,
+           100.0 * g_dense_prof[3] / t, 100.0 * g_dense_prof[4] / t, 100.0 * g_dense_prof[5] / t,
+           100.0 * g_dense_prof[6] / t);
+    for (int k = 0; k < 8; ++k) g_dense_prof[k] = 0;
+    g_dense_done = 0;
+  }
+#endif
 }
 
 // ================================================== diamonds and 4-cliques
