@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verify", action="store_true",
+                    help="N>1: rank 0 checks the gathered rows against a one-GPU transform")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -189,10 +191,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("FGLT_DIST_BACKEND", "nccl") != "nccl":
+        local %= torch.cuda.device_count()  # one-GPU test of the N>1 path only
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL over NVLink; FGLT_DIST_BACKEND=gloo only for the one-GPU test of
+        # this code path (tests/test_gpu_parity.py::test_bench_two_ranks_gloo)
+        backend = os.environ.get("FGLT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     name, rp_h, ci_h = load_graph(args.config)
     n, nnz = len(rp_h) - 1, len(ci_h)
@@ -290,6 +300,12 @@ def main():
     # correctness spot check of the e2e output against the device output (N=1)
     if world == 1:
         assert torch.equal(raw_p, raw_d.cpu()) and torch.equal(net_p, net_d.cpu())
+    elif args.verify and rank == 0:
+        one = _capi.Context(local, stream.cuda_stream)
+        raw1, net1, _ = one.transform_host(rp_h, ci_h, mask, False)
+        assert np.array_equal(raw_p.numpy().view(np.uint64), raw1), "sharded raw differs"
+        assert np.array_equal(net_p.numpy().view(np.uint64), net1), "sharded net differs"
+        one.close()
 
     if rank != 0:
         if world > 1:

@@ -154,6 +154,38 @@ int fglt_stage_epilogue(fglt_ctx* ctx, int64_t v0, int64_t v1,
                         uint64_t* d_raw_rows, uint64_t* d_net_rows,
                         fglt_error* err);
 
+/* ------------------------------------------------------------- per-kernel
+ * The reference's public per-kernel functions on the device
+ * (include/graphlet/kernels.hpp:43-98, src/kernels.cpp:26-288), same inputs
+ * and outputs: host arrays, uint64 vectors of n, the per-edge C3 of nnz
+ * entries aligned with col_idx (SparseCountMatrix, kernels.hpp:17-40).
+ * Caller vectors (p1, p2, c3, C3) are used as given, as the reference does.
+ * Checked sites return FGLT_E_OVERFLOW with the reference's graphlet id and
+ * the lowest offending vertex. compute_c4_d14 and compute_d15 are the
+ * transform's own columns (graphlet:: layer, dictionary {12,14} / {15}). */
+/* compute_p2 (kernels.cpp:26-39) */
+int fglt_kernel_p2(fglt_ctx* ctx, const int32_t* row_ptr, const int32_t* col_idx, int64_t n,
+                   int64_t nnz, const uint64_t* p1, uint64_t* p2, fglt_error* err);
+/* compute_c3_C3 (kernels.cpp:41-89): c3 (n) and C3 (nnz) */
+int fglt_kernel_c3(fglt_ctx* ctx, const int32_t* row_ptr, const int32_t* col_idx, int64_t n,
+                   int64_t nnz, uint64_t* c3, uint64_t* C3, fglt_error* err);
+/* compute_p3 (kernels.cpp:91-107) */
+int fglt_kernel_p3(fglt_ctx* ctx, const int32_t* row_ptr, const int32_t* col_idx, int64_t n,
+                   int64_t nnz, const uint64_t* p1, const uint64_t* p2, const uint64_t* c3,
+                   uint64_t* p3, fglt_error* err);
+/* compute_d7 (kernels.cpp:149-163), checked: graphlet 7 */
+int fglt_kernel_d7(fglt_ctx* ctx, const int32_t* row_ptr, const int32_t* col_idx, int64_t n,
+                   int64_t nnz, const uint64_t* p1, uint64_t* d7, fglt_error* err);
+/* compute_d8 (kernels.cpp:165-174), checked: graphlet 8 */
+int fglt_kernel_d8(fglt_ctx* ctx, int64_t n, const uint64_t* p1, uint64_t* d8, fglt_error* err);
+/* compute_d9_d10_d11 (kernels.cpp:176-205), checked: graphlets 9, 10, 11 */
+int fglt_kernel_d9_d10_d11(fglt_ctx* ctx, const int32_t* row_ptr, const int32_t* col_idx,
+                           int64_t n, int64_t nnz, const uint64_t* p1, const uint64_t* c3,
+                           const uint64_t* C3, uint64_t* d9, uint64_t* d10, uint64_t* d11,
+                           fglt_error* err);
+/* compute_d13 (kernels.cpp:207-232) for the caller's C3 */
+int fglt_kernel_d13(fglt_ctx* ctx, const int32_t* row_ptr, const int32_t* col_idx, int64_t n,
+                    int64_t nnz, const uint64_t* C3, uint64_t* d13, fglt_error* err);
 /* Number of kernels this context has launched so far (CUB calls count 1). */
 uint64_t fglt_ctx_kernel_launches(const fglt_ctx* ctx);
 

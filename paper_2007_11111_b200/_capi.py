@@ -25,7 +25,8 @@ EXPORTS = [
     "fglt_net_from_raw", "fglt_stage_prepare", "fglt_stage_bounds", "fglt_stage_triangles",
     "fglt_stage_local", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
     "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug", "fglt_build_csr",
-    "fglt_csr_fetch",
+    "fglt_csr_fetch", "fglt_kernel_p2", "fglt_kernel_c3", "fglt_kernel_p3", "fglt_kernel_d7",
+    "fglt_kernel_d8", "fglt_kernel_d9_d10_d11", "fglt_kernel_d13",
 ]
 
 DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB = 1, 2, 3, 4

@@ -28,6 +28,7 @@
 #include "fglt_device.cuh"
 #include "fglt_roots.cuh"
 #include "fglt_ingest.cuh"
+#include "fglt_kernels_api.cuh"
 
 using namespace fglt;
 
@@ -63,7 +64,8 @@ enum Buf {
   B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
   B_CUB, B_CURSOR, B_TBND, B_BIGROWS, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
-  B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV, B_COUNT
+  B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV,
+  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_COUNT
 };
 
 struct DevBuf {
@@ -761,8 +763,11 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     }
     if (cnt[3] > 0) {  // class 4: block-flattened hash-partition passes
       const size_t sm = (size_t)(1 << kC4HashLog) * 8;
-      const int g = std::min(cnt[3], c->sms);
       set_smem(k_c4_block<kC4BlockThreads>, sm);
+      int occ = 1;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<kC4BlockThreads>,
+                                                       kC4BlockThreads, sm));
+      const int g = std::min(cnt[3], c->sms * std::max(occ, 1));
       k_c4_block<kC4BlockThreads><<<g, kC4BlockThreads, sm, c->stream>>>(
           c->rp, c->ci, c->split, c->mir, lists[3], cnt[3], wc, parts, kC4HashLog, queues + 1, c4);
       check_launch();
@@ -771,7 +776,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     int* bnd = nullptr;  // absolute tile boundaries of the active rows
     const long long nact = (long long)c->nact;
     const long long kb = nact > 0 ? (nact - 1) / kC4Tile32 + 1 : 0;
-    if ((cnt[4] > 0 || cnt[5] > 0) && kb * nact <= (1ll << 28)) {
+    if ((cnt[4] > 0 || cnt[5] > 0) && kb * nact <= (1ll << 30)) {
       bnd = c->ensure<int>(B_TBND, (size_t)(kb * nact));
       k_tile_bounds<<<c->grid(kb * nact, 256), 256, 0, c->stream>>>(c->rp, c->ci, (int)nact,
                                                                      (int)kb, bnd);
@@ -1387,6 +1392,224 @@ int fglt_stage_epilogue(fglt_ctx* c, int64_t v0, int64_t v1, uint64_t* d_raw_row
     set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
     return f.code;
   }
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- per-kernel
+// The reference's public per-kernel functions (kernels.hpp:43-98) on the
+// device; host arrays in and out (fglt_kernels_api.cuh).
+namespace {
+
+struct ApiCall {
+  fglt_ctx* c;
+  fglt_error* err;
+  const int* d_rp = nullptr;
+  const int* d_ci = nullptr;
+};
+
+// Device copies of the CSR (when given) and a fresh error word.
+void api_begin(ApiCall& a, const int32_t* rp, const int32_t* ci, int64_t n, int64_t nnz) {
+  fglt_ctx* c = a.c;
+  CK(cudaSetDevice(c->device));
+  c->timing = false;
+  c->d_small = c->ensure<u64>(B_SMALL, 64);
+  u64 init = ~0ull;
+  CK(cudaMemcpyAsync(c->d_small, &init, 8, cudaMemcpyHostToDevice, c->stream));
+  if (rp) {
+    int* drp = c->ensure<int>(B_RP_IN, n + 1);
+    int* dci = c->ensure<int>(B_CI_IN, std::max<int64_t>(nnz, 1));
+    CK(cudaMemcpyAsync(drp, rp, (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+    if (nnz) CK(cudaMemcpyAsync(dci, ci, (size_t)nnz * 4, cudaMemcpyHostToDevice, c->stream));
+    a.d_rp = drp;
+    a.d_ci = dci;
+  }
+}
+
+u64* api_upload(fglt_ctx* c, Buf b, const uint64_t* h, int64_t cnt) {
+  u64* d = c->ensure<u64>(b, (size_t)std::max<int64_t>(cnt, 1));
+  if (cnt > 0) CK(cudaMemcpyAsync(d, h, (size_t)cnt * 8, cudaMemcpyHostToDevice, c->stream));
+  return d;
+}
+
+void api_download(fglt_ctx* c, uint64_t* h, const u64* d, int64_t cnt) {
+  if (cnt > 0 && h) CK(cudaMemcpyAsync(h, d, (size_t)cnt * 8, cudaMemcpyDeviceToHost, c->stream));
+}
+
+template <class F>
+int api_run(fglt_ctx* c, fglt_error* err, int64_t n, int64_t nnz, bool csr, F&& body) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!c) {
+    set_err(err, FGLT_E_NO_DEVICE, -1, -1, "null context");
+    return FGLT_E_NO_DEVICE;
+  }
+  int rc = csr ? validate_shape(n, nnz, err) : (n < 0 || n >= ((int64_t)1 << 31) ? FGLT_E_STRUCTURAL : 0);
+  if (rc) {
+    if (!csr) set_err(err, rc, -1, -1, "vector length outside the int32 limits");
+    return rc;
+  }
+  try {
+    body();
+    return read_error(c, err, true);
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
+// Relabelled pipeline up to the per-edge triangle counts (and optionally the
+// diamond roots); C3/c3 land in original order in B_API4 / B_API5.
+void api_c3(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t nnz, bool d13) {
+  const unsigned mask = 3u | (1u << 4) | (d13 ? (1u << 13) : 0u);
+  prepare(c, d_rp, d_ci, n, nnz, mask, 1);
+  u64* C3 = c->ensure<u64>(B_API4, (size_t)std::max<int64_t>(nnz, 1));
+  u64* c3 = c->ensure<u64>(B_API5, (size_t)std::max<int64_t>(n, 1));
+  if (n == 0) return;
+  read_graph_stats(c);
+  triangles(c, 0, n);
+  local_sweeps(c);
+  k_api_map_c3<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(d_rp, d_ci, (int)n, c->inv, c->rp,
+                                                           c->ci, c->C3f, c->V(V_C3), C3, c3);
+  check_launch();
+  c->launched();
+}
+
+}  // namespace
+
+extern "C" {
+
+int fglt_kernel_p2(fglt_ctx* c, const int32_t* rp, const int32_t* ci, int64_t n, int64_t nnz,
+                   const uint64_t* p1, uint64_t* p2, fglt_error* err) {
+  return api_run(c, err, n, nnz, true, [&] {
+    ApiCall a{c, err};
+    api_begin(a, rp, ci, n, nnz);
+    u64* dp1 = api_upload(c, B_API0, p1, n);
+    u64* out = c->ensure<u64>(B_API1, (size_t)std::max<int64_t>(n, 1));
+    if (n) {
+      k_api_p2<<<c->grid(n, 128), 128, 0, c->stream>>>(a.d_rp, a.d_ci, (int)n, dp1, out);
+      check_launch();
+      c->launched();
+    }
+    api_download(c, p2, out, n);
+  });
+}
+
+int fglt_kernel_p3(fglt_ctx* c, const int32_t* rp, const int32_t* ci, int64_t n, int64_t nnz,
+                   const uint64_t* p1, const uint64_t* p2, const uint64_t* c3, uint64_t* p3,
+                   fglt_error* err) {
+  return api_run(c, err, n, nnz, true, [&] {
+    ApiCall a{c, err};
+    api_begin(a, rp, ci, n, nnz);
+    u64* dp1 = api_upload(c, B_API0, p1, n);
+    u64* dp2 = api_upload(c, B_API1, p2, n);
+    u64* dc3 = api_upload(c, B_API2, c3, n);
+    u64* out = c->ensure<u64>(B_API3, (size_t)std::max<int64_t>(n, 1));
+    if (n) {
+      k_api_p3<<<c->grid(n, 128), 128, 0, c->stream>>>(a.d_rp, a.d_ci, (int)n, dp1, dp2, dc3, out);
+      check_launch();
+      c->launched();
+    }
+    api_download(c, p3, out, n);
+  });
+}
+
+int fglt_kernel_d7(fglt_ctx* c, const int32_t* rp, const int32_t* ci, int64_t n, int64_t nnz,
+                   const uint64_t* p1, uint64_t* d7, fglt_error* err) {
+  return api_run(c, err, n, nnz, true, [&] {
+    ApiCall a{c, err};
+    api_begin(a, rp, ci, n, nnz);
+    u64* dp1 = api_upload(c, B_API0, p1, n);
+    u64* out = c->ensure<u64>(B_API1, (size_t)std::max<int64_t>(n, 1));
+    if (n) {
+      k_api_d7<<<c->grid(n, 128), 128, 0, c->stream>>>(a.d_rp, a.d_ci, (int)n, dp1, out, c->d_small);
+      check_launch();
+      c->launched();
+    }
+    api_download(c, d7, out, n);
+  });
+}
+
+int fglt_kernel_d8(fglt_ctx* c, int64_t n, const uint64_t* p1, uint64_t* d8, fglt_error* err) {
+  return api_run(c, err, n, 0, false, [&] {
+    ApiCall a{c, err};
+    api_begin(a, nullptr, nullptr, n, 0);
+    u64* dp1 = api_upload(c, B_API0, p1, n);
+    u64* out = c->ensure<u64>(B_API1, (size_t)std::max<int64_t>(n, 1));
+    if (n) {
+      k_api_d8<<<c->grid(n, 128), 128, 0, c->stream>>>((int)n, dp1, out, c->d_small);
+      check_launch();
+      c->launched();
+    }
+    api_download(c, d8, out, n);
+  });
+}
+
+int fglt_kernel_d9_d10_d11(fglt_ctx* c, const int32_t* rp, const int32_t* ci, int64_t n,
+                           int64_t nnz, const uint64_t* p1, const uint64_t* c3,
+                           const uint64_t* C3, uint64_t* d9, uint64_t* d10, uint64_t* d11,
+                           fglt_error* err) {
+  return api_run(c, err, n, nnz, true, [&] {
+    ApiCall a{c, err};
+    api_begin(a, rp, ci, n, nnz);
+    u64* dp1 = api_upload(c, B_API0, p1, n);
+    u64* dc3 = api_upload(c, B_API1, c3, n);
+    u64* dC3 = api_upload(c, B_API2, C3, nnz);
+    u64* out = c->ensure<u64>(B_API3, 3 * (size_t)std::max<int64_t>(n, 1));
+    if (n) {
+      k_api_d9_11<<<c->grid(n, 128), 128, 0, c->stream>>>(a.d_rp, a.d_ci, (int)n, dp1, dc3, dC3,
+                                                         out, out + n, out + 2 * n, c->d_small);
+      check_launch();
+      c->launched();
+    }
+    api_download(c, d9, out, n);
+    api_download(c, d10, out + n, n);
+    api_download(c, d11, out + 2 * n, n);
+  });
+}
+
+int fglt_kernel_c3(fglt_ctx* c, const int32_t* rp, const int32_t* ci, int64_t n, int64_t nnz,
+                   uint64_t* c3, uint64_t* C3, fglt_error* err) {
+  return api_run(c, err, n, nnz, true, [&] {
+    ApiCall a{c, err};
+    api_begin(a, rp, ci, n, nnz);
+    api_c3(c, a.d_rp, a.d_ci, n, nnz, false);
+    api_download(c, C3, reinterpret_cast<u64*>(c->buf[B_API4].p), nnz);
+    api_download(c, c3, reinterpret_cast<u64*>(c->buf[B_API5].p), n);
+  });
+}
+
+int fglt_kernel_d13(fglt_ctx* c, const int32_t* rp, const int32_t* ci, int64_t n, int64_t nnz,
+                    const uint64_t* C3, uint64_t* d13, fglt_error* err) {
+  return api_run(c, err, n, nnz, true, [&] {
+    ApiCall a{c, err};
+    api_begin(a, rp, ci, n, nnz);
+    u64* given = api_upload(c, B_API0, C3, nnz);
+    u64* out = c->ensure<u64>(B_API1, (size_t)std::max<int64_t>(n, 1));
+    if (n == 0) return;
+    // The caller's C3 is usually the graph's own (compute_c3_C3): then the
+    // root-centric diamond pass applies. Any other C3 is honoured literally.
+    api_c3(c, a.d_rp, a.d_ci, n, nnz, true);
+    unsigned long long* nd = reinterpret_cast<unsigned long long*>(c->d_small + 40);
+    CK(cudaMemsetAsync(nd, 0, 8, c->stream));
+    if (nnz) {
+      k_api_diff<<<c->grid(nnz, 256), 256, 0, c->stream>>>(
+          given, reinterpret_cast<u64*>(c->buf[B_API4].p), nnz, nd);
+      check_launch();
+      c->launched();
+    }
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, nd, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h == 0) {
+      roots(c, 0, n);
+      k_api_gather<<<c->grid(n, 256), 256, 0, c->stream>>>(c->V(V_D13), c->inv, (int)n, out);
+    } else {
+      k_api_d13<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(a.d_rp, a.d_ci, (int)n, given, out);
+    }
+    check_launch();
+    c->launched();
+    api_download(c, d13, out, n);
+  });
 }
 
 }  // extern "C"

@@ -264,9 +264,16 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 //   5 dense tiles, 16-bit packed counters (|N-(u)| < 65536), 96K ids per tile
 //   6 dense tiles, 32-bit counters, 48K ids per tile
 // Class 4 vs 5/6 is chosen per root by the cheaper of the two modelled costs.
-constexpr int kC4HashLog = 14;              // 16384 slots (keys + counts = 128 KB)
+#ifndef FGLT_C4B_LOG
+#define FGLT_C4B_LOG 14
+#define FGLT_C4B_THREADS 1024
+#endif
+#ifndef FGLT_HASH_WEIGHT
+#define FGLT_HASH_WEIGHT 1
+#endif
+constexpr int kC4HashLog = FGLT_C4B_LOG;    // 16384 slots (keys + counts = 128 KB)
 constexpr int kC4SmallLog = 12;             // 4096 slots (32 KB)
-constexpr u64 kC4HashFill = 12288;          // distinct targets per pass (LF 0.75)
+constexpr u64 kC4HashFill = 3ull << (kC4HashLog - 2);  // distinct targets per pass (LF 0.75)
 #ifndef FGLT_DENSE_THREADS
 #define FGLT_DENSE_THREADS 1024
 #define FGLT_DENSE_TILE_BYTES 196608
@@ -281,7 +288,7 @@ constexpr int kC4Long = 48;                 // rows at least this long: flattene
 #endif
 constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many wedges in a tile: warp per row
 constexpr int kQuadsInFlight = 2;          // 16-byte loads in flight per lane (dense batches)
-constexpr int kC4BlockThreads = 1024;      // class-4 block (one 128 KB table per SM)
+constexpr int kC4BlockThreads = FGLT_C4B_THREADS;  // class-4 block (one 128 KB table per SM)
 
 __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
                            const u64* __restrict__ wc, int u0, int u1, u64* __restrict__ cls,
@@ -301,7 +308,7 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
     } else {
       const u64 nq = (u64)(split[u] - rp[u]);
       P = (w + kC4HashFill - 1) / kC4HashFill;
-      const u64 cost_hash = P * (w + 16384) + w;
+      const u64 cost_hash = FGLT_HASH_WEIGHT * (P * (w + (1ull << kC4HashLog)) + w);
       const bool pack = nq < 65536;
       const u64 tile = pack ? kC4Tile16 : kC4Tile32;
       const u64 tiles = ((u64)u + tile - 1) / tile;

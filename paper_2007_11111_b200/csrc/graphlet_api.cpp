@@ -618,4 +618,150 @@ NetFrequencyField net_from_raw(const RawFrequencyField& raw, const ConversionMat
   return net;
 }
 
+// ============================================================ per-kernel API
+// The reference's public per-kernel functions (kernels.hpp:43-98), each one
+// device call through the C-ABI (fglt_kernel_*, fglt_kernels_api.cuh) or a
+// column of the device transform. `threads` is accepted for source
+// compatibility only.
+namespace {
+
+template <class F>
+void device_call(F&& f) {
+  fglt_ctx* ctx = context_for(0);
+  fglt_error err{};
+  int rc;
+  {
+    std::lock_guard<std::mutex> lock(g_run_mu);
+    rc = f(ctx, &err);
+  }
+  if (rc) rethrow(rc, err);
+}
+
+void need_size(const std::vector<count_t>& v, vertex_t n, const char* what) {
+  if (static_cast<vertex_t>(v.size()) < n)
+    throw Error(std::string(what) + " is shorter than the vertex count");
+}
+
+std::vector<count_t> column(const RawFrequencyField& f, int id) {
+  std::vector<count_t> out(static_cast<std::size_t>(f.num_vertices()));
+  const std::size_t c = f.dictionary().position_of(id);
+  for (vertex_t v = 0; v < f.num_vertices(); ++v) out[v] = f.at(v, c);
+  return out;
+}
+
+}  // namespace
+
+std::vector<count_t> compute_p2(const SparseAdjacency& g, const std::vector<count_t>& p1, int) {
+  const vertex_t n = g.num_vertices();
+  need_size(p1, n, "p1");
+  std::vector<count_t> p2(static_cast<std::size_t>(n));
+  const Csr32& c = g.csr32();
+  device_call([&](fglt_ctx* ctx, fglt_error* e) {
+    return fglt_kernel_p2(ctx, c.row_ptr.data(), c.col_idx.data(), n,
+                          static_cast<std::int64_t>(c.col_idx.size()), p1.data(), p2.data(), e);
+  });
+  return p2;
+}
+
+std::pair<std::vector<count_t>, SparseCountMatrix> compute_c3_C3(const SparseAdjacency& g, int) {
+  const vertex_t n = g.num_vertices();
+  const Csr32& c = g.csr32();
+  std::vector<count_t> c3(static_cast<std::size_t>(n)), C3(c.col_idx.size());
+  device_call([&](fglt_ctx* ctx, fglt_error* e) {
+    return fglt_kernel_c3(ctx, c.row_ptr.data(), c.col_idx.data(), n,
+                          static_cast<std::int64_t>(c.col_idx.size()), c3.data(), C3.data(), e);
+  });
+  return {std::move(c3), SparseCountMatrix(g, std::move(C3))};
+}
+
+std::vector<count_t> compute_p3(const SparseAdjacency& g, const std::vector<count_t>& p1,
+                                const std::vector<count_t>& p2, const std::vector<count_t>& c3,
+                                int) {
+  const vertex_t n = g.num_vertices();
+  need_size(p1, n, "p1");
+  need_size(p2, n, "p2");
+  need_size(c3, n, "c3");
+  std::vector<count_t> p3(static_cast<std::size_t>(n));
+  const Csr32& c = g.csr32();
+  device_call([&](fglt_ctx* ctx, fglt_error* e) {
+    return fglt_kernel_p3(ctx, c.row_ptr.data(), c.col_idx.data(), n,
+                          static_cast<std::int64_t>(c.col_idx.size()), p1.data(), p2.data(),
+                          c3.data(), p3.data(), e);
+  });
+  return p3;
+}
+
+FourCycleResult compute_c4_d14(const SparseAdjacency& g, int) {
+  const int ids[] = {12, 14};
+  TransformStats st;
+  RawFrequencyField raw = raw_frequencies(g, Dictionary::from_ids(ids), {}, &st);
+  FourCycleResult r;
+  r.c4 = column(raw, 12);
+  r.d14 = column(raw, 14);
+  r.accumulator_touches = st.p2_row_touches;
+  return r;
+}
+
+std::vector<count_t> compute_d7(const SparseAdjacency& g, const std::vector<count_t>& p1, int) {
+  const vertex_t n = g.num_vertices();
+  need_size(p1, n, "p1");
+  std::vector<count_t> d7(static_cast<std::size_t>(n));
+  const Csr32& c = g.csr32();
+  device_call([&](fglt_ctx* ctx, fglt_error* e) {
+    return fglt_kernel_d7(ctx, c.row_ptr.data(), c.col_idx.data(), n,
+                          static_cast<std::int64_t>(c.col_idx.size()), p1.data(), d7.data(), e);
+  });
+  return d7;
+}
+
+std::vector<count_t> compute_d8(const std::vector<count_t>& p1, int) {
+  std::vector<count_t> d8(p1.size());
+  if (p1.empty()) return d8;
+  device_call([&](fglt_ctx* ctx, fglt_error* e) {
+    return fglt_kernel_d8(ctx, static_cast<std::int64_t>(p1.size()), p1.data(), d8.data(), e);
+  });
+  return d8;
+}
+
+DipperCounts compute_d9_d10_d11(const SparseAdjacency& g, const std::vector<count_t>& p1,
+                                const std::vector<count_t>& c3, const SparseCountMatrix& C3,
+                                int) {
+  const vertex_t n = g.num_vertices();
+  need_size(p1, n, "p1");
+  need_size(c3, n, "c3");
+  const Csr32& c = g.csr32();
+  if (C3.values().size() != c.col_idx.size())
+    throw Error("C3 does not share the graph's CSR pattern");
+  DipperCounts r;
+  r.d9.resize(static_cast<std::size_t>(n));
+  r.d10.resize(static_cast<std::size_t>(n));
+  r.d11.resize(static_cast<std::size_t>(n));
+  device_call([&](fglt_ctx* ctx, fglt_error* e) {
+    return fglt_kernel_d9_d10_d11(ctx, c.row_ptr.data(), c.col_idx.data(), n,
+                                  static_cast<std::int64_t>(c.col_idx.size()), p1.data(),
+                                  c3.data(), C3.values().data(), r.d9.data(), r.d10.data(),
+                                  r.d11.data(), e);
+  });
+  return r;
+}
+
+std::vector<count_t> compute_d13(const SparseAdjacency& g, const SparseCountMatrix& C3, int) {
+  const vertex_t n = g.num_vertices();
+  const Csr32& c = g.csr32();
+  if (C3.values().size() != c.col_idx.size())
+    throw Error("C3 does not share the graph's CSR pattern");
+  std::vector<count_t> d13(static_cast<std::size_t>(n));
+  device_call([&](fglt_ctx* ctx, fglt_error* e) {
+    return fglt_kernel_d13(ctx, c.row_ptr.data(), c.col_idx.data(), n,
+                           static_cast<std::int64_t>(c.col_idx.size()), C3.values().data(),
+                           d13.data(), e);
+  });
+  return d13;
+}
+
+std::vector<count_t> compute_d15(const SparseAdjacency& g, int) {
+  const int ids[] = {15};
+  return column(raw_frequencies(g, Dictionary::from_ids(ids)), 15);
+}
+
 }  // namespace graphlet

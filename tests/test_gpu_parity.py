@@ -8,6 +8,8 @@ incomplete family test_pipeline.cpp:55-65, corrupted raw
 test_conversion.cpp:63-76), and the synthetic configs at sizes the oracle
 finishes in seconds.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -18,6 +20,7 @@ import fglt_testutil as gu
 pytestmark = pytest.mark.gpu
 
 FULL = 0xFFFF
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
@@ -360,3 +363,25 @@ def test_full_size_config_parity(ctx, cfg):
     oraw, onet = ob.transform(rp, ci, FULL, False, 1)
     assert np.array_equal(raw, oraw), name
     assert np.array_equal(net, onet), name
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_gloo():
+    """bench.py's N>1 code path (CSR broadcast, root blocks, the two
+    all-reduces, row gather, max-over-ranks timing) end to end under torchrun
+    with world size 2. Only one GPU exists here, so both ranks share it over
+    gloo (host-staged collectives; no rank's kernels wait on the other's); on
+    the 8-GPU box the same code runs over NCCL."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, FGLT_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29533", "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--config", "1", "--verify"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["e2e"]["value"] > 0

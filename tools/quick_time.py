@@ -27,4 +27,7 @@ for it in range(4):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     print(f"iter {it}: {ms:.3f} ms  -> {n and (nnz//2)/ms/1e3:.3e} edges/s", flush=True)
+import hashlib
+h = hashlib.sha256(raw.cpu().numpy().tobytes() + net.cpu().numpy().tobytes()).hexdigest()[:16]
+print("sha", h)
 print(json.dumps(st))
