@@ -65,7 +65,7 @@ enum Buf {
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
   B_CUB, B_CURSOR, B_TBND, B_BIGROWS, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV,
-  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_COUNT
+  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_TB, B_COUNT
 };
 
 struct DevBuf {
@@ -725,8 +725,19 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   if (P.c4) {
     const int G = group_for((double)c->nnz / (double)c->n);
     DISPATCH_G(G, launch_root_work, c, wc);
+    // degree bands of the dense counters (4 / 8 / 16-or-32 bits)
+    int bands[2] = {0, 0};
+    if (c->nact > 0) {
+      int* d_b = reinterpret_cast<int*>(c->d_small + 41);
+      k_degree_bands<<<1, 32, 0, c->stream>>>(c->rp, (int)c->nact, d_b);
+      check_launch();
+      c->launched();
+      CK(cudaMemcpyAsync(bands, d_b, sizeof(bands), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
     k_c4_class<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(
-        c->rp, c->split, wc, (int)u0, (int)u1, cls, parts, c->force_c4_class, c->force_c4_parts);
+        c->rp, c->split, wc, (int)u0, (int)u1, bands[0], bands[1], cls, parts,
+        c->force_c4_class, c->force_c4_parts);
     check_launch();
     c->launched();
     std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5}, lists, &stride);
@@ -774,14 +785,28 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       c->launched();
     }
     int* bnd = nullptr;  // absolute tile boundaries of the active rows
+    int* tb = nullptr;   // banded tile starts (dense_span), tb[K] = nact
     const long long nact = (long long)c->nact;
-    const long long kb = nact > 0 ? (nact - 1) / kC4Tile32 + 1 : 0;
-    if ((cnt[4] > 0 || cnt[5] > 0) && kb * nact <= (1ll << 30)) {
-      bnd = c->ensure<int>(B_TBND, (size_t)(kb * nact));
-      k_tile_bounds<<<c->grid(kb * nact, 256), 256, 0, c->stream>>>(c->rp, c->ci, (int)nact,
-                                                                     (int)kb, bnd);
-      check_launch();
-      c->launched();
+    if (cnt[4] > 0 || cnt[5] > 0) {
+      std::vector<int> h{0};
+      const long long t4 = 2ll * kC4TileBytes, t8 = kC4TileBytes, t32 = kC4Tile32;
+      for (long long x = 0; x < nact;) {
+        const long long e = x < bands[0] ? std::min<long long>(x + t4, bands[0])
+                          : x < bands[1] ? std::min<long long>(x + t8, bands[1])
+                                         : std::min<long long>(x + t32, nact);
+        h.push_back((int)e);
+        x = e;
+      }
+      const long long K = (long long)h.size() - 1;
+      tb = c->ensure<int>(B_TB, h.size());
+      CK(cudaMemcpyAsync(tb, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      if (K * nact <= (1ll << 30)) {
+        bnd = c->ensure<int>(B_TBND, (size_t)(K * nact));
+        k_tile_bounds<<<c->grid(K * nact, 256), 256, 0, c->stream>>>(c->rp, c->ci, (int)nact,
+                                                                      (int)K, tb, bnd);
+        check_launch();
+        c->launched();
+      }
     }
     for (int bb = 4; bb <= 5; ++bb) {  // classes 5/6: dense tiles
       if (cnt[bb] == 0) continue;
@@ -792,12 +817,12 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         set_smem(k_c4_dense<true>, sm);
         k_c4_dense<true><<<g, kC4DenseThreads, sm, c->stream>>>(
             c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
-            bnd, nact, queues + 2, c4);
+            bnd, nact, tb, bands[0], bands[1], queues + 2, c4);
       } else {
         set_smem(k_c4_dense<false>, sm);
         k_c4_dense<false><<<g, kC4DenseThreads, sm, c->stream>>>(
             c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
-            bnd, nact, queues + 3, c4);
+            bnd, nact, tb, bands[0], bands[1], queues + 3, c4);
       }
       check_launch();
       c->launched();

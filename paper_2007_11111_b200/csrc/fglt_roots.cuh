@@ -271,6 +271,9 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 #ifndef FGLT_HASH_WEIGHT
 #define FGLT_HASH_WEIGHT 1
 #endif
+#ifndef FGLT_TILE_FIXED
+#define FGLT_TILE_FIXED 2048  // per-tile fixed cost (barriers, setup) in the cost model
+#endif
 constexpr int kC4HashLog = FGLT_C4B_LOG;    // 16384 slots (keys + counts = 128 KB)
 constexpr int kC4SmallLog = 12;             // 4096 slots (32 KB)
 constexpr u64 kC4HashFill = 3ull << (kC4HashLog - 2);  // distinct targets per pass (LF 0.75)
@@ -290,9 +293,27 @@ constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many w
 constexpr int kQuadsInFlight = 2;          // 16-byte loads in flight per lane (dense batches)
 constexpr int kC4BlockThreads = FGLT_C4B_THREADS;  // class-4 block (one 128 KB table per SM)
 
+// Dense tiles use counters as narrow as the target's degree allows: L[w] <=
+// deg(w) (each wedge into w has a distinct middle vertex v in N(w)), and the
+// active ids are in ascending degree, so ids [0, b4) (degree <= 15) get 4-bit
+// counters, [b4, b8) (degree <= 255) 8-bit ones, and the rest 16 bits (32
+// when |N-(u)| >= 65536). Tiles never straddle a band: kC4TileBytes hold
+// 2 x kC4TileBytes ids in the 4-bit band, kC4TileBytes in the 8-bit band and
+// kC4Tile32 above (dense_tiles() builds the same boundaries on the host).
+__host__ __device__ inline void dense_span(u64 u, u64 b4, u64 b8, bool pack, u64* tiles,
+                                           u64* bytes) {
+  const u64 nib = u < b4 ? u : b4;
+  const u64 byt = u > b4 ? (u < b8 ? u : b8) - b4 : 0;
+  const u64 rest = u > b8 ? u - b8 : 0;
+  const u64 t4 = 2 * (u64)kC4TileBytes, t8 = kC4TileBytes, t32 = kC4Tile32;
+  *tiles = (nib + t4 - 1) / t4 + (byt + t8 - 1) / t8 + (rest + t32 - 1) / t32;
+  *bytes = (nib + 1) / 2 + byt + rest * (pack ? 2 : 4);
+}
+
 __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
-                           const u64* __restrict__ wc, int u0, int u1, u64* __restrict__ cls,
-                           u64* __restrict__ parts, int force_cls, int force_parts) {
+                           const u64* __restrict__ wc, int u0, int u1, int b4, int b8,
+                           u64* __restrict__ cls, u64* __restrict__ parts, int force_cls,
+                           int force_parts) {
   for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1;
        u += gridDim.x * blockDim.x) {
     const u64 w = wc[u];
@@ -310,9 +331,9 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       P = (w + kC4HashFill - 1) / kC4HashFill;
       const u64 cost_hash = FGLT_HASH_WEIGHT * (P * (w + (1ull << kC4HashLog)) + w);
       const bool pack = nq < 65536;
-      const u64 tile = pack ? kC4Tile16 : kC4Tile32;
-      const u64 tiles = ((u64)u + tile - 1) / tile;
-      const u64 cost_dense = tiles * (kC4TileBytes / 8 + nq) + 2 * w;
+      u64 tiles, bytes;
+      dense_span((u64)u, (u64)b4, (u64)b8, pack, &tiles, &bytes);
+      const u64 cost_dense = bytes / 8 + tiles * (FGLT_TILE_FIXED + nq) + 2 * w;
       if (cost_hash <= cost_dense) c = 4;
       else c = pack ? 5 : 6;
     }
@@ -644,18 +665,31 @@ k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
 }
 
 // Absolute tile boundaries of the active rows, shared by every dense root:
-// bnd[k * nact + v] = first position in N(v) with id >= k * kC4Tile32
-// (k = 0..K-1). A row's segment in a tile is then two independent loads
-// instead of a dependent binary search per (root, row, tile).
+// bnd[k * nact + v] = first position in N(v) with id >= tb[k] (k = 0..K-1,
+// tb = the banded tile starts). A row's segment in a tile is then two
+// independent loads instead of a dependent binary search per (root, row, tile).
 __global__ void k_tile_bounds(const int* __restrict__ rp, const int* __restrict__ ci, int nact,
-                              int K, int* __restrict__ bnd) {
+                              int K, const int* __restrict__ tb, int* __restrict__ bnd) {
   const long long total = (long long)K * nact;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const int k = (int)(i / nact);
     const int v = (int)(i - (long long)k * nact);
-    bnd[i] = k == 0 ? rp[v] : lower_bound_i32(ci, rp[v], rp[v + 1], k * kC4Tile32);
+    bnd[i] = k == 0 ? rp[v] : lower_bound_i32(ci, rp[v], rp[v + 1], tb[k]);
   }
+}
+
+// Degree bands of the active range (ids ascending in degree): out[0] = first
+// id with degree > 15, out[1] = first id with degree > 255.
+__global__ void k_degree_bands(const int* __restrict__ rp, int nact, int* __restrict__ out) {
+  if (threadIdx.x >= 2 || blockIdx.x) return;
+  const int lim = threadIdx.x == 0 ? 15 : 255;
+  int lo = 0, hi = nact;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (rp[mid + 1] - rp[mid] <= lim) lo = mid + 1; else hi = mid;
+  }
+  out[threadIdx.x] = lo;
 }
 
 // Optional phase timers for the dense kernel (profiling builds only,
@@ -681,7 +715,8 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, int* __restrict__ cursor,
            long long cursor_stride, const int* __restrict__ bnd, long long bnd_stride,
-           int* __restrict__ next_root, u64* __restrict__ c4) {
+           const int* __restrict__ tb, int b4, int b8, int* __restrict__ next_root,
+           u64* __restrict__ c4) {
   // roots are sorted by work (largest first) and handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
@@ -693,7 +728,6 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   __shared__ int bsb_all[NW][32];
   __shared__ int next_batch[2];
   __shared__ int next_giant[2];
-  constexpr int TILE = PACK ? kC4Tile16 : kC4Tile32;
   u32* L = reinterpret_cast<u32*>(smem_raw);
   int* cur = cursor + (long long)blockIdx.x * 2 * cursor_stride;
   int* segend = cur + cursor_stride;
@@ -703,13 +737,14 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   int* boff = boff_all[wid];
   int* bsa = bsa_all[wid];
   int* bsb = bsb_all[wid];
+  // counters of the current tile: 2^sh per 32-bit word, 32 >> sh bits each
+  int sh = 0;
   auto inc = [&](int off) {
-    if (PACK) atomicAdd(L + (off >> 1), 1u << ((off & 1) << 4));
-    else atomicAdd(L + off, 1u);
+    atomicAdd(L + (off >> sh), 1u << ((off & ((1 << sh) - 1)) << (5 - sh)));
   };
   auto get = [&](int off) -> u32 {
-    if (PACK) return (L[off >> 1] >> ((off & 1) << 4)) & 0xffffu;
-    return L[off];
+    const u32 x = L[off >> sh] >> ((off & ((1 << sh) - 1)) << (5 - sh));
+    return sh ? x & ((1u << (32 >> sh)) - 1u) : x;
   };
   rs[lane] = 0;
 #ifdef FGLT_DENSE_PROF
@@ -732,7 +767,8 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     }
     const int qs = lo_q;
     // giant rows: expected >= 512 elements per tile -> warp per row
-    const int ntiles = (u + TILE - 1) / TILE;
+    int ntiles = 0;
+    while (tb[ntiles] < u) ++ntiles;
     const int giant_deg = max(kC4Long, kC4GiantPerTile * ntiles);
     hi_q = nq;
     while (lo_q < hi_q) {
@@ -744,10 +780,11 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     const int nb = (qg - qs + 31) >> 5;  // batches of 32 long rows
     for (int q = threadIdx.x; q < nq; q += blockDim.x) cur[q] = rp[ci[b + q]];
     u64 acc = 0;
-    for (int lo = 0; lo < u; lo += TILE) {
-      const int hi = min(lo + TILE, u);
-      const int words = PACK ? (hi - lo + 1) >> 1 : hi - lo;
-      const long long kb_lo = lo / kC4Tile32, kb_hi = kb_lo + TILE / kC4Tile32;
+    for (int t = 0; t < ntiles; ++t) {
+      const int lo = tb[t], hi = min(tb[t + 1], u);
+      sh = lo < b4 ? 3 : lo < b8 ? 2 : (PACK ? 1 : 0);
+      const int words = (hi - lo + (1 << sh) - 1) >> sh;
+      const long long kb_lo = t, kb_hi = t + 1;
       {
         uint4* L4 = reinterpret_cast<uint4*>(L);
         const int n4 = (words + 3) >> 2;
@@ -858,31 +895,27 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         // 16-byte sweep; words past the tile end were zeroed with the tile
         const uint4* L4 = reinterpret_cast<const uint4*>(L);
         const int n4 = (words + 3) >> 2;
-        const u32 ge2 = PACK ? 0xfffefffeu : 0xfffffffeu;  // some counter >= 2
+        // some counter >= 2 in the word
+        const u32 ge2 = sh == 3 ? 0xeeeeeeeeu : sh == 2 ? 0xfefefefeu : sh == 1 ? 0xfffefffeu
+                                                                              : 0xfffffffeu;
+        const int per = 1 << sh, bits = 32 >> sh;
+        const u32 vmask = sh ? (1u << bits) - 1u : 0xffffffffu;
         for (int i4 = threadIdx.x; i4 < n4; i4 += blockDim.x) {
           const uint4 v = L4[i4];
           if (((v.x | v.y | v.z | v.w) & ge2) == 0) continue;
           const u32 xs[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const u32 x = xs[j];
-            const int i = 4 * i4 + j;
-            if (PACK) {
-              const u32 l0 = x & 0xffffu, l1 = x >> 16;
-              if (l0 >= 2) {
-                const u64 c = (u64)l0 * (l0 - 1) / 2;
+            u32 x = xs[j];
+            if ((x & ge2) == 0) continue;
+            const int base = lo + ((4 * i4 + j) << sh);
+            for (int q = 0; q < per; ++q, x = bits < 32 ? x >> bits : 0) {
+              const u32 l = x & vmask;
+              if (l >= 2) {
+                const u64 c = (u64)l * (l - 1) / 2;
                 acc += c;
-                atomicAdd(c4 + lo + 2 * i, c);
+                atomicAdd(c4 + base + q, c);
               }
-              if (l1 >= 2) {
-                const u64 c = (u64)l1 * (l1 - 1) / 2;
-                acc += c;
-                atomicAdd(c4 + lo + 2 * i + 1, c);
-              }
-            } else if (x >= 2) {
-              const u64 c = (u64)x * (x - 1) / 2;
-              acc += c;
-              atomicAdd(c4 + lo + i, c);
             }
           }
         }
