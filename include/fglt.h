@@ -196,6 +196,7 @@ uint64_t fglt_ctx_kernel_launches(const fglt_ctx* ctx);
 #define FGLT_DEBUG_C4_PARTS 2  /* hash passes per root when class 2 is forced  */
 #define FGLT_DEBUG_ROOTS_BIN 3 /* 0 auto, 1..4 smem bitmap bins, 5 global slab */
 #define FGLT_DEBUG_HUB 4       /* 0 auto, 1 no hub rows, 2 hub rows for every hub member */
+#define FGLT_DEBUG_TRILIST 5   /* 0 auto, 1 no triangle list, 2 tiny list pool (fallbacks) */
 int fglt_ctx_set_debug(fglt_ctx* ctx, int key, int value);
 
 /* Library facts */

@@ -29,7 +29,7 @@ EXPORTS = [
     "fglt_kernel_d8", "fglt_kernel_d9_d10_d11", "fglt_kernel_d13",
 ]
 
-DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB = 1, 2, 3, 4
+DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB, DEBUG_TRILIST = 1, 2, 3, 4, 5
 
 
 class FgltError(ctypes.Structure):

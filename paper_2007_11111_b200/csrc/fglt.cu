@@ -65,7 +65,8 @@ enum Buf {
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
   B_CUB, B_CURSOR, B_TBND, B_BIGROWS, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV,
-  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_TB, B_COUNT
+  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_TB, B_TLREC, B_TLPIECES, B_TLFAIL,
+  B_COUNT
 };
 
 struct DevBuf {
@@ -214,6 +215,10 @@ struct fglt_ctx {
 
   // test hooks (fglt_ctx_set_debug): force one code path for every root
   int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1, force_hub = 0;
+  // triangle list (k_roots_block -> k_diamond_list); tl_mode: 0 auto, 1 off,
+  // 2 a tiny pool (test hook: most roots fall back to the probing pass)
+  int tl_mode = 0;
+  TriList tl;
   // hub rows (k_hub_rows): built once per graph by the first root pass
   bool hub_built = false;
   bool big_rows_listed = false;  // list_big_rows
@@ -682,7 +687,7 @@ void roots_pass(fglt_ctx* c) {
     set_smem(k_roots_block<kC3, kD13, kD15, GLOBAL, NT>, sm);                                      \
     k_roots_block<kC3, kD13, kD15, GLOBAL, NT><<<g, NT, sm, c->stream>>>(                         \
         c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], L, slab, slab_stride,           \
-        queues + b, d13, d15, c->hub, c->hub_base, c->hub_hb, c->force_hub == 2);                  \
+        queues + b, d13, d15, c->hub, c->hub_base, c->hub_hb, c->force_hub == 2, c->tl);           \
   } while (0)
     if (global) {
       slab_stride = (long long)((L.bytes_aux() + 255) & ~(size_t)255);
@@ -702,12 +707,69 @@ void roots_pass(fglt_ctx* c) {
   }
 }
 
+// Triangle-list pool for the roots [u0,u1) (see TriList): sized by the
+// C(|S|,2) bound plus one grab per block, capped at 45% of free memory.
+void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
+  c->tl = TriList{};
+  const Plan& P = c->plan;
+  if (!(P.c3 && P.d13) || c->tl_mode == 1 || u1 <= u0) return;
+  unsigned long long* d_bound = reinterpret_cast<unsigned long long*>(c->d_small + 24);
+  CK(cudaMemsetAsync(d_bound, 0, 4 * sizeof(u64), c->stream));
+  k_trilist_bound<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(c->split, c->send, (int)u0,
+                                                               (int)u1, d_bound);
+  check_launch();
+  c->launched();
+  unsigned long long bound = 0;
+  CK(cudaMemcpyAsync(&bound, d_bound, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (bound == 0) return;
+  const unsigned long long blocks = (unsigned long long)c->sms * 8 * 4 * 4;
+  unsigned long long cap = bound + blocks * kTriListChunk;
+  if (cap * 8 > c->buf[B_TLREC].cap) {  // growing: stay within 45% of free memory
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    cap = std::min<unsigned long long>(
+        cap, (unsigned long long)(0.45 * (double)(free_b + c->buf[B_TLREC].cap)) / 8);
+  }
+  if (c->tl_mode == 2) cap = 4096;
+  if (cap < 1024) return;
+  TriList t;
+  t.rec = c->ensure<uint2>(B_TLREC, cap);
+  t.cap = cap;
+  t.top = d_bound + 1;
+  t.npieces = reinterpret_cast<unsigned*>(d_bound + 2);
+  t.pieces_cap = (unsigned)std::min<int64_t>(2 * (u1 - u0) + c->nnz / 32 + 1024, 1ll << 31);
+  t.pieces = c->ensure<TriPiece>(B_TLPIECES, t.pieces_cap);
+  t.fail = c->ensure<unsigned char>(B_TLFAIL, (size_t)c->n);
+  CK(cudaMemsetAsync(t.fail, 0, (size_t)c->n, c->stream));
+  c->tl = t;
+}
+
+// Diamonds of the listed roots (the rest take the probing pass).
+void diamond_list(fglt_ctx* c) {
+  if (!c->tl.rec) return;
+  constexpr int NT = 256;
+  const size_t sm = (size_t)std::min<u64>(std::max<u64>(c->maxout, 1), kTriListMaxS) * 8;
+  set_smem(k_diamond_list<NT>, sm);
+  int occ = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_diamond_list<NT>, NT, sm));
+  int* next = reinterpret_cast<int*>(c->d_small + 27);
+  CK(cudaMemsetAsync(next, 0, sizeof(int), c->stream));
+  k_diamond_list<NT><<<c->sms * std::max(occ, 1), NT, sm, c->stream>>>(
+      c->tl.pieces, c->tl.npieces, c->tl.pieces_cap, c->tl.rec, c->rp, c->ci, c->split, c->send,
+      c->C3f, c->tl.fail, next, c->V(V_D13));
+  check_launch();
+  c->launched();
+}
+
 // Triangle pass over roots [u0,u1): per-edge C3 (and d15 when requested).
 void triangles(fglt_ctx* c, int64_t u0, int64_t u1) {
   const Plan& P = c->plan;
+  c->tl = TriList{};
   if (!(P.c3 || P.d15) || c->n == 0) return;
   if (P.c3) CK(cudaMemsetAsync(c->C3f, 0, (size_t)std::max<int64_t>(c->nnz, 1) * 4, c->stream));
   root_bins(c, u0, u1);
+  setup_trilist(c, u0, u1);
   if (P.c3 && P.d15) roots_pass<true, false, true>(c);
   else if (P.c3) roots_pass<true, false, false>(c);
   else roots_pass<false, false, true>(c);
@@ -832,6 +894,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   if (P.d13) {
     root_bins(c, u0, u1);
     c->mark("roots:start");
+    diamond_list(c);
     roots_pass<false, true, false>(c);
     c->mark("roots:end");
   }
@@ -1126,6 +1189,7 @@ int fglt_ctx_set_debug(fglt_ctx* c, int key, int value) {
     case FGLT_DEBUG_C4_PARTS: c->force_c4_parts = value; return FGLT_OK;
     case FGLT_DEBUG_ROOTS_BIN: c->force_roots_bin = value; return FGLT_OK;
     case FGLT_DEBUG_HUB: c->force_hub = value; c->hub_built = false; return FGLT_OK;
+    case FGLT_DEBUG_TRILIST: c->tl_mode = value; return FGLT_OK;
     default: return FGLT_E_PARSE;
   }
 }

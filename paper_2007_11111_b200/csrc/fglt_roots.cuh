@@ -484,8 +484,15 @@ __device__ __forceinline__ void warp_for_each(const int* __restrict__ a, int st,
 // Block-wide flattening of one segment per thread: writes exclusive offsets
 // (g_off[0..nthreads], g_off[nthreads] = total) and per-row element bases
 // g_st[r] = start - off; returns the total. Contains __syncthreads.
+struct NoReserve {
+  __device__ void operator()(int) const {}
+};
+
+// R(total) is called by one thread between the second and third barrier, so
+// whatever it writes to shared memory is visible to the block on return.
+template <class R = NoReserve>
 __device__ __forceinline__ int block_flatten(int len, int start, int* g_off, int* g_st,
-                                             int* wtot) {
+                                             int* wtot, R reserve = R()) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int incl = len;
 #pragma unroll
@@ -504,7 +511,10 @@ __device__ __forceinline__ int block_flatten(int len, int start, int* g_off, int
       if (lane >= o) xi += t;
     }
     if (lane < nw) wtot[lane] = xi - x;  // exclusive warp base
-    if (lane == 31) g_off[blockDim.x] = xi;
+    if (lane == 31) {
+      g_off[blockDim.x] = xi;
+      reserve(xi);
+    }
   }
   __syncthreads();
   const int off = wtot[wid] + incl - len;
@@ -1229,6 +1239,34 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
 // live in the block's slice of a global slab instead (rare, very large S).
 // Bitmap rows use an odd word stride so lanes reading different rows at the
 // same word index spread over banks.
+// ---- triangle list. The triangle pass of block roots (|S| > 32) records
+// every triangle {u, S[a], S[b]} it finds as (a | b << 16, CSR position of
+// (S[a], S[b])) in a device pool, in per-root pieces; the diamond pass then
+// reads the list (k_diamond_list) instead of probing again. A block reserves
+// pool space for a probe/pair phase up front (an upper bound: one record per
+// probed element or pair test), returns the unused tail after the phase and
+// publishes the phase's records as one piece. Roots whose records did not fit
+// (pool or piece table exhausted, or |S| > kTriListMaxS) are flagged and keep
+// the probing diamond pass; pieces of flagged roots are ignored.
+constexpr int kTriListMaxS = 8192;              // member ids fit 16 bits, sD fits smem
+constexpr unsigned long long kTriListChunk = 1ull << 16;  // records per pool grab
+
+struct TriPiece {
+  unsigned long long start;  // first record
+  int u;                     // root
+  unsigned count;            // records
+};
+
+struct TriList {
+  uint2* rec = nullptr;                 // nullptr: no list
+  unsigned long long cap = 0;           // pool records
+  unsigned long long* top = nullptr;    // pool bump pointer
+  TriPiece* pieces = nullptr;
+  unsigned* npieces = nullptr;
+  unsigned pieces_cap = 0;
+  unsigned char* fail = nullptr;        // per root: 1 = not (fully) listed
+};
+
 struct RootsLayout {
   int s_cap, hcap, hlog, nwarps, stride_cap;
   __host__ __device__ size_t bytes_core() const {  // always in smem
@@ -1301,7 +1339,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
               unsigned char* __restrict__ slab, long long slab_stride,
               int* __restrict__ next_root, u64* __restrict__ d13, u64* __restrict__ d15,
               const unsigned long long* __restrict__ hub, const int* __restrict__ hub_base,
-              int hb, int hub_force) {
+              int hb, int hub_force, TriList tl) {
   // roots sorted by |S| (largest first), handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
@@ -1326,14 +1364,28 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
   unsigned short* mylist = lists + (size_t)wid * L.s_cap;
 
   __shared__ int s_root;
+  // triangle list state (kC3 with tl.rec): this block's pool reservation
+  // [s_tb, s_te), records of the current phase, and the root's failure flag
+  __shared__ unsigned long long s_tb, s_te;
+  __shared__ unsigned s_tc;
+  __shared__ int s_tfail;
+  if (threadIdx.x == 0) {
+    s_tb = s_te = 0;
+    s_tc = 0;
+  }
   while (true) {
     if (threadIdx.x == 0) s_root = atomicAdd(next_root, 1);
     __syncthreads();
     const int k = s_root;
     if (k >= nroots) break;
     const int u = roots[k];
+    if (kD13 && tl.rec && !tl.fail[u]) {  // listed: k_diamond_list handles it
+      __syncthreads();
+      continue;
+    }
     const int s0 = split[u];
     const int s = send[u] - s0;
+    if (kC3 && tl.rec && threadIdx.x == 0) s_tfail = s > kTriListMaxS;
     const int nw = (s + 31) >> 5;
     const int stride = nw | 1;
     int hlog = 6;
@@ -1400,12 +1452,48 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         atomicAdd(C3f + p, 1u);
         atomicAdd(sC + bi, 1u);
         ++na;
+        if (tl.rec && !s_tfail) {  // warp-aggregated append to the phase's reservation
+          const unsigned m = __activemask();
+          const int leader = __ffs(m) - 1;
+          unsigned base = 0;
+          if (lane == leader) base = atomicAdd(&s_tc, (unsigned)__popc(m));
+          base = __shfl_sync(m, base, leader);
+          const unsigned idx = base + __popc(m & ((1u << lane) - 1u));
+          tl.rec[s_tb + idx] = make_uint2((u32)a | ((u32)bi << 16), (u32)p);
+        }
       }
       if (kD13) {
         tu += (u64)__ldg(C3f + p) - 1;
         da += (u64)sC[bi] - 1;
         if (narrow) atomicAdd(reinterpret_cast<u32*>(sD + bi), ca - 1);
         else smem_add_u64(sD + bi, (u64)ca - 1);
+      }
+    };
+    // reserve room for at most `bound` records of the next phase (one thread,
+    // inside block_flatten) / publish the phase's records as a piece (after
+    // the phase's trailing barrier)
+    auto tl_reserve = [&](unsigned long long bound) {
+      if (!(kC3 && tl.rec)) return;
+      s_tc = 0;
+      if (!s_tfail && bound > 0 && s_te - s_tb < bound) {
+        const unsigned long long grab = bound > kTriListChunk ? bound : kTriListChunk;
+        const unsigned long long st = atomicAdd(tl.top, grab);
+        if (st + grab > tl.cap) {
+          s_tfail = 1;
+        } else {
+          s_tb = st;
+          s_te = st + grab;
+        }
+      }
+    };
+    auto tl_publish = [&]() {
+      if (!(kC3 && tl.rec) || threadIdx.x != 0 || s_tfail || s_tc == 0) return;
+      const unsigned pi = atomicAdd(tl.npieces, 1u);
+      if (pi < tl.pieces_cap) {
+        tl.pieces[pi] = TriPiece{s_tb, u, s_tc};
+        s_tb += s_tc;
+      } else {
+        s_tfail = 1;
       }
     };
     for (int c0 = 0; c0 + 1 < s; c0 += NT) {
@@ -1424,7 +1512,8 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         const int nqd = (!pairs && se > st) ? ((se + 3) >> 2) - qa : 0;
         f_sa[threadIdx.x] = st;
         f_sb[threadIdx.x] = se;
-        block_flatten(nqd, qa, f_off, f_st, f_wtot);
+        block_flatten(nqd, qa, f_off, f_st, f_wtot,
+                      [&](int T) { tl_reserve(4ull * (unsigned long long)T); });
       }
       {
         const int T = f_off[NT];
@@ -1470,13 +1559,15 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         }
       }
       __syncthreads();  // f_* are rewritten below
+      tl_publish();
       if (hub == nullptr) continue;
       // pair rows
       {
         f_sa[threadIdx.x] = x;
         f_sb[threadIdx.x] = st;
         f_hb[threadIdx.x] = pairs ? hub_base[x - hb] : 0;
-        block_flatten(pairs ? s - 1 - a_me : 0, 0, f_off, f_st, f_wtot);
+        block_flatten(pairs ? s - 1 - a_me : 0, 0, f_off, f_st, f_wtot,
+                      [&](int T) { tl_reserve((unsigned long long)T); });
       }
       {
         const int T = f_off[NT];
@@ -1514,8 +1605,10 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         }
       }
       __syncthreads();
+      tl_publish();
     }
     __syncthreads();
+    if (kC3 && tl.rec && threadIdx.x == 0 && s_tfail) tl.fail[u] = 1;
     if (kC3)
       for (int a = threadIdx.x; a < s; a += blockDim.x)
         if (sC[a]) atomicAdd(C3f + s0 + a, sC[a]);
@@ -1608,6 +1701,75 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     }
     __syncthreads();
   }
+}
+
+// Diamonds from the triangle list (the kD13 terms of k_roots_block, see
+// above): block per piece, per-member partial sums in shared memory.
+template <int NT>
+__global__ void __launch_bounds__(NT)
+k_diamond_list(const TriPiece* __restrict__ pieces, const unsigned* __restrict__ npieces,
+               unsigned pieces_cap, const uint2* __restrict__ rec, const int* __restrict__ rp,
+               const int* __restrict__ ci, const int* __restrict__ split,
+               const int* __restrict__ send, const u32* __restrict__ C3f,
+               const unsigned char* __restrict__ fail, int* __restrict__ next,
+               u64* __restrict__ d13) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  u64* sD = reinterpret_cast<u64*>(smem_raw);
+  __shared__ u64 red[32];
+  __shared__ int s_item;
+  const unsigned np = min(*npieces, pieces_cap);
+  while (true) {
+    if (threadIdx.x == 0) s_item = atomicAdd(next, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= (int)np) break;
+    const TriPiece pc = pieces[it];
+    const int u = pc.u;
+    if (fail[u]) {
+      __syncthreads();
+      continue;
+    }
+    const int s0 = split[u];
+    const int s = send[u] - s0;
+    for (int a = threadIdx.x; a < s; a += NT) sD[a] = 0;
+    __syncthreads();
+    const bool narrow = (u64)s * (u64)(rp[u + 1] - rp[u]) < (1ull << 32);
+    u64 tu = 0;
+    const uint2* r = rec + pc.start;
+    for (unsigned i = threadIdx.x; i < pc.count; i += NT) {
+      const uint2 x = r[i];
+      const int a = (int)(x.x & 0xffffu), b = (int)(x.x >> 16);
+      const u32 ca = __ldg(C3f + s0 + a), cb = __ldg(C3f + s0 + b), cp = __ldg(C3f + x.y);
+      tu += (u64)cp - 1;
+      if (narrow) {
+        atomicAdd(reinterpret_cast<u32*>(sD + a), cb - 1);
+        atomicAdd(reinterpret_cast<u32*>(sD + b), ca - 1);
+      } else {
+        smem_add_u64(sD + a, (u64)cb - 1);
+        smem_add_u64(sD + b, (u64)ca - 1);
+      }
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < s; a += NT)
+      if (sD[a]) atomicAdd(d13 + ci[s0 + a], sD[a]);
+    tu = block_sum_u64(tu, red);
+    if (threadIdx.x == 0 && tu) atomicAdd(d13 + u, tu);
+    __syncthreads();
+  }
+}
+
+// Sum over roots u in [u0, u1) with 32 < |N+(u)| <= kTriListMaxS of
+// C(|N+(u)|, 2): an upper bound of the records the triangle list can take.
+__global__ void k_trilist_bound(const int* __restrict__ split, const int* __restrict__ send,
+                                int u0, int u1, unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1; u += gridDim.x * blockDim.x) {
+    const unsigned long long s = (unsigned long long)(send[u] - split[u]);
+    if (s > 32 && s <= (unsigned long long)kTriListMaxS) acc += s * (s - 1) / 2;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
 // =============================================================== epilogue

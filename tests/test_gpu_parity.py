@@ -252,6 +252,23 @@ def test_hub_rows_paths(hub, rbin):
     c.close()
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("rbin", [0, 2, 5])
+def test_triangle_list_paths(mode, rbin):
+    """Diamonds from the triangle list (auto), without it (1), and with a pool
+    so small that most roots fall back to the probing pass mid-list (2) give
+    the same bits, in every block bin and with hub-row pair checks forced."""
+    c = _capi.Context(0)
+    c.set_debug(_capi.DEBUG_TRILIST, mode)
+    c.set_debug(_capi.DEBUG_ROOTS_BIN, rbin)
+    c.set_debug(_capi.DEBUG_HUB, 2)
+    cases = [gu.er(300, 0.15, 11), gu.complete(48), graphs.rmat(12, 16, seed=6),
+             graphs.sbm(64, 64, 0.3, 3.0, 4), gu.star(90), gu.demo()]
+    for rp, ci in cases:
+        check_same(c, rp, ci, d15_mode=1)
+    c.close()
+
+
 def test_repeat_determinism_at_scale():
     """Bit-identical results across repeated runs at a size where every
     root bin and 4-cycle class is populated (guards against lost updates;
