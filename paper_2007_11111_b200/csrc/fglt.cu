@@ -219,6 +219,7 @@ struct fglt_ctx {
   // 2 a tiny pool (test hook: most roots fall back to the probing pass)
   int tl_mode = 0;
   TriList tl;
+  int64_t tl_u0 = -1, tl_u1 = -1;  // root range the list was built for
   // hub rows (k_hub_rows): built once per graph by the first root pass
   bool hub_built = false;
   bool big_rows_listed = false;  // list_big_rows
@@ -770,6 +771,8 @@ void triangles(fglt_ctx* c, int64_t u0, int64_t u1) {
   if (P.c3) CK(cudaMemsetAsync(c->C3f, 0, (size_t)std::max<int64_t>(c->nnz, 1) * 4, c->stream));
   root_bins(c, u0, u1);
   setup_trilist(c, u0, u1);
+  c->tl_u0 = u0;
+  c->tl_u1 = u1;
   if (P.c3 && P.d15) roots_pass<true, false, true>(c);
   else if (P.c3) roots_pass<true, false, false>(c);
   else roots_pass<false, false, true>(c);
@@ -894,6 +897,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   if (P.d13) {
     root_bins(c, u0, u1);
     c->mark("roots:start");
+    if (c->tl_u0 != u0 || c->tl_u1 != u1) c->tl = TriList{};  // list of another range
     diamond_list(c);
     roots_pass<false, true, false>(c);
     c->mark("roots:end");

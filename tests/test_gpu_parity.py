@@ -402,3 +402,64 @@ def test_bench_two_ranks_gloo():
     assert len(lines) == 1, out.stdout
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["value"] > 0 and rec["e2e"]["value"] > 0
+
+
+def test_config4_full_size_properties():
+    """BASELINE.json config 4 (R-MAT scale 23, 129M edges) at full size. The
+    oracle's full transform is out of reach here (its reference-algorithm
+    4-cycle and diamond passes are O(W) random accesses, W = 1.34e12), so:
+    (1) the O(nnz) sub-dictionary {0,1,2,3,7,8} raw AND net against the
+    oracle, bit for bit; (2) the full Sigma16 tables are byte-identical to the
+    staged 8-rank decomposition (different root partition, list pools and
+    schedules); (3) raw = U net exactly for every vertex (the conversion leg);
+    (4) degree-sum identities of columns 1 and 3."""
+    import torch
+    from paper_2007_11111_b200.dist import CudaStages
+    name, rp, ci = graphs.config(4)
+    n, nnz = len(rp) - 1, len(ci)
+    cheap = _capi.dict_mask([2, 3, 7, 8])
+    ctx = _capi.Context(0)
+    raw_c, net_c, _ = ctx.transform_host(rp, ci, cheap)
+    oraw, onet = ob.transform(rp, ci, cheap, False, 0)
+    assert np.array_equal(raw_c, oraw) and np.array_equal(net_c, onet), name
+    raw, net, _ = ctx.transform_host(rp, ci)
+    ctx.close()  # its workspace (triangle-list pool included) goes back before (2)
+    assert np.array_equal(raw[:, [0, 1, 2, 3, 7, 8]], oraw)
+    assert int(raw[:, 1].sum()) == nnz
+    deg = np.diff(rp).astype(np.uint64)
+    assert np.array_equal(raw[:, 3], deg * (deg - 1) // 2)
+    # (3) raw = U net, exact in uint64 (no wrap: every term is <= raw)
+    U = ob.u16()
+    back = net.copy()
+    for r in range(16):
+        for c in range(r + 1, 16):
+            if U[r, c]:
+                back[:, r] += U[r, c] * net[:, c]
+    assert np.array_equal(back, raw)
+    assert (net <= raw).all()
+    # (2) staged 8-rank decomposition on one device, byte identical
+    dev = torch.device("cuda", 0)
+    rp_d, ci_d = torch.from_numpy(rp).to(dev), torch.from_numpy(ci).to(dev)
+    world = 8
+    st = CudaStages(dev)
+    st.prepare(rp_d, ci_d, n, nnz, 0xFFFF, False)
+    b = st.bounds(world)
+    c3 = view = None
+    for r in range(world):
+        view = st.triangles(int(b[r]), int(b[r + 1]))  # aliases the context's edge counts
+        c3 = view.clone() if c3 is None else c3 + view
+    view.copy_(c3)
+    st.local()
+    vec = None
+    for r in range(world):
+        view = st.roots(int(b[r]), int(b[r + 1]))  # aliases the context's vectors
+        vec = view.clone() if vec is None else vec + view
+        view.zero_()
+    view.copy_(vec)
+    del c3, vec, rp_d, ci_d
+    raw_d = torch.empty((n, 16), dtype=torch.int64, device=dev)
+    net_d = torch.empty((n, 16), dtype=torch.int64, device=dev)
+    rc, err = st.epilogue(0, n, raw_d, net_d)
+    assert rc == 0, err
+    assert np.array_equal(raw_d.cpu().numpy().view(np.uint64), raw)
+    assert np.array_equal(net_d.cpu().numpy().view(np.uint64), net)
