@@ -192,7 +192,7 @@ uint64_t fglt_ctx_kernel_launches(const fglt_ctx* ctx);
 /* Test hooks: force one internal code path for every root so small graphs
  * exercise paths that otherwise only large graphs reach. Results must be
  * identical for any setting (the parity tests check exactly that). */
-#define FGLT_DEBUG_C4_CLASS 1  /* 0 auto, 2 hash passes, 3 packed tiles, 4 tiles */
+#define FGLT_DEBUG_C4_CLASS 1  /* 0 auto, 2 hash passes, 3 packed tiles, 4 tiles, 5 small packed tiles */
 #define FGLT_DEBUG_C4_PARTS 2  /* hash passes per root when class 2 is forced  */
 #define FGLT_DEBUG_ROOTS_BIN 3 /* 0 auto, 1..4 smem bitmap bins, 5 global slab */
 #define FGLT_DEBUG_HUB 4       /* 0 auto, 1 no hub rows, 2 hub rows for every hub member */

@@ -65,7 +65,7 @@ enum Buf {
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
   B_CUB, B_CURSOR, B_TBND, B_BIGROWS, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV,
-  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_TB, B_TLREC, B_TLPIECES, B_TLFAIL,
+  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_TB, B_TLREC, B_TLPIECES, B_TLFAIL, B_TBS, B_TBNDS, B_CURSORS,
   B_COUNT
 };
 
@@ -805,8 +805,8 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         c->force_c4_class, c->force_c4_parts);
     check_launch();
     c->launched();
-    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5}, lists, &stride);
-    for (int bb = 3; bb <= 5; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc);
+    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6}, lists, &stride);
+    for (int bb = 3; bb <= 6; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc);
     int* queues = reinterpret_cast<int*>(c->d_small + 56);  // dynamic root queues
     CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
     c->mark("four-cycle rows:start");
@@ -849,12 +849,12 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       check_launch();
       c->launched();
     }
-    int* bnd = nullptr;  // absolute tile boundaries of the active rows
-    int* tb = nullptr;   // banded tile starts (dense_span), tb[K] = nact
+    // classes 5/6 (big tiles) and 7 (small tiles): banded tile starts
+    // (dense_span) and the absolute tile boundaries of the active rows
     const long long nact = (long long)c->nact;
-    if (cnt[4] > 0 || cnt[5] > 0) {
+    auto tiles_for = [&](long long tile_bytes, Buf tb_buf, Buf bnd_buf, int** bnd_out) -> int* {
       std::vector<int> h{0};
-      const long long t4 = 2ll * kC4TileBytes, t8 = kC4TileBytes, t32 = kC4Tile32;
+      const long long t4 = 2 * tile_bytes, t8 = tile_bytes, t32 = tile_bytes / 4;
       for (long long x = 0; x < nact;) {
         const long long e = x < bands[0] ? std::min<long long>(x + t4, bands[0])
                           : x < bands[1] ? std::min<long long>(x + t8, bands[1])
@@ -863,32 +863,51 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         x = e;
       }
       const long long K = (long long)h.size() - 1;
-      tb = c->ensure<int>(B_TB, h.size());
+      int* tb = c->ensure<int>(tb_buf, h.size());
       CK(cudaMemcpyAsync(tb, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      *bnd_out = nullptr;
       if (K * nact <= (1ll << 30)) {
-        bnd = c->ensure<int>(B_TBND, (size_t)(K * nact));
+        *bnd_out = c->ensure<int>(bnd_buf, (size_t)(K * nact));
         k_tile_bounds<<<c->grid(K * nact, 256), 256, 0, c->stream>>>(c->rp, c->ci, (int)nact,
-                                                                      (int)K, tb, bnd);
+                                                                      (int)K, tb, *bnd_out);
+        check_launch();
+        c->launched();
+      }
+      return tb;
+    };
+    if (cnt[4] > 0 || cnt[5] > 0) {
+      int* bnd = nullptr;
+      int* tb = tiles_for(kC4TileBytes, B_TB, B_TBND, &bnd);
+      for (int bb = 4; bb <= 5; ++bb) {
+        if (cnt[bb] == 0) continue;
+        const size_t sm = kC4TileBytes;
+        const int g = std::min(cnt[bb], c->sms * (1024 / kC4DenseThreads));
+        int* cur = c->ensure<int>(B_CURSOR, 2 * (size_t)g * (size_t)(c->dmax + 1));
+        if (bb == 4) {
+          set_smem(k_c4_dense<true, kC4DenseThreads>, sm);
+          k_c4_dense<true, kC4DenseThreads><<<g, kC4DenseThreads, sm, c->stream>>>(
+              c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
+              bnd, nact, tb, bands[0], bands[1], queues + 2, c4);
+        } else {
+          set_smem(k_c4_dense<false, kC4DenseThreads>, sm);
+          k_c4_dense<false, kC4DenseThreads><<<g, kC4DenseThreads, sm, c->stream>>>(
+              c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
+              bnd, nact, tb, bands[0], bands[1], queues + 3, c4);
+        }
         check_launch();
         c->launched();
       }
     }
-    for (int bb = 4; bb <= 5; ++bb) {  // classes 5/6: dense tiles
-      if (cnt[bb] == 0) continue;
-      const size_t sm = kC4TileBytes;
-      const int g = std::min(cnt[bb], c->sms * (1024 / kC4DenseThreads));
-      int* cur = c->ensure<int>(B_CURSOR, 2 * (size_t)g * (size_t)(c->dmax + 1));
-      if (bb == 4) {
-        set_smem(k_c4_dense<true>, sm);
-        k_c4_dense<true><<<g, kC4DenseThreads, sm, c->stream>>>(
-            c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
-            bnd, nact, tb, bands[0], bands[1], queues + 2, c4);
-      } else {
-        set_smem(k_c4_dense<false>, sm);
-        k_c4_dense<false><<<g, kC4DenseThreads, sm, c->stream>>>(
-            c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
-            bnd, nact, tb, bands[0], bands[1], queues + 3, c4);
-      }
+    if (cnt[6] > 0) {
+      int* bnd = nullptr;
+      int* tb = tiles_for(kC4TileBytesS, B_TBS, B_TBNDS, &bnd);
+      const size_t sm = kC4TileBytesS;
+      const int g = std::min(cnt[6], c->sms * (1024 / kC4DenseThreadsS));
+      int* cur = c->ensure<int>(B_CURSORS, 2 * (size_t)g * (size_t)(c->dmax + 1));
+      set_smem(k_c4_dense<true, kC4DenseThreadsS>, sm);
+      k_c4_dense<true, kC4DenseThreadsS><<<g, kC4DenseThreadsS, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->mir, lists[6], cnt[6], cur, (long long)(c->dmax + 1), bnd,
+          nact, tb, bands[0], bands[1], queues + 5, c4);
       check_launch();
       c->launched();
     }

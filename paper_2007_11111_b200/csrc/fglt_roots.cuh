@@ -281,8 +281,23 @@ constexpr u64 kC4HashFill = 3ull << (kC4HashLog - 2);  // distinct targets per p
 #define FGLT_DENSE_THREADS 1024
 #define FGLT_DENSE_TILE_BYTES 196608
 #endif
-constexpr int kC4DenseThreads = FGLT_DENSE_THREADS;     // one dense block per SM by default
-constexpr int kC4TileBytes = FGLT_DENSE_TILE_BYTES;     // counter tile per block (192 KB)
+// Two dense configurations, chosen per root by the cost model: big tiles
+// (one 1024-thread block per SM, 192 KB) for roots whose rows pay a per-tile
+// setup (large |N-(u)| x tiles), small tiles (two 512-thread blocks per SM,
+// 96 KB each, so one block's tile barriers overlap the other's work) else.
+constexpr int kC4DenseThreads = FGLT_DENSE_THREADS;     // big: one block per SM
+constexpr int kC4TileBytes = FGLT_DENSE_TILE_BYTES;     // big: counter tile (192 KB)
+constexpr int kC4DenseThreadsS = 512;                   // small: two blocks per SM
+constexpr int kC4TileBytesS = 98304;                    // small: 96 KB tiles
+#ifndef FGLT_ROW_TILE
+#define FGLT_ROW_TILE 1  // cost of one row's segment setup per tile, in wedges
+#endif
+#ifndef FGLT_SMALL_MAX_TILES
+#define FGLT_SMALL_MAX_TILES 8
+#endif
+#ifndef FGLT_SMALL_EFF
+#define FGLT_SMALL_EFF 85  // small-tile cost, percent of the modelled (better latency hiding)
+#endif
 constexpr int kC4Tile16 = kC4TileBytes / 2; // ids per packed tile
 constexpr int kC4Tile32 = kC4TileBytes / 4; // ids per 32-bit tile
 constexpr int kC4Long = 48;                 // rows at least this long: flattened batches
@@ -300,12 +315,12 @@ constexpr int kC4BlockThreads = FGLT_C4B_THREADS;  // class-4 block (one 128 KB 
 // when |N-(u)| >= 65536). Tiles never straddle a band: kC4TileBytes hold
 // 2 x kC4TileBytes ids in the 4-bit band, kC4TileBytes in the 8-bit band and
 // kC4Tile32 above (dense_tiles() builds the same boundaries on the host).
-__host__ __device__ inline void dense_span(u64 u, u64 b4, u64 b8, bool pack, u64* tiles,
-                                           u64* bytes) {
+__host__ __device__ inline void dense_span(u64 u, u64 b4, u64 b8, bool pack, u64 tile_bytes,
+                                           u64* tiles, u64* bytes) {
   const u64 nib = u < b4 ? u : b4;
   const u64 byt = u > b4 ? (u < b8 ? u : b8) - b4 : 0;
   const u64 rest = u > b8 ? u - b8 : 0;
-  const u64 t4 = 2 * (u64)kC4TileBytes, t8 = kC4TileBytes, t32 = kC4Tile32;
+  const u64 t4 = 2 * tile_bytes, t8 = tile_bytes, t32 = tile_bytes / 4;
   *tiles = (nib + t4 - 1) / t4 + (byt + t8 - 1) / t8 + (rest + t32 - 1) / t32;
   *bytes = (nib + 1) / 2 + byt + rest * (pack ? 2 : 4);
 }
@@ -331,17 +346,29 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       P = (w + kC4HashFill - 1) / kC4HashFill;
       const u64 cost_hash = FGLT_HASH_WEIGHT * (P * (w + (1ull << kC4HashLog)) + w);
       const bool pack = nq < 65536;
-      u64 tiles, bytes;
-      dense_span((u64)u, (u64)b4, (u64)b8, pack, &tiles, &bytes);
-      const u64 cost_dense = bytes / 8 + tiles * (FGLT_TILE_FIXED + nq) + 2 * w;
-      if (cost_hash <= cost_dense) c = 4;
-      else c = pack ? 5 : 6;
+      u64 tiles, bytes, tiles_s, bytes_s;
+      dense_span((u64)u, (u64)b4, (u64)b8, pack, kC4TileBytes, &tiles, &bytes);
+      dense_span((u64)u, (u64)b4, (u64)b8, pack, kC4TileBytesS, &tiles_s, &bytes_s);
+      const u64 cost_dense = bytes / 8 + tiles * (FGLT_TILE_FIXED + FGLT_ROW_TILE * nq) + 2 * w;
+      // small tiles only for roots that need few of them: with many tiles per
+      // root the per-tile row setup and tail imbalance outweigh the overlap
+      // (measured: R-MAT 20, <= 6 tiles, small wins 15%; R-MAT 23, up to 34
+      // tiles, small loses 17%)
+      const u64 cost_small =
+          tiles_s > FGLT_SMALL_MAX_TILES
+              ? ~0ull
+              : (bytes_s / 8 + tiles_s * (FGLT_TILE_FIXED / 2 + FGLT_ROW_TILE * nq) + 2 * w) *
+                    FGLT_SMALL_EFF / 100;
+      if (cost_hash <= cost_dense && (!pack || cost_hash <= cost_small)) c = 4;
+      else if (!pack) c = 6;
+      else c = cost_small < cost_dense ? 7 : 5;
     }
     if (force_cls > 0 && w > 0) {  // test hook: route every root to one path
       const u64 nq = (u64)(split[u] - rp[u]);
-      // external numbering: 2 hash passes, 3 packed tiles, 4 32-bit tiles
-      c = (u64)force_cls + 2;
-      if (c == 5 && nq >= 65536) c = 6;
+      // external numbering: 2 hash passes, 3 packed tiles, 4 32-bit tiles,
+      // 5 small packed tiles
+      c = force_cls == 5 ? 7 : (u64)force_cls + 2;
+      if ((c == 5 || c == 7) && nq >= 65536) c = 6;
       if (c == 4) {
         P = (w + kC4HashFill - 1) / kC4HashFill;
         if (force_parts > 0) P = (u64)force_parts;
@@ -719,8 +746,8 @@ __device__ unsigned int g_dense_done;
 #define DPROF_MARK(k) do {} while (0)
 #endif
 
-template <bool PACK>
-__global__ void __launch_bounds__(kC4DenseThreads, 1024 / kC4DenseThreads)
+template <bool PACK, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT)
 k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, int* __restrict__ cursor,
@@ -730,7 +757,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   // roots are sorted by work (largest first) and handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
-  constexpr int NW = kC4DenseThreads / 32;
+  constexpr int NW = NT / 32;
   __shared__ u64 rsum[NW][32];
   __shared__ int bst_all[NW][32];
   __shared__ int boff_all[NW][33];

@@ -215,6 +215,7 @@ FORCED = [
     ("c4 hash P=3", _capi.DEBUG_C4_CLASS, 2, 3),
     ("c4 packed tiles", _capi.DEBUG_C4_CLASS, 3, 0),
     ("c4 32-bit tiles", _capi.DEBUG_C4_CLASS, 4, 0),
+    ("c4 small packed tiles", _capi.DEBUG_C4_CLASS, 5, 0),
     ("roots bin 1", _capi.DEBUG_ROOTS_BIN, 1, 0),
     ("roots bin 2", _capi.DEBUG_ROOTS_BIN, 2, 0),
     ("roots bin 4", _capi.DEBUG_ROOTS_BIN, 4, 0),
