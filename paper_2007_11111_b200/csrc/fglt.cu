@@ -805,7 +805,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         c->force_c4_class, c->force_c4_parts);
     check_launch();
     c->launched();
-    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6}, lists, &stride);
+    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6, 7}, lists, &stride);
     for (int bb = 3; bb <= 6; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc);
     int* queues = reinterpret_cast<int*>(c->d_small + 56);  // dynamic root queues
     CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
@@ -821,17 +821,32 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     }
     if (cnt[1] > 0) {  // class 2: 128-thread block-flattened tables of <= 2048 slots
       const size_t sm = (size_t)(1 << kWarpHashLog2) * 8;
-      const int g = std::min(cnt[1], c->sms * 10);
       set_smem(k_c4_block<128>, sm);
+      int occ = 1;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<128>, 128, sm));
+      const int g = std::min(cnt[1], c->sms * std::max(occ, 1));
       k_c4_block<128><<<g, 128, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[1], cnt[1],
                                                 wc, parts, kWarpHashLog2, queues + 4, c4);
       check_launch();
       c->launched();
     }
+    if (cnt[7] > 0) {  // class 8: 128-thread block-flattened tables of <= 1024 slots
+      const size_t sm = (size_t)(1 << (kWarpHashLog2 - 1)) * 8;
+      set_smem(k_c4_block<128>, (size_t)(1 << kWarpHashLog2) * 8);
+      int occ = 1;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<128>, 128, sm));
+      const int g = std::min(cnt[7], c->sms * std::max(occ, 1));
+      k_c4_block<128><<<g, 128, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[7], cnt[7],
+                                                wc, parts, kWarpHashLog2 - 1, queues + 6, c4);
+      check_launch();
+      c->launched();
+    }
     if (cnt[2] > 0) {  // class 3: 256-thread block-flattened tables of <= 4096 slots
       const size_t sm = (size_t)(1 << kC4SmallLog) * 8;
-      const int g = std::min(cnt[2], c->sms * 6);
       set_smem(k_c4_block<256>, sm);
+      int occ = 1;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<256>, 256, sm));
+      const int g = std::min(cnt[2], c->sms * std::max(occ, 1));
       k_c4_block<256><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[2], cnt[2],
                                                 wc, parts, kC4SmallLog, queues + 0, c4);
       check_launch();

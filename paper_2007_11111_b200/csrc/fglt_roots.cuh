@@ -258,7 +258,8 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 
 // Cost-model classes for roots with wc(u) > 0 (k_c4_class):
 //   1 warp table, 512 slots              wc <= 256
-//   2 warp table, 2048 slots             wc <= 1024
+//   8 small block table (128 threads, 1024 slots), wc <= 512
+//   2 small block table (128 threads, 2048 slots), wc <= 1024
 //   3 small block table (128 threads, <= 4096 slots), wc <= 2048
 //   4 block table, P hash-partition passes over the wedges, P = ceil(wc/12288)
 //   5 dense tiles, 16-bit packed counters (|N-(u)| < 65536), 96K ids per tile
@@ -337,6 +338,8 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       c = 0;
     } else if (w <= 256) {
       c = 1;
+    } else if (w <= 512) {
+      c = 8;  // 128-thread block, 1024-slot table (twice the blocks per SM of class 2)
     } else if (w <= 1024) {
       c = 2;
     } else if (w <= 2048) {
