@@ -1421,11 +1421,31 @@ int fglt_stage_prepare(fglt_ctx* c, const int32_t* d_row_ptr, const int32_t* d_c
 }
 
 // Contiguous root blocks of (nearly) equal exact work: per root u,
-// work(u) = wedges(u) + triangle probes(u) + |N+(u)| + 1.
+// work(u) = wedges(u) + triangle probes(u) + 1, prefix-summed on the device;
+// rank r's block starts at the first root whose inclusive prefix reaches
+// total * r / world.
 __global__ void k_work_total(const u64* __restrict__ wc, const u64* __restrict__ tw, int n,
                              u64* __restrict__ out) {
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x)
     out[u] = wc[u] + tw[u] + 1;
+}
+
+__global__ void k_cut_bounds(const u64* __restrict__ pre, int n, int world,
+                             long long* __restrict__ bounds) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r > world) return;
+  if (r == 0 || r == world) {
+    bounds[r] = r == 0 ? 0 : n;
+    return;
+  }
+  const u64 total = pre[n - 1];
+  const u64 target = (u64)(((unsigned __int128)total * (unsigned)r) / (unsigned)world);
+  int lo = 0, hi = n;  // first u with pre[u] >= target; the block starts after it
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (pre[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  bounds[r] = lo < n ? lo + 1 : n;
 }
 
 int fglt_stage_bounds(fglt_ctx* c, int world, int64_t* bounds, fglt_error* err) {
@@ -1439,23 +1459,25 @@ int fglt_stage_bounds(fglt_ctx* c, int world, int64_t* bounds, fglt_error* err) 
       for (int r = 1; r < world; ++r) bounds[r] = n * r / world;
       return FGLT_OK;
     }
-    u64* work = c->ensure<u64>(B_WORK, 2 * (size_t)n);
+    u64* work = c->ensure<u64>(B_WORK, 3 * (size_t)n);
     const int G = group_for((double)c->nnz / (double)n);
     DISPATCH_G(G, launch_root_work, c, work);
     DISPATCH_G(G, launch_probe_work, c, work + n);
-    std::vector<u64> wc(n), tw(n);
-    CK(cudaMemcpyAsync(wc.data(), work, n * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(tw.data(), work + n, n * 8, cudaMemcpyDeviceToHost, c->stream));
+    k_work_total<<<c->grid(n, 256), 256, 0, c->stream>>>(work, work + n, (int)n, work + 2 * n);
+    check_launch();
+    c->launched();
+    size_t tb = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb, work + 2 * n, work, (int)n, c->stream));
+    void* tmp = c->ensure<unsigned char>(B_CUB, tb);
+    CK(cub::DeviceScan::InclusiveSum(tmp, tb, work + 2 * n, work, (int)n, c->stream));
+    c->launched();
+    long long* d_b = c->ensure<long long>(B_API0, (size_t)world + 1);
+    k_cut_bounds<<<(world + 128) / 128, 128, 0, c->stream>>>(work, (int)n, world, d_b);
+    check_launch();
+    c->launched();
+    CK(cudaMemcpyAsync(bounds, d_b, ((size_t)world + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    long double total = 0;
-    for (int64_t u = 0; u < n; ++u) total += (long double)(wc[u] + tw[u] + 1);
-    long double acc = 0;
-    int r = 1;
-    for (int64_t u = 0; u < n && r < world; ++u) {
-      acc += (long double)(wc[u] + tw[u] + 1);
-      while (r < world && acc >= total * r / world) bounds[r++] = u + 1;
-    }
-    while (r < world) bounds[r++] = n;
+    for (int r = 1; r <= world; ++r) bounds[r] = std::max(bounds[r], bounds[r - 1]);
     return FGLT_OK;
   } catch (const CudaFail& f) {
     set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
