@@ -100,14 +100,31 @@ def load_graph(cfg: int):
     return name, rp, ci
 
 
-def ncu_traffic(cfg: int):
-    """Per-step DRAM bytes from the committed ncu summary, if one matches."""
+def ncu_summary(cfg: int):
+    """The committed ncu launch-list summary for this config, if any."""
     p = os.path.join(ROOT, "profiles", f"ncu_config{cfg}_summary.json")
     if not os.path.exists(p):
-        return None, None
+        return None
     with open(p) as f:
-        d = json.load(f)
-    return d.get("dram_bytes_per_step"), d.get("source")
+        return json.load(f)
+
+
+def dominant_kernel(summary, step_ms: float, peak_gbs: float):
+    """The top kernel of the ncu launch list: its share of the step (ncu's
+    per-launch times are cold-cache and serialised, so the share, not the
+    absolute, carries over), its DRAM bytes per step and the DRAM bandwidth
+    that implies at the live step time — the honest HBM fraction of a kernel
+    whose bound is on-chip (shared-memory atomics, L2 gathers), not HBM."""
+    if not summary or not summary.get("kernels"):
+        return None
+    k = summary["kernels"][0]
+    ms = k["share"] * step_ms
+    dram = k["dram_read"] + k["dram_write"]
+    gbs = dram / (ms * 1e-3) / 1e9 if ms > 0 else None
+    return {"name": k["name"], "share_of_step": k["share"], "ms_at_live_step": ms,
+            "dram_bytes_per_step": dram, "dram_gbs": gbs,
+            "dram_frac_of_peak": gbs / peak_gbs if gbs else None,
+            "bound": "shared-memory atomics + L2 gathers + tile barriers (see profiles/)"}
 
 
 # ----------------------------------------------------------------- reference
@@ -328,7 +345,9 @@ def main():
     peak, peak_kind = peaks()
     achieved = balg / (t_ms * 1e-3) / 1e9 / world
     dom = max(phases.items(), key=lambda kv: kv[1]) if phases else (None, None)
-    traffic, traffic_src = ncu_traffic(args.config)
+    summ = ncu_summary(args.config)
+    traffic = summ.get("dram_bytes_per_step") if summ else None
+    traffic_src = summ.get("source") if summ else None
 
     # device ingest: raw edge sample -> sanitised CSR
     ingest = None
@@ -375,6 +394,8 @@ def main():
                      "peak_kind": peak_kind, "traffic_source": traffic_src,
                      "dominant_phase": {"name": dom[0], "ms": dom[1],
                                         "share": dom[1] / t_ms if dom[1] else None},
+                     "dominant_kernel": dominant_kernel(summ, t_ms, peak),
+                     "measured_dram_gbs": (traffic / (t_ms * 1e-3) / 1e9) if traffic else None,
                      "phases_ms": phases},
         "cpu_baseline": cpu,
         "ingest": ingest,
