@@ -949,13 +949,22 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
             u32 x = xs[j];
             if ((x & ge2) == 0) continue;
             const int base = lo + ((4 * i4 + j) << sh);
-            for (int q = 0; q < per; ++q, x = bits < 32 ? x >> bits : 0) {
-              const u32 l = x & vmask;
-              if (l >= 2) {
-                const u64 c = (u64)l * (l - 1) / 2;
-                acc += c;
-                atomicAdd(c4 + base + q, c);
-              }
+            // one flag bit at the low end of every counter >= 2, visited by ffs
+            u32 f = sh == 0 ? 1u : 0u;
+            if (sh) {
+              u32 hi = x & ge2;  // bits above each counter's lowest
+#pragma unroll
+              for (int t = 1; t < 16; t <<= 1)
+                if (t < bits) hi |= hi >> t;
+              f = hi & (ge2 >> 1) & ~(ge2 >> 1 & ge2);  // keep each counter's low bit
+            }
+            while (f) {
+              const int b = __ffs(f) - 1;
+              f &= f - 1;
+              const u32 l = (x >> b) & vmask;
+              const u64 c = (u64)l * (l - 1) / 2;
+              acc += c;
+              atomicAdd(c4 + base + (b >> (5 - sh)), c);
             }
           }
         }
