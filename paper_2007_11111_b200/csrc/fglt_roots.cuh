@@ -1366,6 +1366,9 @@ __global__ void k_hub_rows(const int* __restrict__ ci, const int* __restrict__ s
   }
 }
 
+#ifndef FGLT_K4_THREAD_NW
+#define FGLT_K4_THREAD_NW 8  // G[S] rows of at most this many words: thread-per-member 4-cliques
+#endif
 constexpr int kRootsThreads = 256;  // block threads for |S| > 256 (smaller bins: 64, 128)
 constexpr int kPairsInFlight = 4;  // hub-row words in flight per lane
 
@@ -1662,6 +1665,35 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
       // number of G[S]-triangles on it and is credited to both ends, so
       // sK[a] = sum_{b in row a} c_ab = 2 t_a (t_a = G[S]-triangles through a).
       u32* sK = reinterpret_cast<u32*>(sD);
+      if (nw <= FGLT_K4_THREAD_NW) {
+        // small S: thread per member, its row in registers; each G[S] edge
+        // (a, b > a) popcounted once and credited to both ends
+        for (int a = threadIdx.x; a + 1 < s; a += NT) {
+          const u32* ra = bm + (long long)a * stride;
+          u32 r[FGLT_K4_THREAD_NW];
+#pragma unroll
+          for (int t = 0; t < FGLT_K4_THREAD_NW; ++t) r[t] = t < nw ? ra[t] : 0u;
+          const int j0 = (a + 1) >> 5;
+          u32 acc = 0;
+          for (int j = j0; j < nw; ++j) {
+            u32 w = ra[j] & (j == j0 ? ~0u << ((a + 1) & 31) : ~0u);
+            while (w) {
+              const int bb = (j << 5) + __ffs(w) - 1;
+              w &= w - 1;
+              const u32* rb = bm + (long long)bb * stride;
+              u32 c = 0;
+#pragma unroll
+              for (int t = 0; t < FGLT_K4_THREAD_NW; ++t)
+                if (t < nw) c += __popc(r[t] & rb[t]);
+              if (c) {
+                acc += c;
+                atomicAdd(sK + bb, c);
+              }
+            }
+          }
+          if (acc) atomicAdd(sK + a, acc);
+        }
+      } else
       while (true) {
         int a = 0;
         if (lane == 0) a = atomicAdd(next_item + 1, 1);
