@@ -65,7 +65,7 @@ enum Buf {
   B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
   B_CUB, B_CURSOR, B_TBND, B_BIGROWS, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV,
-  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_TB, B_TLREC, B_TLPIECES, B_TLFAIL, B_TBS, B_TBNDS, B_CURSORS,
+  B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_TB, B_TLREC, B_TLPIECES, B_TLFAIL, B_TBS, B_TBNDS, B_CURSORS, B_TLCHUNKS,
   B_COUNT
 };
 
@@ -663,7 +663,7 @@ void roots_pass(fglt_ctx* c) {
     const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
     k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(
         c->rp, c->ci, c->split, c->send, c->C3f, lists[0], cnt[0], d13, d15, c->hub, c->hub_base,
-        c->hub_hb, c->force_hub == 2);
+        c->hub_hb, c->force_hub == 2, c->tl);
     check_launch();
     c->launched();
   }
@@ -743,6 +743,10 @@ void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
   t.pieces = c->ensure<TriPiece>(B_TLPIECES, t.pieces_cap);
   t.fail = c->ensure<unsigned char>(B_TLFAIL, (size_t)c->n);
   CK(cudaMemsetAsync(t.fail, 0, (size_t)c->n, c->stream));
+  t.chunks_cap = (unsigned)std::min<unsigned long long>(cap / kTriListWarpChunk + blocks * 8 + 1024,
+                                                        1ull << 31);
+  t.chunks = c->ensure<TriChunk>(B_TLCHUNKS, t.chunks_cap);
+  t.nchunks = reinterpret_cast<unsigned*>(d_bound + 3);
   c->tl = t;
 }
 
@@ -754,11 +758,16 @@ void diamond_list(fglt_ctx* c) {
   set_smem(k_diamond_list<NT>, sm);
   int occ = 1;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_diamond_list<NT>, NT, sm));
-  int* next = reinterpret_cast<int*>(c->d_small + 27);
+  int* next = reinterpret_cast<int*>(c->d_small + 28);
   CK(cudaMemsetAsync(next, 0, sizeof(int), c->stream));
   k_diamond_list<NT><<<c->sms * std::max(occ, 1), NT, sm, c->stream>>>(
       c->tl.pieces, c->tl.npieces, c->tl.pieces_cap, c->tl.rec, c->rp, c->ci, c->split, c->send,
       c->C3f, c->tl.fail, next, c->V(V_D13));
+  check_launch();
+  c->launched();
+  k_diamond_wlist<<<c->sms * 8, 256, 0, c->stream>>>(c->tl.chunks, c->tl.nchunks,
+                                                     c->tl.chunks_cap, c->tl.rec, c->rp, c->ci,
+                                                     c->split, c->send, c->C3f, c->V(V_D13));
   check_launch();
   c->launched();
 }

@@ -1101,8 +1101,51 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
 // d15[S[a]] += t_a and d15[u] += sum_a t_a / 3 (reference compute_d15,
 // kernels.cpp:234-288, same counts).
 
+// ---- triangle list. The triangle pass of block roots (|S| > 32) records
+// every triangle {u, S[a], S[b]} it finds as (a | b << 16, CSR position of
+// (S[a], S[b])) in a device pool, in per-root pieces; the diamond pass then
+// reads the list (k_diamond_list) instead of probing again. A block reserves
+// pool space for a probe/pair phase up front (an upper bound: one record per
+// probed element or pair test), returns the unused tail after the phase and
+// publishes the phase's records as one piece. Roots whose records did not fit
+// (pool or piece table exhausted, or |S| > kTriListMaxS) are flagged and keep
+// the probing diamond pass; pieces of flagged roots are ignored.
+constexpr int kTriListMaxS = 8192;              // member ids fit 16 bits, sD fits smem
+constexpr unsigned long long kTriListChunk = 1ull << 16;  // records per pool grab
+
+struct TriPiece {
+  unsigned long long start;  // first record
+  int u;                     // root
+  unsigned count;            // records
+};
+
+// Warp roots (|S| <= 32) append into per-warp chunks of kTriListWarpChunk
+// records instead of pieces: a header record (0x80000000 | count, root) then
+// the root's records; a chunk directory entry is written when the warp
+// retires the chunk.
+constexpr unsigned kTriListWarpChunk = 4096;
+
+struct TriChunk {
+  unsigned long long start;
+  unsigned used;
+  unsigned pad;
+};
+
+struct TriList {
+  uint2* rec = nullptr;                 // nullptr: no list
+  unsigned long long cap = 0;           // pool records
+  unsigned long long* top = nullptr;    // pool bump pointer
+  TriPiece* pieces = nullptr;
+  unsigned* npieces = nullptr;
+  unsigned pieces_cap = 0;
+  unsigned char* fail = nullptr;        // per root: 1 = not (fully) listed
+  TriChunk* chunks = nullptr;           // warp-root chunk directory
+  unsigned* nchunks = nullptr;
+  unsigned chunks_cap = 0;
+};
+
 // Warp per root, |S| <= 32: rows are single words.
-constexpr int kRootsWarpInts = 32 * 5 + 33;  // sS, sC, rows, fbase, foff(33), fsplit per warp
+constexpr int kRootsWarpInts = 32 * 5 + 33 + 1;  // sS, sC, rows, fbase, foff(33), fsplit, wcnt
 template <bool kC3, bool kD13, bool kD15>
 __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ rp, const int* __restrict__ ci,
                              const int* __restrict__ split, const int* __restrict__ send,
@@ -1110,7 +1153,8 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
                              const int* __restrict__ roots, int nroots,
                              u64* __restrict__ d13, u64* __restrict__ d15,
                              const unsigned long long* __restrict__ hub,
-                             const int* __restrict__ hub_base, int hb, int hub_force) {
+                             const int* __restrict__ hub_base, int hb, int hub_force,
+                             TriList tl) {
   // kC3: per-edge triangle counts (atomics into C3f) — the triangle pass.
   // kD13: diamonds from the final C3 — a later pass (needs complete C3).
   // Members that are hubs may test their pairs against the hub rows instead
@@ -1126,11 +1170,45 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
   int* fbase = reinterpret_cast<int*>(rows + 32);  // per-warp flattening tables
   int* foff = fbase + 32;                           // 33 entries
   int* fsplit = foff + 33;                          // pair rows: split[S[a]]
+  unsigned* wcnt = reinterpret_cast<unsigned*>(fsplit + 32);  // records of the current root
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  // this warp's triangle-list chunk [cb, ce), write cursor wt (warp-uniform)
+  unsigned long long cb = 0, ce = 0, wt = 0;
+  bool wfail = !(kC3 && tl.rec);
+  auto retire = [&]() {
+    if (wt > cb && lane == 0) {
+      const unsigned ci_ = atomicAdd(tl.nchunks, 1u);
+      if (ci_ < tl.chunks_cap) tl.chunks[ci_] = TriChunk{cb, (unsigned)(wt - cb), 0u};
+    }
+  };
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
     const int u = roots[k];
+    if (kD13 && tl.rec && !tl.fail[u]) continue;  // listed: k_diamond_wlist handles it
     const int s0 = split[u];
     const int s = send[u] - s0;
+    // reserve room for a header and up to C(s,2) records of this root
+    bool listing = false;
+    if (kC3 && tl.rec) {
+      const unsigned long long need = 1 + (unsigned long long)s * (s - 1) / 2;
+      if (!wfail && ce - wt < need) {
+        retire();
+        unsigned long long st0 = 0;
+        if (lane == 0) st0 = atomicAdd(tl.top, (unsigned long long)kTriListWarpChunk);
+        st0 = __shfl_sync(0xffffffffu, st0, 0);
+        if (st0 + kTriListWarpChunk > tl.cap) {
+          wfail = true;
+          cb = ce = wt = 0;
+        } else {
+          cb = wt = st0;
+          ce = st0 + kTriListWarpChunk;
+        }
+      }
+      listing = !wfail;
+      if (lane == 0) {
+        *wcnt = 0;
+        if (!listing) tl.fail[u] = 1;
+      }
+    }
     if (lane < s) {
       sS[lane] = ci[s0 + lane];
       if (kD13) sC[lane] = C3f[s0 + lane];
@@ -1183,6 +1261,15 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
           atomicAdd(C3f + p, 1u);
           atomicAdd(sC + bi, 1u);
           ++na;
+          if (listing) {
+            const unsigned m = __activemask();
+            const int leader = __ffs(m) - 1;
+            unsigned base = 0;
+            if (lane == leader) base = atomicAdd(wcnt, (unsigned)__popc(m));
+            base = __shfl_sync(m, base, leader);
+            tl.rec[wt + 1 + base + __popc(m & ((1u << lane) - 1u))] =
+                make_uint2((u32)r | ((u32)bi << 16), (u32)p);
+          }
         }
         if (kD13) {
           tu += (u64)__ldg(C3f + p) - 1;
@@ -1231,6 +1318,15 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
             atomicAdd(C3f + p, 1u);
             atomicAdd(sC + bi, 1u);
             ++na;
+            if (listing) {
+              const unsigned m = __activemask();
+              const int leader = __ffs(m) - 1;
+              unsigned base = 0;
+              if (lane == leader) base = atomicAdd(wcnt, (unsigned)__popc(m));
+              base = __shfl_sync(m, base, leader);
+              tl.rec[wt + 1 + base + __popc(m & ((1u << lane) - 1u))] =
+                  make_uint2((u32)r | ((u32)bi << 16), (u32)p);
+            }
           }
           if (kD13) {
             tu += (u64)__ldg(C3f + p) - 1;
@@ -1243,6 +1339,14 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
       if (kC3 && na) atomicAdd(sC + cr, na);
       if (kD13 && da) smem_add_u64(sD + cr, da);
       __syncwarp();
+    }
+    if (kC3 && listing) {  // close the root's records with their header
+      __syncwarp();
+      const unsigned cnt = *wcnt;
+      if (cnt) {
+        if (lane == 0) tl.rec[wt] = make_uint2(0x80000000u | cnt, (u32)u);
+        wt += 1 + cnt;
+      }
     }
     if (kC3 && lane < s && sC[lane]) atomicAdd(C3f + s0 + lane, sC[lane]);
     if (kD13) {
@@ -1269,6 +1373,7 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
     }
     __syncwarp();
   }
+  if (kC3 && tl.rec) retire();
 }
 
 // Block per root, |S| > 32. Shared-memory layout (host computes the same
@@ -1278,34 +1383,6 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
 // live in the block's slice of a global slab instead (rare, very large S).
 // Bitmap rows use an odd word stride so lanes reading different rows at the
 // same word index spread over banks.
-// ---- triangle list. The triangle pass of block roots (|S| > 32) records
-// every triangle {u, S[a], S[b]} it finds as (a | b << 16, CSR position of
-// (S[a], S[b])) in a device pool, in per-root pieces; the diamond pass then
-// reads the list (k_diamond_list) instead of probing again. A block reserves
-// pool space for a probe/pair phase up front (an upper bound: one record per
-// probed element or pair test), returns the unused tail after the phase and
-// publishes the phase's records as one piece. Roots whose records did not fit
-// (pool or piece table exhausted, or |S| > kTriListMaxS) are flagged and keep
-// the probing diamond pass; pieces of flagged roots are ignored.
-constexpr int kTriListMaxS = 8192;              // member ids fit 16 bits, sD fits smem
-constexpr unsigned long long kTriListChunk = 1ull << 16;  // records per pool grab
-
-struct TriPiece {
-  unsigned long long start;  // first record
-  int u;                     // root
-  unsigned count;            // records
-};
-
-struct TriList {
-  uint2* rec = nullptr;                 // nullptr: no list
-  unsigned long long cap = 0;           // pool records
-  unsigned long long* top = nullptr;    // pool bump pointer
-  TriPiece* pieces = nullptr;
-  unsigned* npieces = nullptr;
-  unsigned pieces_cap = 0;
-  unsigned char* fail = nullptr;        // per root: 1 = not (fully) listed
-};
-
 struct RootsLayout {
   int s_cap, hcap, hlog, nwarps, stride_cap;
   __host__ __device__ size_t bytes_core() const {  // always in smem
@@ -1829,14 +1906,66 @@ k_diamond_list(const TriPiece* __restrict__ pieces, const unsigned* __restrict__
   }
 }
 
-// Sum over roots u in [u0, u1) with 32 < |N+(u)| <= kTriListMaxS of
-// C(|N+(u)|, 2): an upper bound of the records the triangle list can take.
+// Diamonds of the listed warp roots: warp per chunk, root by root (header,
+// then its records, one per lane), per-member sums in shared memory.
+__global__ void __launch_bounds__(256)
+k_diamond_wlist(const TriChunk* __restrict__ chunks, const unsigned* __restrict__ nchunks,
+                unsigned chunks_cap, const uint2* __restrict__ rec, const int* __restrict__ rp,
+                const int* __restrict__ ci, const int* __restrict__ split,
+                const int* __restrict__ send, const u32* __restrict__ C3f,
+                u64* __restrict__ d13) {
+  __shared__ u64 sDall[8][32];
+  __shared__ u32 sCall[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  u64* sD = sDall[wib];
+  u32* sC = sCall[wib];
+  const unsigned nc = min(*nchunks, chunks_cap);
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nc; k += warps) {
+    const TriChunk ch = chunks[k];
+    unsigned long long pos = ch.start;
+    const unsigned long long end = ch.start + ch.used;
+    while (pos < end) {
+      const uint2 h = rec[pos];
+      const unsigned cnt = h.x & 0x7fffffffu;
+      const int u = (int)h.y;
+      const int s0 = split[u];
+      const int s = send[u] - s0;
+      sD[lane] = 0;
+      sC[lane] = lane < s ? C3f[s0 + lane] : 0u;
+      __syncwarp();
+      const bool narrow = (u64)s * (u64)(rp[u + 1] - rp[u]) < (1ull << 32);
+      u64 tu = 0;
+      for (unsigned i = lane; i < cnt; i += 32) {
+        const uint2 x = rec[pos + 1 + i];
+        const int a = (int)(x.x & 0xffffu), b = (int)(x.x >> 16);
+        tu += (u64)__ldg(C3f + x.y) - 1;
+        if (narrow) {
+          atomicAdd(reinterpret_cast<u32*>(sD + a), sC[b] - 1);
+          atomicAdd(reinterpret_cast<u32*>(sD + b), sC[a] - 1);
+        } else {
+          smem_add_u64(sD + a, (u64)sC[b] - 1);
+          smem_add_u64(sD + b, (u64)sC[a] - 1);
+        }
+      }
+      __syncwarp();
+      if (lane < s && sD[lane]) atomicAdd(d13 + ci[s0 + lane], sD[lane]);
+      tu = warp_sum_u64(tu);
+      if (lane == 0 && tu) atomicAdd(d13 + u, tu);
+      __syncwarp();
+      pos += 1 + cnt;
+    }
+  }
+}
+
+// Sum over roots u in [u0, u1) with 2 <= |N+(u)| <= kTriListMaxS of
+// C(|N+(u)|, 2) (+1 header for warp roots): an upper bound of the records.
 __global__ void k_trilist_bound(const int* __restrict__ split, const int* __restrict__ send,
                                 int u0, int u1, unsigned long long* __restrict__ out) {
   unsigned long long acc = 0;
   for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1; u += gridDim.x * blockDim.x) {
     const unsigned long long s = (unsigned long long)(send[u] - split[u]);
-    if (s > 32 && s <= (unsigned long long)kTriListMaxS) acc += s * (s - 1) / 2;
+    if (s >= 2 && s <= (unsigned long long)kTriListMaxS) acc += s * (s - 1) / 2 + (s <= 32);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
