@@ -306,7 +306,10 @@ constexpr int kC4Long = 48;                 // rows at least this long: flattene
 #define FGLT_GIANT 512
 #endif
 constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many wedges in a tile: warp per row
-constexpr int kQuadsInFlight = 2;          // 16-byte loads in flight per lane (dense batches)
+#ifndef FGLT_QUADS
+#define FGLT_QUADS 2
+#endif
+constexpr int kQuadsInFlight = FGLT_QUADS;          // 16-byte loads in flight per lane (dense batches)
 constexpr int kC4BlockThreads = FGLT_C4B_THREADS;  // class-4 block (one 128 KB table per SM)
 
 // Dense tiles use counters as narrow as the target's degree allows: L[w] <=
