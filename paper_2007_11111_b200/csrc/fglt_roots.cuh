@@ -941,7 +941,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         // some counter >= 2 in the word
         const u32 ge2 = sh == 3 ? 0xeeeeeeeeu : sh == 2 ? 0xfefefefeu : sh == 1 ? 0xfffefffeu
                                                                               : 0xfffffffeu;
-        const int per = 1 << sh, bits = 32 >> sh;
+        const int bits = 32 >> sh;
         const u32 vmask = sh ? (1u << bits) - 1u : 0xffffffffu;
         for (int i4 = threadIdx.x; i4 < n4; i4 += blockDim.x) {
           const uint4 v = L4[i4];

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <sstream>
 #include <string>
 
@@ -262,86 +263,212 @@ std::string lower(std::string_view s) {
   return o;
 }
 
-bool skip_line(std::string_view body) {
-  auto t = tokens(body);
-  return t.empty() || t[0][0] == '#' || t[0][0] == '%';
+
+}  // namespace
+
+// ------------------------------------------------------------ text parsers
+// Same grammar, error classes and messages as the reference's serial parsers
+// (proj/src/graph.cpp:52-157), parsed in parallel: the stream is read whole,
+// cut into per-thread chunks at line boundaries, each chunk is parsed with
+// its own first error, and the chunks are merged in file order, so the error
+// reported is the one the serial parser would have thrown first.
+namespace {
+
+std::string slurp(std::istream& in) {
+  std::string buf;
+  constexpr std::size_t kBlock = std::size_t{1} << 24;
+  for (;;) {
+    const std::size_t at = buf.size();
+    buf.resize(at + kBlock);
+    in.read(buf.data() + at, static_cast<std::streamsize>(kBlock));
+    buf.resize(at + static_cast<std::size_t>(in.gcount()));
+    if (!in) break;
+  }
+  return buf;
+}
+
+std::string_view trim_ws(std::string_view s) {
+  while (!s.empty() && std::isspace(static_cast<unsigned char>(s.front()))) s.remove_prefix(1);
+  while (!s.empty() && std::isspace(static_cast<unsigned char>(s.back()))) s.remove_suffix(1);
+  return s;
+}
+
+// Next line of buf starting at *pos (without the '\n'); false at the end.
+bool next_line(std::string_view buf, std::size_t* pos, std::string_view* line) {
+  if (*pos >= buf.size()) return false;
+  const char* b = buf.data() + *pos;
+  const void* nl = std::memchr(b, '\n', buf.size() - *pos);
+  const std::size_t len = nl ? static_cast<std::size_t>(static_cast<const char*>(nl) - b)
+                             : buf.size() - *pos;
+  *line = std::string_view(b, len);
+  *pos += len + (nl ? 1 : 0);
+  return true;
+}
+
+struct ParsedChunk {
+  std::vector<std::pair<vertex_t, vertex_t>> edges;
+  std::size_t lines = 0;
+  bool failed = false;
+  std::size_t fail_line = 0;         // 1-based within the chunk
+  std::size_t entries_before = 0;    // entries parsed before the failing line
+  std::string fail_suffix;           // message after "line N"
+};
+
+// Chunks [begin, end) of buf cut at line starts.
+std::vector<std::pair<std::size_t, std::size_t>> line_chunks(std::string_view buf, std::size_t from) {
+  const std::size_t len = buf.size() > from ? buf.size() - from : 0;
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t parts = std::max<std::size_t>(1, std::min<std::size_t>(hw, len >> 20));
+  std::vector<std::pair<std::size_t, std::size_t>> out;
+  std::size_t start = from;
+  for (std::size_t k = 1; k <= parts && start < buf.size(); ++k) {
+    std::size_t end = k == parts ? buf.size() : from + len * k / parts;
+    if (end < start) end = start;
+    if (end < buf.size()) {
+      const void* nl = std::memchr(buf.data() + end, '\n', buf.size() - end);
+      end = nl ? static_cast<std::size_t>(static_cast<const char*>(nl) - buf.data()) + 1 : buf.size();
+    }
+    out.emplace_back(start, end);
+    start = end;
+  }
+  return out;
+}
+
+// Parse every chunk on its own thread with `entry(line_view, chunk)`.
+template <class F>
+std::vector<ParsedChunk> parse_chunks(std::string_view buf, std::size_t from, F entry) {
+  auto cuts = line_chunks(buf, from);
+  std::vector<ParsedChunk> res(cuts.size());
+  auto work = [&](std::size_t k) {
+    ParsedChunk& c = res[k];
+    std::size_t pos = cuts[k].first;
+    std::string_view whole = buf.substr(0, cuts[k].second), line;
+    while (next_line(whole, &pos, &line)) {
+      ++c.lines;
+      if (c.failed) continue;  // keep counting lines only
+      std::string suffix;
+      if (!entry(trim_ws(line), &c, &suffix)) {
+        c.failed = true;
+        c.fail_line = c.lines;
+        c.entries_before = c.edges.size();
+        c.fail_suffix = std::move(suffix);
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (std::size_t k = 1; k < cuts.size(); ++k) th.emplace_back(work, k);
+  if (!cuts.empty()) work(0);
+  for (auto& t : th) t.join();
+  return res;
+}
+
+bool parse_i64(std::string_view t, std::int64_t* v) {
+  auto r = std::from_chars(t.data(), t.data() + t.size(), *v);
+  return r.ec == std::errc{} && r.ptr == t.data() + t.size();
 }
 
 }  // namespace
 
 EdgeCollection parse_edge_list(std::istream& in) {
+  const std::string buf = slurp(in);
+  auto chunks = parse_chunks(buf, 0, [](std::string_view body, ParsedChunk* c, std::string* err) {
+    if (body.empty() || body.front() == '#' || body.front() == '%') return true;
+    auto t = tokens(body);
+    if (t.size() != 2) {
+      *err = ": expected 'u v', got " + std::to_string(t.size()) + " tokens";
+      return false;
+    }
+    std::int64_t u = 0, v = 0;
+    if (!parse_i64(t[0], &u)) { *err = ": malformed vertex id '" + std::string(t[0]) + "'"; return false; }
+    if (!parse_i64(t[1], &v)) { *err = ": malformed vertex id '" + std::string(t[1]) + "'"; return false; }
+    if (u < 0 || v < 0) { *err = ": negative vertex id"; return false; }
+    c->edges.emplace_back(u, v);
+    return true;
+  });
   EdgeCollection ec;
   ec.origin = EdgeOrigin::kEdgeList;
-  std::string line;
-  std::size_t ln = 0;
-  while (std::getline(in, line)) {
-    ++ln;
-    if (skip_line(line)) continue;
-    auto t = tokens(line);
-    if (t.size() != 2)
-      throw ParseError("line " + std::to_string(ln) + ": expected 'u v', got " +
-                       std::to_string(t.size()) + " tokens");
-    const vertex_t u = to_int(t[0], ln, "vertex id"), v = to_int(t[1], ln, "vertex id");
-    if (u < 0 || v < 0) throw ParseError("line " + std::to_string(ln) + ": negative vertex id");
-    ec.edges.emplace_back(u, v);
+  std::size_t line_base = 0, total = 0;
+  for (auto& c : chunks) {
+    if (c.failed) throw ParseError("line " + std::to_string(line_base + c.fail_line) + c.fail_suffix);
+    line_base += c.lines;
+    total += c.edges.size();
   }
+  ec.edges.reserve(total);
+  for (auto& c : chunks) ec.edges.insert(ec.edges.end(), c.edges.begin(), c.edges.end());
   return ec;
 }
 
 EdgeCollection parse_matrix_market(std::istream& in) {
-  std::string line;
-  if (!std::getline(in, line)) throw ParseError("empty Matrix Market stream");
+  const std::string buf = slurp(in);
+  std::size_t pos = 0, ln = 0;
+  std::string_view line;
+  if (!next_line(buf, &pos, &line)) throw ParseError("empty Matrix Market stream");
+  ++ln;
   auto banner = tokens(line);
   if (banner.size() < 5 || lower(banner[0]) != "%%matrixmarket" || lower(banner[1]) != "matrix")
     throw ParseError("line 1: missing %%MatrixMarket matrix banner");
   if (lower(banner[2]) != "coordinate")
-    throw ParseError("line 1: only coordinate format is supported, got '" +
-                     std::string(banner[2]) + "'");
+    throw ParseError("line 1: only coordinate format is supported, got '" + lower(banner[2]) + "'");
   const std::string field = lower(banner[3]), sym = lower(banner[4]);
   if (field != "pattern" && field != "real" && field != "integer")
     throw ParseError("line 1: unsupported field '" + field + "'");
   if (sym != "general" && sym != "symmetric")
     throw ParseError("line 1: unsupported symmetry '" + sym + "'");
   const std::size_t per_entry = field == "pattern" ? 2 : 3;
-  std::size_t ln = 1;
-  std::int64_t rows = -1, cols = -1, nnz = -1;
-  while (std::getline(in, line)) {
+  // size line, after any comments (only '%' lines are comments here)
+  std::int64_t rows = 0, cols = 0, nnz = 0;
+  for (;;) {
+    if (!next_line(buf, &pos, &line)) throw ParseError("unexpected end of stream before size line");
     ++ln;
-    if (skip_line(line)) continue;
-    auto t = tokens(line);
+    const std::string_view body = trim_ws(line);
+    if (body.empty() || body.front() == '%') continue;
+    auto t = tokens(body);
     if (t.size() != 3) throw ParseError("line " + std::to_string(ln) + ": expected 'rows cols nnz'");
     rows = to_int(t[0], ln, "row count");
     cols = to_int(t[1], ln, "column count");
     nnz = to_int(t[2], ln, "entry count");
     break;
   }
-  if (rows < 0 && cols < 0 && nnz < 0) throw ParseError("unexpected end of stream before size line");
   if (rows != cols)
     throw ParseError("dimension mismatch: adjacency must be square, got " + std::to_string(rows) +
                      "x" + std::to_string(cols));
   if (rows < 0 || nnz < 0) throw ParseError("negative size header");
+  auto chunks = parse_chunks(buf, pos, [&](std::string_view body, ParsedChunk* c, std::string* err) {
+    if (body.empty() || body.front() == '%') return true;
+    auto t = tokens(body);
+    if (t.size() != per_entry) {
+      *err = ": expected " + std::to_string(per_entry) + " tokens per entry";
+      return false;
+    }
+    std::int64_t i = 0, j = 0;
+    if (!parse_i64(t[0], &i)) { *err = ": malformed row index '" + std::string(t[0]) + "'"; return false; }
+    if (!parse_i64(t[1], &j)) { *err = ": malformed column index '" + std::string(t[1]) + "'"; return false; }
+    if (i < 1 || i > rows || j < 1 || j > cols) {
+      *err = ": entry (" + std::to_string(i) + "," + std::to_string(j) + ") out of declared range " +
+             std::to_string(rows);
+      return false;
+    }
+    c->edges.emplace_back(i - 1, j - 1);
+    return true;
+  });
   EdgeCollection ec;
   ec.origin = sym == "symmetric" ? EdgeOrigin::kMatrixMarketSymmetric : EdgeOrigin::kMatrixMarketGeneral;
   ec.declared_n = rows;
-  ec.edges.reserve(static_cast<std::size_t>(nnz));
-  std::int64_t got = 0;
-  while (got < nnz) {
-    if (!std::getline(in, line))
-      throw ParseError("unexpected end of stream: got " + std::to_string(got) + " of " +
-                       std::to_string(nnz) + " entries");
-    ++ln;
-    if (skip_line(line)) continue;
-    auto t = tokens(line);
-    if (t.size() != per_entry)
-      throw ParseError("line " + std::to_string(ln) + ": expected " + std::to_string(per_entry) +
-                       " tokens per entry");
-    const vertex_t i = to_int(t[0], ln, "row index"), j = to_int(t[1], ln, "column index");
-    if (i < 1 || i > rows || j < 1 || j > cols)
-      throw ParseError("line " + std::to_string(ln) + ": entry (" + std::to_string(i) + "," +
-                       std::to_string(j) + ") out of declared range " + std::to_string(rows));
-    ec.edges.emplace_back(i - 1, j - 1);
-    ++got;
+  // the serial parser stops after nnz entries: later lines (even malformed ones) are never read
+  std::int64_t seen = 0;
+  std::size_t line_base = ln;
+  for (auto& c : chunks) {
+    if (seen >= nnz) break;
+    if (c.failed && seen + static_cast<std::int64_t>(c.entries_before) < nnz)
+      throw ParseError("line " + std::to_string(line_base + c.fail_line) + c.fail_suffix);
+    const std::int64_t take = std::min<std::int64_t>(static_cast<std::int64_t>(c.edges.size()), nnz - seen);
+    ec.edges.insert(ec.edges.end(), c.edges.begin(), c.edges.begin() + take);
+    seen += take;
+    line_base += c.lines;
   }
+  if (seen < nnz)
+    throw ParseError("unexpected end of stream: got " + std::to_string(seen) + " of " +
+                     std::to_string(nnz) + " entries");
   return ec;
 }
 
