@@ -2010,15 +2010,36 @@ __device__ __forceinline__ void offer_err(u64* err, int stage, long long v, int 
   atomicMin(err, key);
 }
 
-__global__ void k_epilogue(EpilogueIn in, const DictInfo* __restrict__ dict, int v0, int v1,
+constexpr int kEpilogueThreads = 128;
+
+__global__ void __launch_bounds__(kEpilogueThreads) k_epilogue(EpilogueIn in, const DictInfo* __restrict__ dict, int v0, int v1,
                            int lenient, u64* __restrict__ raw, u64* __restrict__ net,
                            u64* __restrict__ err) {
   __shared__ DictInfo D;
+  // rows are staged here and written out coalesced (a thread's own row is
+  // 128 B: direct stores would touch 32 lines per warp instruction)
+  __shared__ u64 stage[kEpilogueThreads * 17];
   if (threadIdx.x == 0) D = *dict;
   __syncthreads();
   const int k = D.k;
+  const int stride = k | 1;  // odd row stride: conflict-free 8-byte staging
   const unsigned m = D.mask;
-  for (int v = v0 + blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += gridDim.x * blockDim.x) {
+  for (int vb = v0 + blockIdx.x * blockDim.x; vb < v1; vb += gridDim.x * blockDim.x) {
+    const int v = vb + threadIdx.x;
+    const int nrows = min((int)blockDim.x, v1 - vb);
+    auto store_rows = [&](const u64* vals, u64* out) {
+      __syncthreads();
+      if (v < v1)
+        for (int i = 0; i < k; ++i) stage[threadIdx.x * stride + i] = vals[i];
+      __syncthreads();
+      u64* o = out + (long long)(vb - v0) * k;
+      for (int i = threadIdx.x; i < nrows * k; i += blockDim.x) {
+        const int row = i / k;
+        o[i] = stage[row * stride + (i - row * k)];
+      }
+    };
+    u64 rw[16], nt[16];
+    if (v < v1) {
     const int r = in.inv ? in.inv[v] : v;
     const u64 d = (u64)(in.rp[r + 1] - in.rp[r]);
     u64 col[16];
@@ -2057,7 +2078,6 @@ __global__ void k_epilogue(EpilogueIn in, const DictInfo* __restrict__ dict, int
     col[13] = in.d13 ? in.d13[r] : 0;
     col[14] = in.d14 ? in.d14[r] : 0;
     col[15] = in.d15 ? in.d15[r] : 0;
-    u64 rw[16], nt[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (i < k) rw[i] = col[D.ids[i]];
@@ -2087,11 +2107,9 @@ __global__ void k_epilogue(EpilogueIn in, const DictInfo* __restrict__ dict, int
         nt[rr] = rw[rr] - absorbed;
       }
     }
-    const long long o = (long long)(v - v0) * k;
-    if (raw)
-      for (int i = 0; i < k; ++i) raw[o + i] = rw[i];
-    if (net)
-      for (int i = 0; i < k; ++i) net[o + i] = nt[i];
+    }
+    if (raw) store_rows(rw, raw);
+    if (net) store_rows(nt, net);
   }
 }
 
