@@ -55,6 +55,12 @@ const unsigned char kU16[16][16] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
 };
 
+#ifndef FGLT_C4_CLASS2_THREADS
+#define FGLT_C4_CLASS2_THREADS 128
+#endif
+#ifndef FGLT_C4_CLASS8_THREADS
+#define FGLT_C4_CLASS8_THREADS 64
+#endif
 constexpr int kSmallS = 32;       // roots with |N+(u)| <= 32: warp kernel
 constexpr int kBlockS = 1024;     // <= 1024: block kernel, bitmap in smem
 constexpr int kWarpHashLog = 9;   // 512-slot table per warp (wc <= 256)
@@ -828,24 +834,26 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       check_launch();
       c->launched();
     }
-    if (cnt[1] > 0) {  // class 2: 128-thread block-flattened tables of <= 2048 slots
+    if (cnt[1] > 0) {  // class 2: block-flattened tables of <= 2048 slots
+      constexpr int NT2 = FGLT_C4_CLASS2_THREADS;
       const size_t sm = (size_t)(1 << kWarpHashLog2) * 8;
-      set_smem(k_c4_block<128>, sm);
+      set_smem(k_c4_block<NT2>, sm);
       int occ = 1;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<128>, 128, sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<NT2>, NT2, sm));
       const int g = std::min(cnt[1], c->sms * std::max(occ, 1));
-      k_c4_block<128><<<g, 128, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[1], cnt[1],
+      k_c4_block<NT2><<<g, NT2, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[1], cnt[1],
                                                 wc, parts, kWarpHashLog2, queues + 4, c4);
       check_launch();
       c->launched();
     }
-    if (cnt[7] > 0) {  // class 8: 128-thread block-flattened tables of <= 1024 slots
+    if (cnt[7] > 0) {  // class 8: block-flattened tables of <= 1024 slots
+      constexpr int NT8 = FGLT_C4_CLASS8_THREADS;
       const size_t sm = (size_t)(1 << (kWarpHashLog2 - 1)) * 8;
-      set_smem(k_c4_block<128>, (size_t)(1 << kWarpHashLog2) * 8);
+      set_smem(k_c4_block<NT8>, sm);
       int occ = 1;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<128>, 128, sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<NT8>, NT8, sm));
       const int g = std::min(cnt[7], c->sms * std::max(occ, 1));
-      k_c4_block<128><<<g, 128, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[7], cnt[7],
+      k_c4_block<NT8><<<g, NT8, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[7], cnt[7],
                                                 wc, parts, kWarpHashLog2 - 1, queues + 6, c4);
       check_launch();
       c->launched();
