@@ -306,6 +306,9 @@ constexpr int kC4Long = 48;                 // rows at least this long: flattene
 #define FGLT_GIANT 512
 #endif
 constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many wedges in a tile: warp per row
+#ifndef FGLT_PROBE_NOCUT
+#define FGLT_PROBE_NOCUT 0  // probe lists up to this long are probed whole (no cut search)
+#endif
 #ifndef FGLT_QUADS
 #define FGLT_QUADS 2
 #endif
@@ -1230,7 +1233,8 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
     if (lane + 1 < s) {
       x = sS[lane];
       st = split[x];
-      len = lower_bound_i32(ci, st, rp[x + 1], smax + 1) - st;
+      const int full = rp[x + 1];  // short lists: probe whole, skip the dependent search
+      len = (full - st <= FGLT_PROBE_NOCUT ? full : lower_bound_i32(ci, st, full, smax + 1)) - st;
       pairs = hub != nullptr && x >= hb && (hub_force || s - 1 - lane < len);
       if (pairs) len = 0;
     }
@@ -1625,7 +1629,8 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
       if (a_me + 1 < s) {
         x = sS[a_me];
         st = split[x];
-        se = lower_bound_i32(ci, st, rp[x + 1], smax + 1);
+        const int full = rp[x + 1];  // short lists: probe whole, skip the dependent search
+        se = full - st <= FGLT_PROBE_NOCUT ? full : lower_bound_i32(ci, st, full, smax + 1);
         pairs = hub != nullptr && x >= hb && (hub_force || (s - 1 - a_me) < se - st);
       }
       // probe rows
