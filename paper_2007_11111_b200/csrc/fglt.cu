@@ -578,19 +578,21 @@ __global__ void k_gather_keys(const int* __restrict__ list, int cnt, const u64* 
 }
 
 // Order a root list by work, largest first (LPT for the dynamic queues).
-void sort_by_work_desc(fglt_ctx* c, int* list, int cnt, const u64* w) {
+// Keys are < 2^bits (radix passes only over the live bits).
+void sort_by_work_desc(fglt_ctx* c, int* list, int cnt, const u64* w, int bits = 64) {
   if (cnt < 2) return;
+  bits = std::max(1, std::min(bits, 64));
   u64* k = c->ensure<u64>(B_SORTK, 2 * (size_t)cnt);
   int* v = c->ensure<int>(B_SORTV, (size_t)cnt);
   k_gather_keys<<<c->grid(cnt, 256), 256, 0, c->stream>>>(list, cnt, w, k);
   check_launch();
   c->launched();
   size_t tb = 0;
-  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, k, k + cnt, list, v, cnt, 0, 64,
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, k, k + cnt, list, v, cnt, 0, bits,
                                                c->stream));
   void* tmp = c->ensure<unsigned char>(B_CUB, tb);
   tb = c->buf[B_CUB].cap;
-  CK(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, k, k + cnt, list, v, cnt, 0, 64,
+  CK(cub::DeviceRadixSort::SortPairsDescending(tmp, tb, k, k + cnt, list, v, cnt, 0, bits,
                                                c->stream));
   c->launched();
   CK(cudaMemcpyAsync(list, v, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, c->stream));
@@ -645,8 +647,10 @@ void root_bins(fglt_ctx* c, int64_t u0, int64_t u1) {
   int64_t stride = 0;
   c->rb_cnt = bin_roots(c, key, u0, u1, std::vector<u64>(std::begin(kRootThr), std::end(kRootThr)),
                         c->rb_lists, &stride, B_RLISTS);
+  // keys are |N+(u)| <= max out-degree (or a forced bin key <= 1025)
+  const int kbits = 64 - __builtin_clzll(std::max<u64>(std::max<u64>(c->maxout, 1025), 1));
   for (int b = 1; b < (int)c->rb_cnt.size(); ++b)
-    sort_by_work_desc(c, c->rb_lists[b], c->rb_cnt[b], key);
+    sort_by_work_desc(c, c->rb_lists[b], c->rb_cnt[b], key, kbits);
   c->rb_u0 = u0;
   c->rb_u1 = u1;
 }
@@ -821,7 +825,9 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     check_launch();
     c->launched();
     std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6, 7}, lists, &stride);
-    for (int bb = 3; bb <= 6; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc);
+    // wc(u) <= W = sum of squared degrees
+    const int wbits = 64 - __builtin_clzll(std::max<u64>(c->W, 1));
+    for (int bb = 3; bb <= 6; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc, wbits);
     int* queues = reinterpret_cast<int*>(c->d_small + 56);  // dynamic root queues
     CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
     c->mark("four-cycle rows:start");
