@@ -86,6 +86,10 @@ typedef struct fglt_ctx fglt_ctx;
  * the legacy default stream). Returns NULL and fills err on failure. */
 fglt_ctx* fglt_ctx_create(int device, void* stream, fglt_error* err);
 void fglt_ctx_destroy(fglt_ctx* ctx);
+/* Free the context's device workspace (it is kept between calls for reuse;
+ * the triangle-list pool alone may hold up to 45% of the free HBM after a
+ * large transform). The next call re-allocates what it needs. */
+int fglt_ctx_release_workspace(fglt_ctx* ctx);
 
 /* One full transform: raw + net for the dictionary `dict_mask` (bit k =
  * graphlet k; bits 0 and 1 are forced, Dictionary::from_ids,

@@ -21,7 +21,7 @@ CODES = {0: "ok", 1: "parse", 2: "structural", 3: "overflow", 4: "inconsistency"
          5: "io", 6: "cuda", 7: "no-device"}
 
 EXPORTS = [
-    "fglt_ctx_create", "fglt_ctx_destroy", "fglt_ctx_transform", "fglt_transform_csr32",
+    "fglt_ctx_create", "fglt_ctx_destroy", "fglt_ctx_release_workspace", "fglt_ctx_transform", "fglt_transform_csr32",
     "fglt_net_from_raw", "fglt_stage_prepare", "fglt_stage_bounds", "fglt_stage_triangles",
     "fglt_stage_local", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
     "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug", "fglt_build_csr",
@@ -78,6 +78,8 @@ def lib():
         L.fglt_ctx_create.argtypes = [ctypes.c_int, vp, ctypes.POINTER(FgltError)]
         L.fglt_ctx_destroy.restype = None
         L.fglt_ctx_destroy.argtypes = [vp]
+        L.fglt_ctx_release_workspace.restype = ctypes.c_int
+        L.fglt_ctx_release_workspace.argtypes = [vp]
         L.fglt_ctx_transform.restype = ctypes.c_int
         L.fglt_ctx_transform.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32,
                                          ctypes.c_int, ctypes.c_uint32, vp, vp,
@@ -188,6 +190,12 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(self._L.fglt_ctx_kernel_launches(self._h))
+
+    def release_workspace(self):
+        """Free the device workspace kept between calls (see include/fglt.h)."""
+        rc = self._L.fglt_ctx_release_workspace(self._h)
+        if rc:
+            raise RuntimeError(f"fglt_ctx_release_workspace failed ({CODES.get(rc, rc)})")
 
     def close(self):
         if getattr(self, "_h", None):

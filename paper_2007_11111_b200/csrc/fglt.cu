@@ -1298,6 +1298,27 @@ fglt_ctx* fglt_ctx_create(int device, void* stream, fglt_error* err) {
   return c;
 }
 
+int fglt_ctx_release_workspace(fglt_ctx* c) {
+  if (!c) return FGLT_E_NO_DEVICE;
+  if (cudaSetDevice(c->device) != cudaSuccess) return FGLT_E_CUDA;
+  for (auto& b : c->buf) {
+    if (b.p) cudaFreeAsync(b.p, c->stream);
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  c->scratch_bytes = 0;
+  c->n = c->nnz = c->m = 0;  // cached graph state refers to the freed buffers
+  c->have_stats = false;
+  c->rb_u0 = c->rb_u1 = -1;
+  c->rb_cnt.clear();
+  c->hub_built = false;
+  c->big_rows_listed = false;
+  c->tl = TriList{};
+  c->tl_u0 = c->tl_u1 = -1;
+  c->ing_n = c->ing_nnz = 0;
+  return cudaStreamSynchronize(c->stream) == cudaSuccess ? FGLT_OK : FGLT_E_CUDA;
+}
+
 void fglt_ctx_destroy(fglt_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);

@@ -727,6 +727,12 @@ TransformResult transform(const SparseAdjacency& g, const TransformOptions& opt)
   return r;
 }
 
+void release_device_workspace() {
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  std::lock_guard<std::mutex> run(g_run_mu);
+  for (auto& kv : g_ctx) fglt_ctx_release_workspace(kv.second);
+}
+
 NetFrequencyField net_from_raw(const RawFrequencyField& raw, const ConversionMatrix& U,
                                bool lenient, int /*threads*/) {
   if (raw.dictionary().ids() != U.ids())

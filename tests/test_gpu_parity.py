@@ -464,3 +464,17 @@ def test_config4_full_size_properties():
     assert rc == 0, err
     assert np.array_equal(raw_d.cpu().numpy().view(np.uint64), raw)
     assert np.array_equal(net_d.cpu().numpy().view(np.uint64), net)
+
+
+def test_release_workspace_then_transform():
+    """Freeing the kept workspace between calls changes nothing but memory."""
+    import paper_2007_11111_b200 as gt
+    rp, ci = graphs.rmat(12, 16, seed=8)
+    c = _capi.Context(0)
+    a = c.transform_host(rp, ci)
+    c.release_workspace()
+    b = c.transform_host(rp, ci)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    c.close()
+    from paper_2007_11111_b200 import _core
+    _core.release_device_memory()
