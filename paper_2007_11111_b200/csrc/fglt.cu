@@ -55,6 +55,9 @@ const unsigned char kU16[16][16] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
 };
 
+#ifndef FGLT_MIRROR_SORT_DEG
+#define FGLT_MIRROR_SORT_DEG 8  // mean degree from which mirror slots come from a transpose sort
+#endif
 #ifndef FGLT_C4_CLASS2_THREADS
 #define FGLT_C4_CLASS2_THREADS 128
 #endif
@@ -465,7 +468,7 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   int* mir = c->ensure<int>(B_MIR, std::max<int64_t>(nnz, 1));
   int* ce_row = c->ensure<int>(B_CE_ROW, std::max<int64_t>(c->m, 1));
   int* ce_pos = c->ensure<int>(B_CE_POS, std::max<int64_t>(c->m, 1));
-  const bool sort_mirror = nnz >= 8 * n;  // else per-edge binary searches are cheaper
+  const bool sort_mirror = nnz >= FGLT_MIRROR_SORT_DEG * n;  // else per-edge binary searches
   if (nnz > 0 && !sort_mirror) {
     k_mirror<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, send, orp, N, mir,
                                                           ce_row, ce_pos);
