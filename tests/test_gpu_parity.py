@@ -478,3 +478,21 @@ def test_release_workspace_then_transform():
     c.close()
     from paper_2007_11111_b200 import _core
     _core.release_device_memory()
+
+
+def test_degenerate_shapes(ctx):
+    """Shapes that leave parts of the pipeline empty: no active vertices
+    (perfect matching, single edge), one vertex, isolated tail vertices, two
+    disjoint triangles, a path, a 4-clique plus pendants, and a star with one
+    hub whose N-(u) holds every other vertex."""
+    m = 50
+    matching = gu.from_pairs([(2 * i, 2 * i + 1) for i in range(m)], 2 * m)
+    cases = [matching, gu.from_pairs([(0, 1)], 2), gu.from_pairs([], 1),
+             gu.from_pairs([(0, 1), (1, 2), (2, 0)], 40),
+             gu.from_pairs([(0, 1), (1, 2), (2, 0), (3, 4), (4, 5), (5, 3)], 6),
+             gu.path(300), gu.complete(4),
+             gu.from_pairs([(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3), (3, 4), (4, 5)], 6),
+             gu.star(2000)]
+    for rp, ci in cases:
+        check_same(ctx, rp, ci)
+        check_same(ctx, rp, ci, mask=_capi.dict_mask([12, 13, 15]))
