@@ -691,7 +691,7 @@ void roots_pass(fglt_ctx* c) {
     // block size follows |S|: 64 threads for |S| <= 128, 128 for <= 256, else 256
     const int nt = global ? kRootsThreads : (b == 1 ? 64 : b == 2 ? 128 : kRootsThreads);
     L.nwarps = nt / 32;
-    L.stride_cap = ((L.s_cap + 31) / 32) | 1;
+    L.stride_cap = bitmap_stride((L.s_cap + 31) / 32);
     size_t sm = L.bytes_core();
     unsigned char* slab = nullptr;
     long long slab_stride = 0;

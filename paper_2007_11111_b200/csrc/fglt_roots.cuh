@@ -1388,8 +1388,13 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
 // hash keys int[hcap] | hash idx u16[hcap] | per-warp pair lists u16[nw x s_cap]
 // | bitmap u32[s_cap x stride_cap]. With kGlobal the bitmap, hash and lists
 // live in the block's slice of a global slab instead (rare, very large S).
-// Bitmap rows use an odd word stride so lanes reading different rows at the
+// Bitmap rows use the bitmap_stride() stride so lanes reading different rows at the
 // same word index spread over banks.
+// G[S] bitmap row stride in 32-bit words: rows hold whole 64-bit words (for
+// 64-bit popcounts) and an odd number of them, so lanes reading different
+// rows at the same index spread over the banks.
+__host__ __device__ inline int bitmap_stride(int nw) { return 2 * (((nw + 1) >> 1) | 1); }
+
 struct RootsLayout {
   int s_cap, hcap, hlog, nwarps, stride_cap;
   __host__ __device__ size_t bytes_core() const {  // always in smem
@@ -1513,7 +1518,8 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     const int s = send[u] - s0;
     if (kC3 && tl.rec && threadIdx.x == 0) s_tfail = s > kTriListMaxS;
     const int nw = (s + 31) >> 5;
-    const int stride = nw | 1;
+    const int stride = bitmap_stride(nw);
+    const int nw64 = (nw + 1) >> 1;
     int hlog = 6;
     while ((1 << hlog) < 4 * s) ++hlog;
     const int hcap = 1 << hlog;
@@ -1755,9 +1761,10 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         // (a, b > a) popcounted once and credited to both ends
         for (int a = threadIdx.x; a + 1 < s; a += NT) {
           const u32* ra = bm + (long long)a * stride;
-          u32 r[FGLT_K4_THREAD_NW];
+          const u64* ra64 = reinterpret_cast<const u64*>(ra);
+          u64 r[FGLT_K4_THREAD_NW / 2];
 #pragma unroll
-          for (int t = 0; t < FGLT_K4_THREAD_NW; ++t) r[t] = t < nw ? ra[t] : 0u;
+          for (int t = 0; t < FGLT_K4_THREAD_NW / 2; ++t) r[t] = t < nw64 ? ra64[t] : 0ull;
           const int j0 = (a + 1) >> 5;
           u32 acc = 0;
           for (int j = j0; j < nw; ++j) {
@@ -1765,11 +1772,11 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
             while (w) {
               const int bb = (j << 5) + __ffs(w) - 1;
               w &= w - 1;
-              const u32* rb = bm + (long long)bb * stride;
+              const u64* rb = reinterpret_cast<const u64*>(bm + (long long)bb * stride);
               u32 c = 0;
 #pragma unroll
-              for (int t = 0; t < FGLT_K4_THREAD_NW; ++t)
-                if (t < nw) c += __popc(r[t] & rb[t]);
+              for (int t = 0; t < FGLT_K4_THREAD_NW / 2; ++t)
+                if (t < nw64) c += __popcll(r[t] & rb[t]);
               if (c) {
                 acc += c;
                 atomicAdd(sK + bb, c);
@@ -1795,9 +1802,10 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
             if (w == 0) continue;
             if ((w >> lane) & 1u) {
               const int bb = (j << 5) + lane;
-              const u32* rb = bm + (long long)bb * stride;
+              const u64* rb = reinterpret_cast<const u64*>(bm + (long long)bb * stride);
+              const u64* ra64 = reinterpret_cast<const u64*>(ra);
               u32 c = 0;
-              for (int t = 0; t < nw; ++t) c += __popc(ra[t] & rb[t]);
+              for (int t = 0; t < nw64; ++t) c += __popcll(ra64[t] & rb[t]);
               if (c) {
                 acc += c;
                 atomicAdd(sK + bb, c);
@@ -1829,9 +1837,10 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
           for (int i = lane; i < written; i += 32) {
             const int bb = mylist[i];
             FGLT_BOUNDS(bb > a && bb < s, "list", bb, s);
-            const u32* rb = bm + (long long)bb * stride;
+            const u64* rb = reinterpret_cast<const u64*>(bm + (long long)bb * stride);
+            const u64* ra64 = reinterpret_cast<const u64*>(ra);
             u32 c = 0;
-            for (int t = 0; t < nw; ++t) c += __popc(ra[t] & rb[t]);
+            for (int t = 0; t < nw64; ++t) c += __popcll(ra64[t] & rb[t]);
             if (c) {
               acc += c;
               atomicAdd(sK + bb, c);
