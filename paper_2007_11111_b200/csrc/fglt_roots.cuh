@@ -1456,7 +1456,7 @@ __global__ void k_hub_rows(const int* __restrict__ ci, const int* __restrict__ s
 }
 
 #ifndef FGLT_K4_THREAD_NW
-#define FGLT_K4_THREAD_NW 8  // G[S] rows of at most this many words: thread-per-member 4-cliques
+#define FGLT_K4_THREAD_NW 16  // G[S] rows of at most this many words: thread-per-member 4-cliques
 #endif
 constexpr int kRootsThreads = 256;  // block threads for |S| > 256 (smaller bins: 64, 128)
 constexpr int kPairsInFlight = 4;  // hub-row words in flight per lane
