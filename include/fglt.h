@@ -87,7 +87,7 @@ typedef struct fglt_ctx fglt_ctx;
 fglt_ctx* fglt_ctx_create(int device, void* stream, fglt_error* err);
 void fglt_ctx_destroy(fglt_ctx* ctx);
 /* Free the context's device workspace (it is kept between calls for reuse;
- * the triangle-list pool alone may hold up to 45% of the free HBM after a
+ * the triangle-list pool alone may hold up to 70% of the free HBM after a
  * large transform). The next call re-allocates what it needs. */
 int fglt_ctx_release_workspace(fglt_ctx* ctx);
 

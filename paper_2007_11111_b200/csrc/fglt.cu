@@ -55,6 +55,9 @@ const unsigned char kU16[16][16] = {
     {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
 };
 
+#ifndef FGLT_TL_MEM_FRAC
+#define FGLT_TL_MEM_FRAC 0.70  // triangle-list pool: at most this share of the free HBM
+#endif
 #ifndef FGLT_MIRROR_SORT_DEG
 #define FGLT_MIRROR_SORT_DEG 8  // mean degree from which mirror slots come from a transpose sort
 #endif
@@ -722,7 +725,7 @@ void roots_pass(fglt_ctx* c) {
 }
 
 // Triangle-list pool for the roots [u0,u1) (see TriList): sized by the
-// C(|S|,2) bound plus one grab per block, capped at 45% of free memory.
+// C(|S|,2) bound plus one grab per block, capped at FGLT_TL_MEM_FRAC (70%) of free memory.
 void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
   c->tl = TriList{};
   const Plan& P = c->plan;
@@ -739,11 +742,11 @@ void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
   if (bound == 0) return;
   const unsigned long long blocks = (unsigned long long)c->sms * 8 * 4 * 4;
   unsigned long long cap = bound + blocks * kTriListChunk;
-  if (cap * 8 > c->buf[B_TLREC].cap) {  // growing: stay within 45% of free memory
+  if (cap * 8 > c->buf[B_TLREC].cap) {  // growing: stay within FGLT_TL_MEM_FRAC of free memory
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
     cap = std::min<unsigned long long>(
-        cap, (unsigned long long)(0.45 * (double)(free_b + c->buf[B_TLREC].cap)) / 8);
+        cap, (unsigned long long)(FGLT_TL_MEM_FRAC * (double)(free_b + c->buf[B_TLREC].cap)) / 8);
   }
   if (c->tl_mode == 2) cap = 4096;
   if (cap < 1024) return;
