@@ -816,7 +816,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     const int G = group_for((double)c->nnz / (double)c->n);
     DISPATCH_G(G, launch_root_work, c, wc);
     // degree bands of the dense counters (4 / 8 / 16-or-32 bits)
-    int bands[2] = {0, 0};
+    int bands[3] = {0, 0, 0};
     if (c->nact > 0) {
       int* d_b = reinterpret_cast<int*>(c->d_small + 41);
       k_degree_bands<<<1, 32, 0, c->stream>>>(c->rp, (int)c->nact, d_b);
@@ -826,7 +826,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       CK(cudaStreamSynchronize(c->stream));
     }
     k_c4_class<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(
-        c->rp, c->split, wc, (int)u0, (int)u1, bands[0], bands[1], cls, parts,
+        c->rp, c->split, wc, (int)u0, (int)u1, bands[0], bands[1], bands[2], cls, parts,
         c->force_c4_class, c->force_c4_parts);
     check_launch();
     c->launched();
@@ -898,10 +898,12 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     const long long nact = (long long)c->nact;
     auto tiles_for = [&](long long tile_bytes, Buf tb_buf, Buf bnd_buf, int** bnd_out) -> int* {
       std::vector<int> h{0};
-      const long long t4 = 2 * tile_bytes, t8 = tile_bytes, t32 = tile_bytes / 4;
+      const long long t4 = 2 * tile_bytes, t8 = tile_bytes, t16 = tile_bytes / 2,
+                      t32 = tile_bytes / 4;
       for (long long x = 0; x < nact;) {
         const long long e = x < bands[0] ? std::min<long long>(x + t4, bands[0])
                           : x < bands[1] ? std::min<long long>(x + t8, bands[1])
+                          : x < bands[2] ? std::min<long long>(x + t16, bands[2])
                                          : std::min<long long>(x + t32, nact);
         h.push_back((int)e);
         x = e;
@@ -931,12 +933,12 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
           set_smem(k_c4_dense<true, kC4DenseThreads>, sm);
           k_c4_dense<true, kC4DenseThreads><<<g, kC4DenseThreads, sm, c->stream>>>(
               c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
-              bnd, nact, tb, bands[0], bands[1], queues + 2, c4);
+              bnd, nact, tb, bands[0], bands[1], bands[2], queues + 2, c4);
         } else {
           set_smem(k_c4_dense<false, kC4DenseThreads>, sm);
           k_c4_dense<false, kC4DenseThreads><<<g, kC4DenseThreads, sm, c->stream>>>(
               c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
-              bnd, nact, tb, bands[0], bands[1], queues + 3, c4);
+              bnd, nact, tb, bands[0], bands[1], bands[2], queues + 3, c4);
         }
         check_launch();
         c->launched();
@@ -951,7 +953,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       set_smem(k_c4_dense<true, kC4DenseThreadsS>, sm);
       k_c4_dense<true, kC4DenseThreadsS><<<g, kC4DenseThreadsS, sm, c->stream>>>(
           c->rp, c->ci, c->split, c->mir, lists[6], cnt[6], cur, (long long)(c->dmax + 1), bnd,
-          nact, tb, bands[0], bands[1], queues + 5, c4);
+          nact, tb, bands[0], bands[1], bands[2], queues + 5, c4);
       check_launch();
       c->launched();
     }

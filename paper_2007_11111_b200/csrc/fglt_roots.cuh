@@ -318,22 +318,24 @@ constexpr int kC4BlockThreads = FGLT_C4B_THREADS;  // class-4 block (one 128 KB 
 // Dense tiles use counters as narrow as the target's degree allows: L[w] <=
 // deg(w) (each wedge into w has a distinct middle vertex v in N(w)), and the
 // active ids are in ascending degree, so ids [0, b4) (degree <= 15) get 4-bit
-// counters, [b4, b8) (degree <= 255) 8-bit ones, and the rest 16 bits (32
-// when |N-(u)| >= 65536). Tiles never straddle a band: kC4TileBytes hold
-// 2 x kC4TileBytes ids in the 4-bit band, kC4TileBytes in the 8-bit band and
-// kC4Tile32 above (dense_tiles() builds the same boundaries on the host).
-__host__ __device__ inline void dense_span(u64 u, u64 b4, u64 b8, bool pack, u64 tile_bytes,
+// counters, [b4, b8) (degree <= 255) 8-bit, [b8, b16) (degree <= 65535)
+// 16-bit and the few ids above b16 32-bit ones. Tiles never straddle a band:
+// a tile of T bytes holds 2T ids in the 4-bit band, T in the 8-bit band, T/2
+// in the 16-bit band and T/4 above (the host builds the same boundaries).
+// Roots u <= b16 never meet a 32-bit band (PACK kernels).
+__host__ __device__ inline void dense_span(u64 u, u64 b4, u64 b8, u64 b16, u64 tile_bytes,
                                            u64* tiles, u64* bytes) {
   const u64 nib = u < b4 ? u : b4;
   const u64 byt = u > b4 ? (u < b8 ? u : b8) - b4 : 0;
-  const u64 rest = u > b8 ? u - b8 : 0;
-  const u64 t4 = 2 * tile_bytes, t8 = tile_bytes, t32 = tile_bytes / 4;
-  *tiles = (nib + t4 - 1) / t4 + (byt + t8 - 1) / t8 + (rest + t32 - 1) / t32;
-  *bytes = (nib + 1) / 2 + byt + rest * (pack ? 2 : 4);
+  const u64 sht = u > b8 ? (u < b16 ? u : b16) - b8 : 0;
+  const u64 rest = u > b16 ? u - b16 : 0;
+  const u64 t4 = 2 * tile_bytes, t8 = tile_bytes, t16 = tile_bytes / 2, t32 = tile_bytes / 4;
+  *tiles = (nib + t4 - 1) / t4 + (byt + t8 - 1) / t8 + (sht + t16 - 1) / t16 + (rest + t32 - 1) / t32;
+  *bytes = (nib + 1) / 2 + byt + 2 * sht + 4 * rest;
 }
 
 __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
-                           const u64* __restrict__ wc, int u0, int u1, int b4, int b8,
+                           const u64* __restrict__ wc, int u0, int u1, int b4, int b8, int b16,
                            u64* __restrict__ cls, u64* __restrict__ parts, int force_cls,
                            int force_parts) {
   for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1;
@@ -354,10 +356,10 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       const u64 nq = (u64)(split[u] - rp[u]);
       P = (w + kC4HashFill - 1) / kC4HashFill;
       const u64 cost_hash = FGLT_HASH_WEIGHT * (P * (w + (1ull << kC4HashLog)) + w);
-      const bool pack = nq < 65536;
+      const bool pack = u <= b16;  // no 32-bit band below u
       u64 tiles, bytes, tiles_s, bytes_s;
-      dense_span((u64)u, (u64)b4, (u64)b8, pack, kC4TileBytes, &tiles, &bytes);
-      dense_span((u64)u, (u64)b4, (u64)b8, pack, kC4TileBytesS, &tiles_s, &bytes_s);
+      dense_span((u64)u, (u64)b4, (u64)b8, (u64)b16, kC4TileBytes, &tiles, &bytes);
+      dense_span((u64)u, (u64)b4, (u64)b8, (u64)b16, kC4TileBytesS, &tiles_s, &bytes_s);
       const u64 cost_dense = bytes / 8 + tiles * (FGLT_TILE_FIXED + FGLT_ROW_TILE * nq) + 2 * w;
       // small tiles only for roots that need few of them: with many tiles per
       // root the per-tile row setup and tail imbalance outweigh the overlap
@@ -377,7 +379,7 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
       // external numbering: 2 hash passes, 3 packed tiles, 4 32-bit tiles,
       // 5 small packed tiles
       c = force_cls == 5 ? 7 : (u64)force_cls + 2;
-      if ((c == 5 || c == 7) && nq >= 65536) c = 6;
+      if ((c == 5 || c == 7) && u > b16) c = 6;
       if (c == 4) {
         P = (w + kC4HashFill - 1) / kC4HashFill;
         if (force_parts > 0) P = (u64)force_parts;
@@ -726,10 +728,10 @@ __global__ void k_tile_bounds(const int* __restrict__ rp, const int* __restrict_
 }
 
 // Degree bands of the active range (ids ascending in degree): out[0] = first
-// id with degree > 15, out[1] = first id with degree > 255.
+// id with degree > 15, out[1] > 255, out[2] > 65535.
 __global__ void k_degree_bands(const int* __restrict__ rp, int nact, int* __restrict__ out) {
-  if (threadIdx.x >= 2 || blockIdx.x) return;
-  const int lim = threadIdx.x == 0 ? 15 : 255;
+  if (threadIdx.x >= 3 || blockIdx.x) return;
+  const int lim = threadIdx.x == 0 ? 15 : threadIdx.x == 1 ? 255 : 65535;
   int lo = 0, hi = nact;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
@@ -761,7 +763,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, int* __restrict__ cursor,
            long long cursor_stride, const int* __restrict__ bnd, long long bnd_stride,
-           const int* __restrict__ tb, int b4, int b8, int* __restrict__ next_root,
+           const int* __restrict__ tb, int b4, int b8, int b16, int* __restrict__ next_root,
            u64* __restrict__ c4) {
   // roots are sorted by work (largest first) and handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -828,7 +830,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     u64 acc = 0;
     for (int t = 0; t < ntiles; ++t) {
       const int lo = tb[t], hi = min(tb[t + 1], u);
-      sh = lo < b4 ? 3 : lo < b8 ? 2 : (PACK ? 1 : 0);
+      sh = lo < b4 ? 3 : lo < b8 ? 2 : lo < b16 ? 1 : 0;  // PACK roots never reach b16
       const int words = (hi - lo + (1 << sh) - 1) >> sh;
       const long long kb_lo = t, kb_hi = t + 1;
       {
