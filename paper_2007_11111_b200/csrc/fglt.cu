@@ -575,7 +575,12 @@ __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict
   }
 }
 
-constexpr u64 kRootThr[] = {(u64)kSmallS, 128, 256, 512, (u64)kBlockS};
+#ifndef FGLT_BIN1
+#define FGLT_BIN1 128  // |S| cap of the 64-thread root bin
+#define FGLT_BIN2 256  // |S| cap of the 128-thread root bin
+#define FGLT_BIN3 512
+#endif
+constexpr u64 kRootThr[] = {(u64)kSmallS, FGLT_BIN1, FGLT_BIN2, FGLT_BIN3, (u64)kBlockS};
 
 __global__ void k_gather_keys(const int* __restrict__ list, int cnt, const u64* __restrict__ w,
                               u64* __restrict__ keys) {
