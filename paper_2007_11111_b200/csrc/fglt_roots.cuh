@@ -309,6 +309,9 @@ constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many w
 #ifndef FGLT_PROBE_NOCUT
 #define FGLT_PROBE_NOCUT 0  // probe lists up to this long are probed whole (no cut search)
 #endif
+#ifndef FGLT_PROBE_NOCUT_WARP
+#define FGLT_PROBE_NOCUT_WARP 0  // the same for warp roots (|S| <= 32)
+#endif
 #ifndef FGLT_QUADS
 #define FGLT_QUADS 2
 #endif
@@ -1236,7 +1239,7 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
       x = sS[lane];
       st = split[x];
       const int full = rp[x + 1];  // short lists: probe whole, skip the dependent search
-      len = (full - st <= FGLT_PROBE_NOCUT ? full : lower_bound_i32(ci, st, full, smax + 1)) - st;
+      len = (full - st <= FGLT_PROBE_NOCUT_WARP ? full : lower_bound_i32(ci, st, full, smax + 1)) - st;
       pairs = hub != nullptr && x >= hb && (hub_force || s - 1 - lane < len);
       if (pairs) len = 0;
     }
