@@ -990,8 +990,12 @@ void epilogue(fglt_ctx* c, int64_t v0, int64_t v1, u64* raw, u64* net) {
   in.c4 = P.c4 ? c->V(V_C4) : nullptr;
   in.d13 = P.d13 ? c->V(V_D13) : nullptr;
   in.d15 = P.d15 ? c->V(V_D15) : nullptr;
-  k_epilogue<<<c->grid(v1 - v0, 128), 128, 0, c->stream>>>(in, c->d_dict, (int)v0, (int)v1,
-                                                         c->lenient, raw, net, c->d_small);
+  if (v0 == 0 && v1 == c->n && c->perm && c->inv)  // whole table: walk rows in vector order
+    k_epilogue_rank<<<c->grid(v1, kEpilogueThreads), kEpilogueThreads, 0, c->stream>>>(
+        in, c->perm, c->d_dict, (int)v1, c->lenient, raw, net, c->d_small);
+  else
+    k_epilogue<<<c->grid(v1 - v0, 128), 128, 0, c->stream>>>(in, c->d_dict, (int)v0, (int)v1,
+                                                           c->lenient, raw, net, c->d_small);
   check_launch();
   c->launched();
 }

@@ -2029,6 +2029,82 @@ __device__ __forceinline__ void offer_err(u64* err, int stage, long long v, int 
   atomicMin(err, key);
 }
 
+// One vertex's raw columns (kernels.cpp:384-412) and their exact net
+// back-substitution (conversion.cpp:80-116); v = ORIGINAL id (error order),
+// r = its row in the vector arrays.
+__device__ __forceinline__ void epi_row(const EpilogueIn& in, const DictInfo& D, int v, int r,
+                                        int lenient, bool want_net, u64* __restrict__ err,
+                                        u64 (&rw)[16], u64 (&nt)[16]) {
+  const int k = D.k;
+  const unsigned m = D.mask;
+  const u64 d = (u64)(in.rp[r + 1] - in.rp[r]);
+  u64 col[16];
+  u64 t;
+  col[0] = 1;
+  col[1] = d;
+  col[2] = (m & (1u << 2) || m & (1u << 5) || m & (1u << 6)) && in.p2 ? in.p2[r] : 0;
+  // col 3: choose2(p1), checked (types.hpp:84-88)
+  col[3] = 0;
+  if (m & (1u << 3) && d >= 2) {
+    if (mul_ov(d, d - 1, &t)) offer_err(err, 1, v, 0, 3);
+    col[3] = t / 2;
+  }
+  const u64 c3v = in.c3 ? in.c3[r] : 0;
+  col[4] = c3v;
+  col[5] = in.p3 ? in.p3[r] : 0;
+  col[6] = 0;
+  if (m & (1u << 6)) {
+    if (mul_ov(col[2], sat_sub(d, 1), &t)) offer_err(err, 2, v, 0, 6);
+    col[6] = sat_sub(t, 2 * c3v);
+  }
+  col[7] = in.d7 ? in.d7[r] : 0;
+  col[8] = 0;
+  if (m & (1u << 8) && d >= 3) {  // choose3: unchecked d(d-1)/2, checked *(d-2)
+    if (mul_ov(d * (d - 1) / 2, d - 2, &t)) offer_err(err, 4, v, 0, 8);
+    col[8] = t / 3;
+  }
+  col[9] = in.d9 ? in.d9[r] : 0;
+  col[10] = in.d10 ? in.d10[r] : 0;
+  col[11] = 0;
+  if (m & ((1u << 9) | (1u << 10) | (1u << 11))) {
+    if (mul_ov(sat_sub(d, 2), c3v, &t)) offer_err(err, 5, v, 0, 11);
+    col[11] = t;
+  }
+  col[12] = in.c4 ? in.c4[r] : 0;
+  col[13] = in.d13 ? in.d13[r] : 0;
+  col[14] = in.d14 ? in.d14[r] : 0;
+  col[15] = in.d15 ? in.d15[r] : 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (i < k) rw[i] = col[D.ids[i]];
+  bool stop = !want_net;  // raw only: the conversion never runs
+  for (int rr = k - 1; rr >= 0; --rr) {
+    u64 absorbed = 0;
+    nt[rr] = 0;
+    if (stop) continue;
+    for (int j = 0; j < D.ntail[rr]; ++j) {
+      u64 prod;
+      if (mul_ov((u64)D.tail_coef[rr][j], nt[D.tail_col[rr][j]], &prod) ||
+          add_ov(absorbed, prod, &absorbed)) {
+        offer_err(err, 6, v, 0, D.ids[rr]);
+        stop = true;
+        break;
+      }
+    }
+    if (stop) continue;
+    if (absorbed > rw[rr]) {
+      if (!lenient) {
+        offer_err(err, 6, v, 1, D.ids[rr]);
+        stop = true;
+        continue;
+      }
+      nt[rr] = 0;
+    } else {
+      nt[rr] = rw[rr] - absorbed;
+    }
+  }
+}
+
 constexpr int kEpilogueThreads = 128;
 
 __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue(EpilogueIn in, const DictInfo* __restrict__ dict, int v0, int v1,
@@ -2060,75 +2136,44 @@ __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue(EpilogueIn in, co
     u64 rw[16], nt[16];
     if (v < v1) {
     const int r = in.inv ? in.inv[v] : v;
-    const u64 d = (u64)(in.rp[r + 1] - in.rp[r]);
-    u64 col[16];
-    u64 t;
-    col[0] = 1;
-    col[1] = d;
-    col[2] = (m & (1u << 2) || m & (1u << 5) || m & (1u << 6)) && in.p2 ? in.p2[r] : 0;
-    // col 3: choose2(p1), checked (types.hpp:84-88)
-    col[3] = 0;
-    if (m & (1u << 3) && d >= 2) {
-      if (mul_ov(d, d - 1, &t)) offer_err(err, 1, v, 0, 3);
-      col[3] = t / 2;
-    }
-    const u64 c3v = in.c3 ? in.c3[r] : 0;
-    col[4] = c3v;
-    col[5] = in.p3 ? in.p3[r] : 0;
-    col[6] = 0;
-    if (m & (1u << 6)) {
-      if (mul_ov(col[2], sat_sub(d, 1), &t)) offer_err(err, 2, v, 0, 6);
-      col[6] = sat_sub(t, 2 * c3v);
-    }
-    col[7] = in.d7 ? in.d7[r] : 0;
-    col[8] = 0;
-    if (m & (1u << 8) && d >= 3) {  // choose3: unchecked d(d-1)/2, checked *(d-2)
-      if (mul_ov(d * (d - 1) / 2, d - 2, &t)) offer_err(err, 4, v, 0, 8);
-      col[8] = t / 3;
-    }
-    col[9] = in.d9 ? in.d9[r] : 0;
-    col[10] = in.d10 ? in.d10[r] : 0;
-    col[11] = 0;
-    if (m & ((1u << 9) | (1u << 10) | (1u << 11))) {
-      if (mul_ov(sat_sub(d, 2), c3v, &t)) offer_err(err, 5, v, 0, 11);
-      col[11] = t;
-    }
-    col[12] = in.c4 ? in.c4[r] : 0;
-    col[13] = in.d13 ? in.d13[r] : 0;
-    col[14] = in.d14 ? in.d14[r] : 0;
-    col[15] = in.d15 ? in.d15[r] : 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i < k) rw[i] = col[D.ids[i]];
-    bool stop = net == nullptr;  // raw only: the conversion never runs
-    for (int rr = k - 1; rr >= 0; --rr) {
-      u64 absorbed = 0;
-      nt[rr] = 0;
-      if (stop) continue;
-      for (int j = 0; j < D.ntail[rr]; ++j) {
-        u64 prod;
-        if (mul_ov((u64)D.tail_coef[rr][j], nt[D.tail_col[rr][j]], &prod) ||
-            add_ov(absorbed, prod, &absorbed)) {
-          offer_err(err, 6, v, 0, D.ids[rr]);
-          stop = true;
-          break;
-        }
-      }
-      if (stop) continue;
-      if (absorbed > rw[rr]) {
-        if (!lenient) {
-          offer_err(err, 6, v, 1, D.ids[rr]);
-          stop = true;
-          continue;
-        }
-        nt[rr] = 0;
-      } else {
-        nt[rr] = rw[rr] - absorbed;
-      }
-    }
+    epi_row(in, D, v, r, lenient, net != nullptr, err, rw, nt);
     }
     if (raw) store_rows(rw, raw);
     if (net) store_rows(nt, net);
+  }
+}
+
+// Whole-table variant (rows [0, n)): walks the vector rows r in order (every
+// vector read coalesced) and writes each row to its original id perm[r] as
+// whole 16-byte units (a full 128-byte line per table when k = 16).
+__global__ void __launch_bounds__(kEpilogueThreads) k_epilogue_rank(
+    EpilogueIn in, const int* __restrict__ perm, const DictInfo* __restrict__ dict, int n,
+    int lenient, u64* __restrict__ raw, u64* __restrict__ net, u64* __restrict__ err) {
+  __shared__ DictInfo D;
+  if (threadIdx.x == 0) D = *dict;
+  __syncthreads();
+  const int k = D.k;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int v = perm[r];
+    u64 rw[16], nt[16];
+    epi_row(in, D, v, r, lenient, net != nullptr, err, rw, nt);
+    const long long o = (long long)v * k;
+    const bool vec = (k & 1) == 0 &&
+                     ((reinterpret_cast<unsigned long long>(raw) |
+                       reinterpret_cast<unsigned long long>(net)) & 15ull) == 0;
+    if (vec) {
+      if (raw)
+        for (int i = 0; i < k; i += 2)
+          *reinterpret_cast<ulonglong2*>(raw + o + i) = make_ulonglong2(rw[i], rw[i + 1]);
+      if (net)
+        for (int i = 0; i < k; i += 2)
+          *reinterpret_cast<ulonglong2*>(net + o + i) = make_ulonglong2(nt[i], nt[i + 1]);
+    } else {
+      if (raw)
+        for (int i = 0; i < k; ++i) raw[o + i] = rw[i];
+      if (net)
+        for (int i = 0; i < k; ++i) net[o + i] = nt[i];
+    }
   }
 }
 
