@@ -109,6 +109,28 @@ def ncu_summary(cfg: int):
         return json.load(f)
 
 
+# SURVEY.md §8(d) terms of B_alg charged to each reference step (bytes)
+PHASE_BYTES = {
+    "four-cycle rows": lambda nnz, W: 4 * nnz + 4 * W,   # two-hop base col + index reads
+    "triangles": lambda nnz, W: 8 * nnz + 4 * W,         # edge pass col + C3 write + intersections
+    "diamond rows": lambda nnz, W: 4 * W,                # C3 values read alongside (D4 term)
+}
+
+
+def dominant_phase(dom, step_ms: float, nnz: int, W: int, peak_gbs: float):
+    """The longest reference step, timed live (CUDA events on the launch
+    stream), with its share of B_alg and the implied fraction of the HBM
+    roofline (work-reduced vs the paper formulation, like the step total)."""
+    name, ms = dom
+    out = {"name": name, "ms": ms, "share": ms / step_ms if ms else None}
+    f = PHASE_BYTES.get(name)
+    if f and ms:
+        b = f(nnz, W)
+        out.update({"alg_bytes": b, "achieved_gbs": b / (ms * 1e-3) / 1e9,
+                    "frac": b / (ms * 1e-3) / 1e9 / peak_gbs})
+    return out
+
+
 def dominant_kernel(summary, step_ms: float, peak_gbs: float):
     """The top kernel of the ncu launch list: its share of the step (ncu's
     per-launch times are cold-cache and serialised, so the share, not the
@@ -392,8 +414,7 @@ def main():
                      "note": "work-reduced vs paper formulation: degree-oriented enumeration "
                              "does less than the 12W index/value traffic the model charges",
                      "peak_kind": peak_kind, "traffic_source": traffic_src,
-                     "dominant_phase": {"name": dom[0], "ms": dom[1],
-                                        "share": dom[1] / t_ms if dom[1] else None},
+                     "dominant_phase": dominant_phase(dom, t_ms, nnz, W, peak),
                      "dominant_kernel": dominant_kernel(summ, t_ms, peak),
                      "measured_dram_gbs": (traffic / (t_ms * 1e-3) / 1e9) if traffic else None,
                      "phases_ms": phases},
