@@ -496,3 +496,34 @@ def test_degenerate_shapes(ctx):
     for rp, ci in cases:
         check_same(ctx, rp, ci)
         check_same(ctx, rp, ci, mask=_capi.dict_mask([12, 13, 15]))
+
+
+def test_randomised_paths_fuzz():
+    """Seeded random graphs under random combinations of the internal-path
+    hooks (4-cycle class, root bin, hub rows, triangle list mode) against the
+    oracle: interactions between paths, not just each path alone."""
+    rng = np.random.default_rng(2026)
+    c = _capi.Context(0)
+    for it in range(120):
+        kind = it % 4
+        if kind == 0:
+            rp, ci = graphs.rmat(int(rng.integers(8, 13)), int(rng.integers(4, 20)),
+                                 seed=int(rng.integers(1, 1000)))
+        elif kind == 1:
+            rp, ci = gu.er(int(rng.integers(50, 400)), float(rng.uniform(0.02, 0.3)),
+                           int(rng.integers(1, 1000)))
+        elif kind == 2:
+            rp, ci = graphs.sbm(int(rng.integers(8, 64)), int(rng.integers(8, 64)),
+                                float(rng.uniform(0.1, 0.6)), float(rng.uniform(0.5, 4.0)),
+                                int(rng.integers(1, 1000)))
+        else:
+            rp, ci = gu.regular(int(rng.integers(100, 600)), int(rng.integers(3, 30)),
+                                int(rng.integers(1, 1000)))
+        c.set_debug(_capi.DEBUG_C4_CLASS, int(rng.choice([0, 0, 2, 3, 4, 5])))
+        c.set_debug(_capi.DEBUG_C4_PARTS, int(rng.choice([0, 1, 2, 5])))
+        c.set_debug(_capi.DEBUG_ROOTS_BIN, int(rng.choice([0, 0, 1, 2, 3, 4, 5])))
+        c.set_debug(_capi.DEBUG_HUB, int(rng.choice([0, 1, 2])))
+        c.set_debug(_capi.DEBUG_TRILIST, int(rng.choice([0, 0, 1, 2])))
+        mask = 0xFFFF if it % 3 else int(rng.integers(0, 1 << 16)) | 3
+        check_same(c, rp, ci, mask=mask, lenient=True, d15_mode=1)
+    c.close()
