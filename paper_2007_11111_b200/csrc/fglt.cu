@@ -34,26 +34,6 @@ using namespace fglt;
 
 namespace {
 
-// Net-to-raw coefficients U16 (Table 2; reference encoding
-// proj/src/conversion.cpp:14-32). Rows = raw graphlet, cols = net graphlet.
-const unsigned char kU16[16][16] = {
-    {1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 1, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 1, 0, 2, 4, 2, 6},
-    {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 2, 2, 2, 4, 6},
-    {0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 2, 1, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 1, 1},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 0, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 2, 6},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
-};
 
 #ifndef FGLT_TL_MEM_FRAC
 #define FGLT_TL_MEM_FRAC 0.70  // triangle-list pool: at most this share of the free HBM
@@ -991,8 +971,12 @@ void epilogue(fglt_ctx* c, int64_t v0, int64_t v1, u64* raw, u64* net) {
   in.d13 = P.d13 ? c->V(V_D13) : nullptr;
   in.d15 = P.d15 ? c->V(V_D15) : nullptr;
   if (v0 == 0 && v1 == c->n && c->perm && c->inv)  // whole table: walk rows in vector order
-    k_epilogue_rank<<<c->grid(v1, kEpilogueThreads), kEpilogueThreads, 0, c->stream>>>(
-        in, c->perm, c->d_dict, (int)v1, c->lenient, raw, net, c->d_small);
+    if (c->dict.mask == 0xFFFFu)
+      k_epilogue_rank<true><<<c->grid(v1, kEpilogueThreads), kEpilogueThreads, 0, c->stream>>>(
+          in, c->perm, c->d_dict, (int)v1, c->lenient, raw, net, c->d_small);
+    else
+      k_epilogue_rank<false><<<c->grid(v1, kEpilogueThreads), kEpilogueThreads, 0, c->stream>>>(
+          in, c->perm, c->d_dict, (int)v1, c->lenient, raw, net, c->d_small);
   else
     k_epilogue<<<c->grid(v1 - v0, 128), 128, 0, c->stream>>>(in, c->d_dict, (int)v0, (int)v1,
                                                            c->lenient, raw, net, c->d_small);

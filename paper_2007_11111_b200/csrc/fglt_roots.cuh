@@ -2018,6 +2018,54 @@ __device__ __forceinline__ bool add_ov(u64 a, u64 b, u64* r) {
   return *r < a;
 }
 
+// Net-to-raw coefficients U16 (Table 2; reference encoding
+// proj/src/conversion.cpp:14-32). Rows = raw graphlet, cols = net graphlet.
+constexpr unsigned char kU16[16][16] = {
+    {1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 1, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
+    {0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 1, 0, 2, 4, 2, 6},
+    {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 2, 2, 2, 4, 6},
+    {0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 2, 1, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 1, 1},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 0, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 2, 6},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 3},
+    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
+};
+
+// U16 coefficient (r, c) as a compile-time constant on host and device:
+// row r packed 3 bits per column.
+__host__ __device__ constexpr unsigned long long u16_row_packed(int r) {
+  switch (r) {
+    case 0: return 0x000000000001ull;
+    case 1: return 0x000000000008ull;
+    case 2: return 0x000000002040ull;
+    case 3: return 0x000000001200ull;
+    case 4: return 0x000000001000ull;
+    case 5: return 0xca2050008000ull;
+    case 6: return 0xd12440040000ull;
+    case 7: return 0x650048200000ull;
+    case 8: return 0x240201000000ull;
+    case 9: return 0x610008000000ull;
+    case 10: return 0xc90040000000ull;
+    case 11: return 0x680200000000ull;
+    case 12: return 0x649000000000ull;
+    case 13: return 0x608000000000ull;
+    case 14: return 0x640000000000ull;
+    case 15: return 0x200000000000ull;
+    default: return 0ull;
+  }
+}
+__host__ __device__ constexpr unsigned u16_coef(int r, int c) {
+  return (unsigned)((u16_row_packed(r) >> (3 * c)) & 7ull);
+}
+
 struct EpilogueIn {
   const int* rp;   // graph the vectors are indexed by (relabelled or original)
   const int* inv;  // original id -> row of that graph; null = identity
@@ -2032,6 +2080,84 @@ __device__ __forceinline__ void offer_err(u64* err, int stage, long long v, int 
 // One vertex's raw columns (kernels.cpp:384-412) and their exact net
 // back-substitution (conversion.cpp:80-116); v = ORIGINAL id (error order),
 // r = its row in the vector arrays.
+__device__ __forceinline__ void epi_row_full(const EpilogueIn& in, const DictInfo& D, int v, int r,
+                                        int lenient, bool want_net, u64* __restrict__ err,
+                                        u64 (&rw)[16], u64 (&nt)[16]) {
+  const int k = D.k;
+  const unsigned m = D.mask;
+  const u64 d = (u64)(in.rp[r + 1] - in.rp[r]);
+  u64 col[16];
+  u64 t;
+  col[0] = 1;
+  col[1] = d;
+  col[2] = (m & (1u << 2) || m & (1u << 5) || m & (1u << 6)) && in.p2 ? in.p2[r] : 0;
+  // col 3: choose2(p1), checked (types.hpp:84-88)
+  col[3] = 0;
+  if (m & (1u << 3) && d >= 2) {
+    if (mul_ov(d, d - 1, &t)) offer_err(err, 1, v, 0, 3);
+    col[3] = t / 2;
+  }
+  const u64 c3v = in.c3 ? in.c3[r] : 0;
+  col[4] = c3v;
+  col[5] = in.p3 ? in.p3[r] : 0;
+  col[6] = 0;
+  if (m & (1u << 6)) {
+    if (mul_ov(col[2], sat_sub(d, 1), &t)) offer_err(err, 2, v, 0, 6);
+    col[6] = sat_sub(t, 2 * c3v);
+  }
+  col[7] = in.d7 ? in.d7[r] : 0;
+  col[8] = 0;
+  if (m & (1u << 8) && d >= 3) {  // choose3: unchecked d(d-1)/2, checked *(d-2)
+    if (mul_ov(d * (d - 1) / 2, d - 2, &t)) offer_err(err, 4, v, 0, 8);
+    col[8] = t / 3;
+  }
+  col[9] = in.d9 ? in.d9[r] : 0;
+  col[10] = in.d10 ? in.d10[r] : 0;
+  col[11] = 0;
+  if (m & ((1u << 9) | (1u << 10) | (1u << 11))) {
+    if (mul_ov(sat_sub(d, 2), c3v, &t)) offer_err(err, 5, v, 0, 11);
+    col[11] = t;
+  }
+  col[12] = in.c4 ? in.c4[r] : 0;
+  col[13] = in.d13 ? in.d13[r] : 0;
+  col[14] = in.d14 ? in.d14[r] : 0;
+  col[15] = in.d15 ? in.d15[r] : 0;
+  // full dictionary: identity column map and the constant U16, fully
+  // unrolled so every table stays in registers
+#pragma unroll
+  for (int i = 0; i < 16; ++i) rw[i] = col[i];
+  bool stop = !want_net;
+#pragma unroll
+  for (int rr = 15; rr >= 0; --rr) {
+    nt[rr] = 0;
+    if (stop) continue;
+    u64 absorbed = 0;
+    bool bad = false;
+#pragma unroll
+    for (int cc = rr + 1; cc < 16; ++cc) {
+      if (u16_coef(rr, cc) == 0) continue;
+      u64 prod;
+      if (!bad && (mul_ov((u64)u16_coef(rr, cc), nt[cc], &prod) || add_ov(absorbed, prod, &absorbed)))
+        bad = true;
+    }
+    if (bad) {
+      offer_err(err, 6, v, 0, rr);
+      stop = true;
+      continue;
+    }
+    if (absorbed > rw[rr]) {
+      if (!lenient) {
+        offer_err(err, 6, v, 1, rr);
+        stop = true;
+        continue;
+      }
+      nt[rr] = 0;
+    } else {
+      nt[rr] = rw[rr] - absorbed;
+    }
+  }
+}
+
 __device__ __forceinline__ void epi_row(const EpilogueIn& in, const DictInfo& D, int v, int r,
                                         int lenient, bool want_net, u64* __restrict__ err,
                                         u64 (&rw)[16], u64 (&nt)[16]) {
@@ -2146,6 +2272,7 @@ __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue(EpilogueIn in, co
 // Whole-table variant (rows [0, n)): walks the vector rows r in order (every
 // vector read coalesced) and writes each row to its original id perm[r] as
 // whole 16-byte units (a full 128-byte line per table when k = 16).
+template <bool kFull>
 __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue_rank(
     EpilogueIn in, const int* __restrict__ perm, const DictInfo* __restrict__ dict, int n,
     int lenient, u64* __restrict__ raw, u64* __restrict__ net, u64* __restrict__ err) {
@@ -2155,9 +2282,28 @@ __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue_rank(
   const int k = D.k;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const int v = perm[r];
+    const long long o = (long long)v * k;
+    if (kFull) {  // full dictionary: all tables in registers, 16-byte stores
+      u64 rw[16], nt[16];
+      epi_row_full(in, D, v, r, lenient, net != nullptr, err, rw, nt);
+      if (((reinterpret_cast<unsigned long long>(raw) |
+            reinterpret_cast<unsigned long long>(net)) & 15ull) == 0) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          if (raw) *reinterpret_cast<ulonglong2*>(raw + o + i) = make_ulonglong2(rw[i], rw[i + 1]);
+          if (net) *reinterpret_cast<ulonglong2*>(net + o + i) = make_ulonglong2(nt[i], nt[i + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (raw) raw[o + i] = rw[i];
+          if (net) net[o + i] = nt[i];
+        }
+      }
+      continue;
+    }
     u64 rw[16], nt[16];
     epi_row(in, D, v, r, lenient, net != nullptr, err, rw, nt);
-    const long long o = (long long)v * k;
     const bool vec = (k & 1) == 0 &&
                      ((reinterpret_cast<unsigned long long>(raw) |
                        reinterpret_cast<unsigned long long>(net)) & 15ull) == 0;
