@@ -1696,9 +1696,11 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
           flush(c0);
         }
       }
-      __syncthreads();  // f_* are rewritten below
+      // barrier (f_* are rewritten below) that also tells whether any member
+      // of this chunk takes the hub-row pair path
+      const int any_pairs = __syncthreads_or(pairs ? 1 : 0);
       tl_publish();
-      if (hub == nullptr) continue;
+      if (hub == nullptr || !any_pairs) continue;
       // pair rows
       {
         f_sa[threadIdx.x] = x;
