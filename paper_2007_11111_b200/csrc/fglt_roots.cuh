@@ -301,7 +301,10 @@ constexpr int kC4TileBytesS = 98304;                    // small: 96 KB tiles
 #endif
 constexpr int kC4Tile16 = kC4TileBytes / 2; // ids per packed tile
 constexpr int kC4Tile32 = kC4TileBytes / 4; // ids per 32-bit tile
-constexpr int kC4Long = 48;                 // rows at least this long: flattened batches
+#ifndef FGLT_C4_LONG
+#define FGLT_C4_LONG 16
+#endif
+constexpr int kC4Long = FGLT_C4_LONG;       // rows at least this long: flattened batches
 #ifndef FGLT_GIANT
 #define FGLT_GIANT 512
 #endif
