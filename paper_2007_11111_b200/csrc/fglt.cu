@@ -674,7 +674,7 @@ void roots_pass(fglt_ctx* c) {
     RootsLayout L;
     L.s_cap = global ? (int)c->maxout : (int)std::min<u64>(kRootThr[b], std::max<u64>(c->maxout, 33));
     L.hlog = 6;
-    while ((1 << L.hlog) < 4 * L.s_cap) ++L.hlog;
+    while ((1 << L.hlog) < FGLT_ROOT_HASH_FACTOR * L.s_cap) ++L.hlog;
     L.hcap = 1 << L.hlog;
     // block size follows |S|: 64 threads for |S| <= 128, 128 for <= 256, else 256
     const int nt = global ? kRootsThreads : (b == 1 ? 64 : b == 2 ? 128 : kRootsThreads);

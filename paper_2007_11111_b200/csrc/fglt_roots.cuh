@@ -1433,8 +1433,15 @@ __device__ __forceinline__ int s_hash_find(const int* keys, const unsigned short
 // x+32+32k; low 32 bits = adjacency, high 32 bits = number of N+(x) entries
 // before the word (so the CSR position of (x, y) is split[x] + high +
 // popc(low below y)). Rows are ceil((R-1-i)/32) words, packed back to back.
-constexpr int kHubMax = 16384;  // R cap: R^2/8 bytes of rows (32 MB), L2-resident
-constexpr int kHubMinDegree = 128;  // hub rows only when the R-th largest degree reaches this
+#ifndef FGLT_HUB_MAX
+#define FGLT_HUB_MAX 49152
+#define FGLT_HUB_MIN_DEG 128
+#endif
+#ifndef FGLT_ROOT_HASH_FACTOR
+#define FGLT_ROOT_HASH_FACTOR 4  // root hash slots >= this x |S|
+#endif
+constexpr int kHubMax = FGLT_HUB_MAX;  // R cap: R^2/8 bytes of rows (288 MB at 48K)
+constexpr int kHubMinDegree = FGLT_HUB_MIN_DEG;  // hub rows only when the R-th largest degree reaches this
 
 __global__ void k_hub_words(int R, int* __restrict__ w) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= R; i += gridDim.x * blockDim.x)
@@ -1529,7 +1536,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
     const int stride = bitmap_stride(nw);
     const int nw64 = (nw + 1) >> 1;
     int hlog = 6;
-    while ((1 << hlog) < 4 * s) ++hlog;
+    while ((1 << hlog) < FGLT_ROOT_HASH_FACTOR * s) ++hlog;
     const int hcap = 1 << hlog;
     FGLT_BOUNDS(s <= L.s_cap, "s", s, L.s_cap);
     FGLT_BOUNDS(hlog <= L.hlog, "hlog", hlog, L.hlog);
