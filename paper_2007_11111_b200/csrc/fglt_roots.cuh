@@ -315,6 +315,10 @@ constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many w
 #ifndef FGLT_PROBE_NOCUT_WARP
 #define FGLT_PROBE_NOCUT_WARP 0  // the same for warp roots (|S| <= 32)
 #endif
+#ifndef FGLT_PAIR_W
+#define FGLT_PAIR_W 1   // relative cost of one hub-row pair test ...
+#define FGLT_PROBE_W 3  // ... and of one probed element (members choose the cheaper path)
+#endif
 #ifndef FGLT_QUADS
 #define FGLT_QUADS 2
 #endif
@@ -1243,7 +1247,8 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
       st = split[x];
       const int full = rp[x + 1];  // short lists: probe whole, skip the dependent search
       len = (full - st <= FGLT_PROBE_NOCUT_WARP ? full : lower_bound_i32(ci, st, full, smax + 1)) - st;
-      pairs = hub != nullptr && x >= hb && (hub_force || s - 1 - lane < len);
+      pairs = hub != nullptr && x >= hb &&
+              (hub_force || (s - 1 - lane) * FGLT_PAIR_W < len * FGLT_PROBE_W);
       if (pairs) len = 0;
     }
     int T;
@@ -1474,7 +1479,10 @@ __global__ void k_hub_rows(const int* __restrict__ ci, const int* __restrict__ s
 #define FGLT_K4_THREAD_NW 16  // G[S] rows of at most this many words: thread-per-member 4-cliques
 #endif
 constexpr int kRootsThreads = 256;  // block threads for |S| > 256 (smaller bins: 64, 128)
-constexpr int kPairsInFlight = 4;  // hub-row words in flight per lane
+#ifndef FGLT_PAIRS_IN_FLIGHT
+#define FGLT_PAIRS_IN_FLIGHT 4
+#endif
+constexpr int kPairsInFlight = FGLT_PAIRS_IN_FLIGHT;  // hub-row words in flight per lane
 
 template <bool kC3, bool kD13, bool kD15, bool kGlobal, int NT>
 __global__ void __launch_bounds__(NT)
@@ -1652,7 +1660,8 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         st = split[x];
         const int full = rp[x + 1];  // short lists: probe whole, skip the dependent search
         se = full - st <= FGLT_PROBE_NOCUT ? full : lower_bound_i32(ci, st, full, smax + 1);
-        pairs = hub != nullptr && x >= hb && (hub_force || (s - 1 - a_me) < se - st);
+        pairs = hub != nullptr && x >= hb &&
+                (hub_force || (s - 1 - a_me) * FGLT_PAIR_W < (se - st) * FGLT_PROBE_W);
       }
       // probe rows
       {
