@@ -555,6 +555,10 @@ __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict
   }
 }
 
+#ifndef FGLT_BIN1_NT
+#define FGLT_BIN1_NT 64   // block threads of root bin 1 (64, 128 or 256)
+#define FGLT_BIN2_NT 128  // ... and of bin 2
+#endif
 #ifndef FGLT_BIN1
 #define FGLT_BIN1 128  // |S| cap of the 64-thread root bin
 #define FGLT_BIN2 256  // |S| cap of the 128-thread root bin
@@ -677,7 +681,7 @@ void roots_pass(fglt_ctx* c) {
     while ((1 << L.hlog) < FGLT_ROOT_HASH_FACTOR * L.s_cap) ++L.hlog;
     L.hcap = 1 << L.hlog;
     // block size follows |S|: 64 threads for |S| <= 128, 128 for <= 256, else 256
-    const int nt = global ? kRootsThreads : (b == 1 ? 64 : b == 2 ? 128 : kRootsThreads);
+    const int nt = global ? kRootsThreads : (b == 1 ? FGLT_BIN1_NT : b == 2 ? FGLT_BIN2_NT : kRootsThreads);
     L.nwarps = nt / 32;
     L.stride_cap = bitmap_stride((L.s_cap + 31) / 32);
     size_t sm = L.bytes_core();
