@@ -555,6 +555,9 @@ __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict
   }
 }
 
+#ifndef FGLT_DLIST_NT
+#define FGLT_DLIST_NT 256  // block threads of the diamond-list kernel
+#endif
 #ifndef FGLT_BIN1_NT
 #define FGLT_BIN1_NT 64   // block threads of root bin 1 (64, 128 or 256)
 #define FGLT_BIN2_NT 128  // ... and of bin 2
@@ -758,7 +761,7 @@ void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
 // Diamonds of the listed roots (the rest take the probing pass).
 void diamond_list(fglt_ctx* c) {
   if (!c->tl.rec) return;
-  constexpr int NT = 256;
+  constexpr int NT = FGLT_DLIST_NT;
   const size_t sm = (size_t)std::min<u64>(std::max<u64>(c->maxout, 1), kTriListMaxS) * 8;
   set_smem(k_diamond_list<NT>, sm);
   int occ = 1;
