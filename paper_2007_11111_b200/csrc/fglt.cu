@@ -888,7 +888,8 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     // classes 5/6 (big tiles) and 7 (small tiles): banded tile starts
     // (dense_span) and the absolute tile boundaries of the active rows
     const long long nact = (long long)c->nact;
-    auto tiles_for = [&](long long tile_bytes, Buf tb_buf, Buf bnd_buf, int** bnd_out) -> int* {
+    auto tiles_for = [&](long long tile_bytes, Buf tb_buf, Buf bnd_buf, int** bnd_out,
+                         int* k_out) -> int* {
       std::vector<int> h{0};
       const long long t4 = 2 * tile_bytes, t8 = tile_bytes, t16 = tile_bytes / 2,
                       t32 = tile_bytes / 4;
@@ -901,6 +902,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         x = e;
       }
       const long long K = (long long)h.size() - 1;
+      *k_out = (int)K;
       int* tb = c->ensure<int>(tb_buf, h.size());
       CK(cudaMemcpyAsync(tb, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
       *bnd_out = nullptr;
@@ -915,22 +917,34 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     };
     if (cnt[4] > 0 || cnt[5] > 0) {
       int* bnd = nullptr;
-      int* tb = tiles_for(kC4TileBytes, B_TB, B_TBND, &bnd);
+      int K = 0;
+      int* tb = tiles_for(kC4TileBytes, B_TB, B_TBND, &bnd, &K);
       for (int bb = 4; bb <= 5; ++bb) {
         if (cnt[bb] == 0) continue;
         const size_t sm = kC4TileBytes;
-        const int g = std::min(cnt[bb], c->sms * (1024 / kC4DenseThreads));
+        // 32-bit-band roots (the few ranked above degree 65535) are huge: hand
+        // out (root, tile) items so they spread over every SM
+        const int skt = (bb == 5 && bnd) ? K : 0;
+        const int g = skt ? c->sms * (1024 / kC4DenseThreads)
+                          : std::min(cnt[bb], c->sms * (1024 / kC4DenseThreads));
         int* cur = c->ensure<int>(B_CURSOR, 2 * (size_t)g * (size_t)(c->dmax + 1));
         if (bb == 4) {
           set_smem(k_c4_dense<true, kC4DenseThreads>, sm);
           k_c4_dense<true, kC4DenseThreads><<<g, kC4DenseThreads, sm, c->stream>>>(
               c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
-              bnd, nact, tb, bands[0], bands[1], bands[2], queues + 2, c4);
+              bnd, nact, tb, bands[0], bands[1], bands[2], queues + 2, c4, 0);
         } else {
-          set_smem(k_c4_dense<false, kC4DenseThreads>, sm);
-          k_c4_dense<false, kC4DenseThreads><<<g, kC4DenseThreads, sm, c->stream>>>(
-              c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
-              bnd, nact, tb, bands[0], bands[1], bands[2], queues + 3, c4);
+          if (skt) {
+            set_smem(k_c4_dense<false, kC4DenseThreads, true>, sm);
+            k_c4_dense<false, kC4DenseThreads, true><<<g, kC4DenseThreads, sm, c->stream>>>(
+                c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
+                bnd, nact, tb, bands[0], bands[1], bands[2], queues + 3, c4, skt);
+          } else {
+            set_smem(k_c4_dense<false, kC4DenseThreads>, sm);
+            k_c4_dense<false, kC4DenseThreads><<<g, kC4DenseThreads, sm, c->stream>>>(
+                c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
+                bnd, nact, tb, bands[0], bands[1], bands[2], queues + 3, c4, 0);
+          }
         }
         check_launch();
         c->launched();
@@ -938,14 +952,15 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     }
     if (cnt[6] > 0) {
       int* bnd = nullptr;
-      int* tb = tiles_for(kC4TileBytesS, B_TBS, B_TBNDS, &bnd);
+      int K = 0;
+      int* tb = tiles_for(kC4TileBytesS, B_TBS, B_TBNDS, &bnd, &K);
       const size_t sm = kC4TileBytesS;
       const int g = std::min(cnt[6], c->sms * (1024 / kC4DenseThreadsS));
       int* cur = c->ensure<int>(B_CURSORS, 2 * (size_t)g * (size_t)(c->dmax + 1));
       set_smem(k_c4_dense<true, kC4DenseThreadsS>, sm);
       k_c4_dense<true, kC4DenseThreadsS><<<g, kC4DenseThreadsS, sm, c->stream>>>(
           c->rp, c->ci, c->split, c->mir, lists[6], cnt[6], cur, (long long)(c->dmax + 1), bnd,
-          nact, tb, bands[0], bands[1], bands[2], queues + 5, c4);
+          nact, tb, bands[0], bands[1], bands[2], queues + 5, c4, 0);
       check_launch();
       c->launched();
     }

@@ -767,15 +767,18 @@ __device__ unsigned int g_dense_done;
 #define DPROF_MARK(k) do {} while (0)
 #endif
 
-template <bool PACK, int NT>
+template <bool PACK, int NT, bool SPLIT = false>
 __global__ void __launch_bounds__(NT, 1024 / NT)
 k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, int* __restrict__ cursor,
            long long cursor_stride, const int* __restrict__ bnd, long long bnd_stride,
            const int* __restrict__ tb, int b4, int b8, int b16, int* __restrict__ next_root,
-           u64* __restrict__ c4) {
-  // roots are sorted by work (largest first) and handed out dynamically
+           u64* __restrict__ c4, int split_kt_arg) {
+  // roots are sorted by work (largest first) and handed out dynamically; with
+  // SPLIT (requires bnd) the work items are (root, tile) pairs, item
+  // k * split_kt + t, so a few huge roots spread over all SMs
+  const int split_kt = SPLIT ? split_kt_arg : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
   constexpr int NW = NT / 32;
@@ -812,9 +815,15 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   while (true) {
     if (threadIdx.x == 0) s_root = atomicAdd(next_root, 1);
     __syncthreads();
-    const int k = s_root;
+    const int item = s_root;
+    const int k = split_kt ? item / split_kt : item;
     if (k >= nroots) break;
+    const int t_only = split_kt ? item % split_kt : 0;
     const int u = roots[k];
+    if (split_kt && t_only > 0 && tb[t_only] >= u) {  // root has no such tile
+      __syncthreads();
+      continue;
+    }
     const int b = rp[u], nq = split[u] - b;
     // first long row (rows in N-(u) have nondecreasing degree)
     int lo_q = 0, hi_q = nq;
@@ -836,9 +845,13 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     }
     const int qg = lo_q;
     const int nb = (qg - qs + 31) >> 5;  // batches of 32 long rows
-    for (int q = threadIdx.x; q < nq; q += blockDim.x) cur[q] = rp[ci[b + q]];
+    // short rows walk with per-row cursors across the tiles; a split item
+    // (one tile of a root) takes their segments from the tile boundaries
+    if (!split_kt)
+      for (int q = threadIdx.x; q < nq; q += blockDim.x) cur[q] = rp[ci[b + q]];
     u64 acc = 0;
-    for (int t = 0; t < ntiles; ++t) {
+    const int t_end = split_kt ? t_only + 1 : ntiles;
+    for (int t = split_kt ? t_only : 0; t < t_end; ++t) {
       const int lo = tb[t], hi = min(tb[t + 1], u);
       sh = lo < b4 ? 3 : lo < b8 ? 2 : lo < b16 ? 1 : 0;  // PACK roots never reach b16
       const int words = (hi - lo + (1 << sh) - 1) >> sh;
@@ -879,6 +892,13 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
       }
       for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
+        if (split_kt) {  // segment from the tile boundaries
+          const int v = ci[b + q];
+          const int st = bnd[kb_lo * bnd_stride + v];
+          const int se = hi >= u ? end : min(end, bnd[kb_hi * bnd_stride + v]);
+          for (int p = st; p < se; ++p) inc(ci[p] - lo);
+          continue;
+        }
         for (int p = cur[q]; p < end; ++p) {
           const int w = ci[p];
           if (w >= hi) break;
@@ -1007,14 +1027,21 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
       }
       for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
-        int p = cur[q];
         u64 sv = 0;
-        for (; p < end; ++p) {
-          const int w = ci[p];
-          if (w >= hi) break;
-          sv += get(w - lo) - 1;
+        if (split_kt) {
+          const int v = ci[b + q];
+          const int st = bnd[kb_lo * bnd_stride + v];
+          const int se = hi >= u ? end : min(end, bnd[kb_hi * bnd_stride + v]);
+          for (int p = st; p < se; ++p) sv += get(ci[p] - lo) - 1;
+        } else {
+          int p = cur[q];
+          for (; p < end; ++p) {
+            const int w = ci[p];
+            if (w >= hi) break;
+            sv += get(w - lo) - 1;
+          }
+          cur[q] = p;
         }
-        cur[q] = p;
         if (sv) atomicAdd(c4 + ci[b + q], sv);
       }
       while (true) {
