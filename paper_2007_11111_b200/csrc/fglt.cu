@@ -555,6 +555,9 @@ __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict
   }
 }
 
+#ifndef FGLT_SPLIT_BIG
+#define FGLT_SPLIT_BIG 0  // big-tile packed roots as (root, tile) items too
+#endif
 #ifndef FGLT_DLIST_NT
 #define FGLT_DLIST_NT 256  // block threads of the diamond-list kernel
 #endif
@@ -924,11 +927,16 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         const size_t sm = kC4TileBytes;
         // 32-bit-band roots (the few ranked above degree 65535) are huge: hand
         // out (root, tile) items so they spread over every SM
-        const int skt = (bb == 5 && bnd) ? K : 0;
+        const int skt = ((bb == 5 || FGLT_SPLIT_BIG) && bnd) ? K : 0;
         const int g = skt ? c->sms * (1024 / kC4DenseThreads)
                           : std::min(cnt[bb], c->sms * (1024 / kC4DenseThreads));
         int* cur = c->ensure<int>(B_CURSOR, 2 * (size_t)g * (size_t)(c->dmax + 1));
-        if (bb == 4) {
+        if (bb == 4 && skt) {
+          set_smem(k_c4_dense<true, kC4DenseThreads, true>, sm);
+          k_c4_dense<true, kC4DenseThreads, true><<<g, kC4DenseThreads, sm, c->stream>>>(
+              c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
+              bnd, nact, tb, bands[0], bands[1], bands[2], queues + 2, c4, skt);
+        } else if (bb == 4) {
           set_smem(k_c4_dense<true, kC4DenseThreads>, sm);
           k_c4_dense<true, kC4DenseThreads><<<g, kC4DenseThreads, sm, c->stream>>>(
               c->rp, c->ci, c->split, c->mir, lists[bb], cnt[bb], cur, (long long)(c->dmax + 1),
