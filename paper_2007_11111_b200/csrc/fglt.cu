@@ -558,6 +558,9 @@ __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict
 #ifndef FGLT_SPLIT_BIG
 #define FGLT_SPLIT_BIG 0  // big-tile packed roots as (root, tile) items too
 #endif
+#ifndef FGLT_SLAB_BLOCKS_PER_SM
+#define FGLT_SLAB_BLOCKS_PER_SM 2  // resident global-slab root blocks per SM (|S| > 1024)
+#endif
 #ifndef FGLT_DLIST_NT
 #define FGLT_DLIST_NT 256  // block threads of the diamond-list kernel
 #endif
@@ -704,7 +707,12 @@ void roots_pass(fglt_ctx* c) {
     if (global) {
       slab_stride = (long long)((L.bytes_aux() + 255) & ~(size_t)255);
       const long long fit = std::max<long long>(1, (4ll << 30) / slab_stride);
-      g = (int)std::min<long long>({(long long)cnt[b], (long long)c->sms, fit});
+      int occ = 1;  // resident blocks per SM (shared memory holds the per-member arrays)
+      set_smem(k_roots_block<kC3, kD13, kD15, true, kRootsThreads>, sm);
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &occ, k_roots_block<kC3, kD13, kD15, true, kRootsThreads>, kRootsThreads, sm));
+      g = (int)std::min<long long>(
+          {(long long)cnt[b], (long long)c->sms * std::max(1, std::min(occ, FGLT_SLAB_BLOCKS_PER_SM)), fit});
       slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
       FGLT_ROOTS_LAUNCH(true, kRootsThreads);
     } else {
