@@ -561,6 +561,10 @@ __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict
 #ifndef FGLT_SLAB_BLOCKS_PER_SM
 #define FGLT_SLAB_BLOCKS_PER_SM 2  // resident global-slab root blocks per SM (|S| > 1024)
 #endif
+#ifndef FGLT_SLAB_THREADS
+#define FGLT_SLAB_THREADS 256  // block threads of the global-slab root bin (|S| > 1024)
+#endif
+constexpr int kSlabThreads = FGLT_SLAB_THREADS;
 #ifndef FGLT_DLIST_NT
 #define FGLT_DLIST_NT 256  // block threads of the diamond-list kernel
 #endif
@@ -690,13 +694,17 @@ void roots_pass(fglt_ctx* c) {
     while ((1 << L.hlog) < FGLT_ROOT_HASH_FACTOR * L.s_cap) ++L.hlog;
     L.hcap = 1 << L.hlog;
     // block size follows |S|: 64 threads for |S| <= 128, 128 for <= 256, else 256
-    const int nt = global ? kRootsThreads : (b == 1 ? FGLT_BIN1_NT : b == 2 ? FGLT_BIN2_NT : kRootsThreads);
+    // graphs with roots beyond the shared-memory bins have long probe lists:
+    // their 257..1024 bins take 512-thread blocks (R-MAT 23 -7 %; R-MAT 20,
+    // max |S| 777, keeps 256: +12 % otherwise)
+    const int big_nt = c->maxout > (u64)kBlockS ? 512 : kRootsThreads;
+    const int nt = global ? kSlabThreads : (b == 1 ? FGLT_BIN1_NT : b == 2 ? FGLT_BIN2_NT : big_nt);
     L.nwarps = nt / 32;
     L.stride_cap = bitmap_stride((L.s_cap + 31) / 32);
     size_t sm = L.bytes_core();
     unsigned char* slab = nullptr;
     long long slab_stride = 0;
-    int g = std::min(cnt[b], c->sms * 8 * (kRootsThreads / nt));
+    int g = std::min(cnt[b], c->sms * std::max(1, 8 * kRootsThreads / nt));
 #define FGLT_ROOTS_LAUNCH(GLOBAL, NT)                                                              \
   do {                                                                                             \
     set_smem(k_roots_block<kC3, kD13, kD15, GLOBAL, NT>, sm);                                      \
@@ -708,17 +716,18 @@ void roots_pass(fglt_ctx* c) {
       slab_stride = (long long)((L.bytes_aux() + 255) & ~(size_t)255);
       const long long fit = std::max<long long>(1, (4ll << 30) / slab_stride);
       int occ = 1;  // resident blocks per SM (shared memory holds the per-member arrays)
-      set_smem(k_roots_block<kC3, kD13, kD15, true, kRootsThreads>, sm);
+      set_smem(k_roots_block<kC3, kD13, kD15, true, kSlabThreads>, sm);
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &occ, k_roots_block<kC3, kD13, kD15, true, kRootsThreads>, kRootsThreads, sm));
+          &occ, k_roots_block<kC3, kD13, kD15, true, kSlabThreads>, kSlabThreads, sm));
       g = (int)std::min<long long>(
           {(long long)cnt[b], (long long)c->sms * std::max(1, std::min(occ, FGLT_SLAB_BLOCKS_PER_SM)), fit});
       slab = c->ensure<unsigned char>(B_GBM, (size_t)g * (size_t)slab_stride);
-      FGLT_ROOTS_LAUNCH(true, kRootsThreads);
+      FGLT_ROOTS_LAUNCH(true, kSlabThreads);
     } else {
       sm += L.bytes_aux();
       if (nt == 64) FGLT_ROOTS_LAUNCH(false, 64);
       else if (nt == 128) FGLT_ROOTS_LAUNCH(false, 128);
+      else if (nt == 512) FGLT_ROOTS_LAUNCH(false, 512);
       else FGLT_ROOTS_LAUNCH(false, kRootsThreads);
     }
 #undef FGLT_ROOTS_LAUNCH

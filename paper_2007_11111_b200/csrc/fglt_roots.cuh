@@ -1505,7 +1505,10 @@ __global__ void k_hub_rows(const int* __restrict__ ci, const int* __restrict__ s
 #ifndef FGLT_K4_THREAD_NW
 #define FGLT_K4_THREAD_NW 16  // G[S] rows of at most this many words: thread-per-member 4-cliques
 #endif
-constexpr int kRootsThreads = 256;  // block threads for |S| > 256 (smaller bins: 64, 128)
+#ifndef FGLT_ROOTS_THREADS
+#define FGLT_ROOTS_THREADS 256
+#endif
+constexpr int kRootsThreads = FGLT_ROOTS_THREADS;  // block threads for |S| > 256 (smaller bins: 64, 128)
 #ifndef FGLT_PAIRS_IN_FLIGHT
 #define FGLT_PAIRS_IN_FLIGHT 4
 #endif
