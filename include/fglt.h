@@ -113,6 +113,12 @@ int fglt_transform_csr32(const int32_t* row_ptr, const int32_t* col_idx,
 int fglt_net_from_raw(fglt_ctx* ctx, const uint64_t* raw, int64_t n,
                       uint32_t dict_mask, int lenient, uint64_t* net,
                       fglt_error* err);
+/* Same with the caller's conversion matrix U (k x k row-major uint64, unit
+ * upper triangular; NULL = U16(s,s)): net_from_raw(raw, U, lenient)
+ * honours any validated ConversionMatrix (conversion.hpp:14-37,49-51). */
+int fglt_net_from_raw_matrix(fglt_ctx* ctx, const uint64_t* raw, int64_t n,
+                             uint32_t dict_mask, const uint64_t* U, int lenient,
+                             uint64_t* net, fglt_error* err);
 
 /* ------------------------------------------------------------------ ingest
  * Device CSR ingest replacing build_adjacency (src/graph.cpp:192-249):

@@ -68,6 +68,10 @@ def ref():
         L.fglt_ref_oracle.restype = ctypes.c_int
         L.fglt_ref_oracle.argtypes = [vp, vp, i64, i64, vp, vp]
         L.fglt_ref_counts.argtypes = [vp, vp, i64, i64, vp]
+        L.fglt_ref_build_adjacency.restype = ctypes.c_int
+        L.fglt_ref_build_adjacency.argtypes = [vp, vp, i64, i64, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_int, vp, vp, vp, ctypes.c_char_p,
+                                               ctypes.c_int]
         L.fglt_ref_d15.restype = ctypes.c_int
         L.fglt_ref_d15.argtypes = [vp, vp, i64, i64, ctypes.c_int, vp]
         _r = L
@@ -224,3 +228,24 @@ def ref_d15(rp, ci, threads=0):
     ref().fglt_ref_d15(rp.ctypes.data, ci.ctypes.data, len(rp) - 1, len(ci), threads,
                        out.ctypes.data)
     return out
+
+
+def ref_build_adjacency(eu, ev, declared_n=0, symmetrize=True, drop_self_loops=True, dedupe=True):
+    """The reference's build_adjacency on int64 pairs. Returns (rp, ci,
+    self_loops_dropped, duplicates_merged) or raises OracleError(2, msg)."""
+    eu, ev = _c(eu, np.int64), _c(ev, np.int64)
+    ne = len(eu)
+    nmax = max(int(declared_n), int(max(eu.max(initial=-1), ev.max(initial=-1))) + 1, 0)
+    rp = np.zeros(nmax + 1, np.int32)
+    ci = np.zeros(max(2 * ne, 1), np.int32)
+    out = np.zeros(4, np.int64)
+    msg = ctypes.create_string_buffer(256)
+    rc = ref().fglt_ref_build_adjacency(eu.ctypes.data, ev.ctypes.data, ne, int(declared_n),
+                                        int(symmetrize), int(drop_self_loops), int(dedupe),
+                                        rp.ctypes.data, ci.ctypes.data, out.ctypes.data, msg, 256)
+    if rc:
+        e = OracleError(rc, -1, -1)
+        e.msg = msg.value.decode()
+        raise e
+    n, nnz = int(out[0]), int(out[1])
+    return rp[:n + 1].copy(), ci[:nnz].copy(), int(out[2]), int(out[3])

@@ -98,6 +98,12 @@ void fglt_oracle_p2(const i32 *rp, const i32 *ci, i64 n, const u64 *p1, u64 *p2)
   }
 }
 
+/* fglt_oriented.c */
+void fglt_oriented_c3(const i32 *rp, const i32 *ci, i64 n, u64 *c3, u64 *C3);
+void fglt_oriented_d13(const i32 *rp, const i32 *ci, i64 n, const u64 *C3, u64 *d13);
+u64 fglt_oriented_c4_d14(const i32 *rp, const i32 *ci, i64 n, const u64 *C3, u64 *c4, u64 *d14);
+void fglt_oriented_d15(const i32 *rp, const i32 *ci, i64 n, u64 *d15);
+
 static i64 lower_bound_i32(const i32 *a, i64 lo, i64 hi, i32 key) {
   while (lo < hi) {
     i64 mid = lo + (hi - lo) / 2;
@@ -451,7 +457,9 @@ void fglt_oracle_net_from_raw(const u64 *raw, u64 *net, i64 n, uint32_t dict_mas
  * Plan (proj/src/dictionary.cpp:143-158) then column fill
  * (proj/src/kernels.cpp:384-412), then net (proj/src/transform.cpp:9-26).
  * d15_mode: 0 = the reference's own algorithm, 1 = the independent oriented
- * K4 counter (pinned equal; used at sizes the former cannot reach).
+ * K4 counter (pinned equal; used at sizes the former cannot reach), 2 = every
+ * W-cost term (C3, c4/d14, d13, d15) from the degree-oriented restatements of
+ * fglt_oriented.c (pinned equal; the only mode that finishes at R-MAT 23).
  * Returns 0 or the reference CLI exit class (tools/glt.cpp:17-21). */
 int fglt_oracle_transform(const i32 *rp, const i32 *ci, i64 n, uint32_t dict_mask,
                           int lenient, int d15_mode, u64 *raw, u64 *net,
@@ -459,6 +467,7 @@ int fglt_oracle_transform(const i32 *rp, const i32 *ci, i64 n, uint32_t dict_mas
                           u64 *touches_out) {
   int ids[16], pos[16];
   int k = ids_of(dict_mask, ids);
+  const int oriented = d15_mode == 2;
   uint32_t m = 0;
   for (int i = 0; i < 16; ++i) pos[i] = -1;
   for (int t = 0; t < k; ++t) { pos[ids[t]] = t; m |= 1u << ids[t]; }
@@ -475,17 +484,27 @@ int fglt_oracle_transform(const i32 *rp, const i32 *ci, i64 n, uint32_t dict_mas
   if (touches_out) *touches_out = 0;
 
   fglt_oracle_p1(rp, n, p1);
-  if (ANY((1u << 4) | (1u << 5) | (1u << 6) | (1u << 9) | (1u << 10) | (1u << 11) | (1u << 13)))
+  const uint32_t tri_cols =
+      (1u << 4) | (1u << 5) | (1u << 6) | (1u << 9) | (1u << 10) | (1u << 11) | (1u << 13);
+  if (oriented) {
+    if (ANY(tri_cols | (1u << 14))) fglt_oriented_c3(rp, ci, n, c3, C3);
+  } else if (ANY(tri_cols)) {
     fglt_oracle_c3(rp, ci, n, c3, C3);
+  }
   if (ANY((1u << 2) | (1u << 5) | (1u << 6))) fglt_oracle_p2(rp, ci, n, p1, p2);
   if (HAS(5)) fglt_oracle_p3(rp, ci, n, p1, p2, c3, p3);
   if (ANY((1u << 12) | (1u << 14))) {
-    u64 t = fglt_oracle_c4_d14(rp, ci, n, c4, d14);
+    u64 t = oriented ? fglt_oriented_c4_d14(rp, ci, n, C3, c4, d14)
+                     : fglt_oracle_c4_d14(rp, ci, n, c4, d14);
     if (touches_out) *touches_out = t;
   }
-  if (HAS(13)) fglt_oracle_d13(rp, ci, n, C3, d13);
+  if (HAS(13)) {
+    if (oriented) fglt_oriented_d13(rp, ci, n, C3, d13);
+    else fglt_oracle_d13(rp, ci, n, C3, d13);
+  }
   if (HAS(15)) {
-    if (d15_mode) fglt_oracle_d15_oriented(rp, ci, n, d15);
+    if (oriented) fglt_oriented_d15(rp, ci, n, d15);
+    else if (d15_mode) fglt_oracle_d15_oriented(rp, ci, n, d15);
     else fglt_oracle_d15_ref_algorithm(rp, ci, n, d15);
   }
 

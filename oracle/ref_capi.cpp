@@ -11,6 +11,7 @@
 //   fglt_ref_transform_csr32  -> graphlet::transform     (proj/src/transform.cpp:9-26)
 //   fglt_ref_er_graph          -> testutil::er_graph      (proj/tests/testutil.hpp:90-99)
 //   fglt_ref_oracle_raw/net    -> graphlet::oracle_raw/net (proj/src/oracle.cpp:102-308)
+//   fglt_ref_build_adjacency   -> graphlet::build_adjacency (proj/src/graph.cpp:192-249)
 //   fglt_ref_count_*           -> whole-graph tallies     (proj/src/oracle.cpp:359-407)
 #include <chrono>
 #include <cstdint>
@@ -81,6 +82,7 @@ int fglt_ref_transform_csr32(const int32_t* rp, const int32_t* ci, int64_t n,
        << ", \"p2_row_touches\": " << r.stats.p2_row_touches
        << ", \"p2_touch_bound\": " << r.stats.p2_touch_bound
        << ", \"peak_aux_words\": " << r.stats.peak_aux_words
+       << ", \"largest_aux_alloc_words\": " << r.stats.largest_aux_alloc_words
        << ", \"kernel_times\": [";
     for (std::size_t i = 0; i < r.stats.kernel_times.size(); ++i)
       js << (i ? ", " : "") << "[\"" << r.stats.kernel_times[i].name << "\", "
@@ -111,6 +113,41 @@ int fglt_ref_transform_csr32(const int32_t* rp, const int32_t* ci, int64_t n,
 }
 
 const char* fglt_ref_last_stats(void) { return g_last_stats.c_str(); }
+
+// build_adjacency (proj/src/graph.cpp:192-249) on (eu[i], ev[i]) pairs with
+// SanitizeOptions; rp/ci caller-allocated (n_max + 1, 2 ne); out4 = {n, nnz,
+// self_loops_dropped, duplicates_merged}. Returns 0 or 2 (StructuralError).
+int fglt_ref_build_adjacency(const int64_t* eu, const int64_t* ev, int64_t ne,
+                             int64_t declared_n, int symmetrize, int drop_self_loops,
+                             int dedupe, int32_t* rp, int32_t* ci, int64_t* out4,
+                             char* msg, int msglen) {
+  try {
+    EdgeCollection ec;
+    ec.edges.reserve(static_cast<std::size_t>(ne));
+    for (int64_t i = 0; i < ne; ++i) ec.edges.emplace_back(eu[i], ev[i]);
+    if (declared_n > 0) ec.declared_n = declared_n;
+    SanitizeOptions o;
+    o.symmetrize = symmetrize != 0;
+    o.drop_self_loops = drop_self_loops != 0;
+    o.dedupe = dedupe != 0;
+    BuildResult b = build_adjacency(ec, o);
+    const auto& off = b.graph.row_offsets();
+    const auto& col = b.graph.col_indices();
+    for (std::size_t i = 0; i < off.size(); ++i) rp[i] = static_cast<int32_t>(off[i]);
+    for (std::size_t i = 0; i < col.size(); ++i) ci[i] = static_cast<int32_t>(col[i]);
+    out4[0] = b.graph.num_vertices();
+    out4[1] = static_cast<int64_t>(col.size());
+    out4[2] = static_cast<int64_t>(b.report.self_loops_dropped);
+    out4[3] = static_cast<int64_t>(b.report.duplicates_merged);
+    return 0;
+  } catch (const StructuralError& e) {
+    put_msg(msg, msglen, e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    put_msg(msg, msglen, e.what());
+    return 6;
+  }
+}
 
 // er_graph(n, p, seed): first call with rp == nullptr to learn nnz.
 int64_t fglt_ref_er_graph(int64_t n, double p, uint64_t seed, int32_t* rp,

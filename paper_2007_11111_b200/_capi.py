@@ -22,7 +22,7 @@ CODES = {0: "ok", 1: "parse", 2: "structural", 3: "overflow", 4: "inconsistency"
 
 EXPORTS = [
     "fglt_ctx_create", "fglt_ctx_destroy", "fglt_ctx_release_workspace", "fglt_ctx_transform", "fglt_transform_csr32",
-    "fglt_net_from_raw", "fglt_stage_prepare", "fglt_stage_bounds", "fglt_stage_triangles",
+    "fglt_net_from_raw", "fglt_net_from_raw_matrix", "fglt_stage_prepare", "fglt_stage_bounds", "fglt_stage_triangles",
     "fglt_stage_local", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
     "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug", "fglt_build_csr",
     "fglt_csr_fetch", "fglt_kernel_p2", "fglt_kernel_c3", "fglt_kernel_p3", "fglt_kernel_d7",
@@ -91,6 +91,9 @@ def lib():
         L.fglt_net_from_raw.restype = ctypes.c_int
         L.fglt_net_from_raw.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int, vp,
                                         ctypes.POINTER(FgltError)]
+        L.fglt_net_from_raw_matrix.restype = ctypes.c_int
+        L.fglt_net_from_raw_matrix.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_uint32, vp,
+                                               ctypes.c_int, vp, ctypes.POINTER(FgltError)]
         L.fglt_stage_prepare.restype = ctypes.c_int
         L.fglt_stage_prepare.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32,
                                          ctypes.c_int, ctypes.POINTER(FgltError)]
@@ -253,12 +256,20 @@ class Context:
             _raise(rc, err)
         return st.as_dict()
 
-    def net_from_raw(self, raw: np.ndarray, mask: int, lenient=False):
+    def net_from_raw(self, raw: np.ndarray, mask: int, lenient=False, U=None):
+        """net_from_raw on the device; U = the caller's k x k conversion matrix
+        (None: U16(s,s))."""
         raw = np.ascontiguousarray(raw, dtype=np.uint64)
         net = np.empty_like(raw)
         err = FgltError()
-        rc = self._L.fglt_net_from_raw(self._h, raw.ctypes.data, raw.shape[0], mask, int(lenient),
-                                       net.ctypes.data, ctypes.byref(err))
+        if U is None:
+            rc = self._L.fglt_net_from_raw(self._h, raw.ctypes.data, raw.shape[0], mask,
+                                           int(lenient), net.ctypes.data, ctypes.byref(err))
+        else:
+            U = np.ascontiguousarray(U, dtype=np.uint64)
+            rc = self._L.fglt_net_from_raw_matrix(self._h, raw.ctypes.data, raw.shape[0], mask,
+                                                  U.ctypes.data, int(lenient), net.ctypes.data,
+                                                  ctypes.byref(err))
         if rc:
             _raise(rc, err)
         return net

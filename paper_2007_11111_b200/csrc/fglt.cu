@@ -64,7 +64,15 @@ enum Buf {
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  uint64_t call = 0;  // last call that used this buffer (per-call accounting)
 };
+
+// Staging copies of the caller's CSR and of the output tables: the graph and
+// the result fields, which the reference's MemoryTracker does not count as
+// auxiliary scratch (proj/include/graphlet/instrumentation.hpp:9-15).
+inline bool is_staging(int b) {
+  return b == B_RP_IN || b == B_CI_IN || b == B_RAW || b == B_NET;
+}
 
 // Per-vertex vectors, each n u64, in B_VEC.
 enum Vec { V_P2, V_D7, V_C3, V_D14, V_D10, V_P3, V_D9, V_C4, V_D13, V_D15, V_COUNT };
@@ -172,8 +180,13 @@ struct fglt_ctx {
   cudaStream_t stream = nullptr;
   int sms = 148;
   DevBuf buf[B_COUNT];
-  size_t scratch_bytes = 0, peak_scratch = 0, largest = 0;
-  uint64_t launches = 0;
+  size_t scratch_bytes = 0;  // device bytes held by the workspace (all calls)
+  // per-call auxiliary scratch (TransformStats::peak_aux_words /
+  // largest_aux_alloc_words, reset by begin_call like the reference's
+  // MemoryTracker reset in raw_frequencies, src/kernels.cpp:312)
+  uint64_t call = 0;
+  size_t call_bytes = 0, peak_scratch = 0, largest = 0;
+  uint64_t launches = 0, launches_at_call = 0;
 
   // prepared graph
   int64_t n = 0, nnz = 0, m = 0;
@@ -224,21 +237,36 @@ struct fglt_ctx {
   bool timing = false;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
 
+  void begin_call() {
+    ++call;
+    call_bytes = peak_scratch = largest = 0;
+    launches_at_call = launches;
+  }
+
   template <class T>
   T* ensure(Buf b, size_t count) {
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
     DevBuf& d = buf[b];
+    const bool counted = d.call == call;
     if (d.cap < bytes) {
       if (d.p) {
         CK(cudaFreeAsync(d.p, stream));
         scratch_bytes -= d.cap;
+        if (counted && !is_staging(b)) call_bytes -= d.cap;
       }
       size_t grow = bytes + bytes / 8;
       CK(cudaMallocAsync(&d.p, grow, stream));
       d.cap = grow;
       scratch_bytes += grow;
-      peak_scratch = std::max(peak_scratch, scratch_bytes);
-      largest = std::max(largest, grow);
+      if (counted && !is_staging(b)) call_bytes += grow;
+    }
+    if (!counted) {
+      d.call = call;
+      if (!is_staging(b)) call_bytes += d.cap;
+    }
+    if (!is_staging(b)) {
+      peak_scratch = std::max(peak_scratch, call_bytes);
+      largest = std::max(largest, d.cap);
     }
     return reinterpret_cast<T*>(d.p);
   }
@@ -752,8 +780,16 @@ void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
   CK(cudaMemcpyAsync(&bound, d_bound, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (bound == 0) return;
-  const unsigned long long blocks = (unsigned long long)c->sms * 8 * 4 * 4;
-  unsigned long long cap = bound + blocks * kTriListChunk;
+  // slack for the reservations the launched blocks and warps hold at once
+  // (each grabs >= kTriListChunk / kTriListWarpChunk records): bounded by the
+  // grids roots_pass actually launches, so the pool follows the graph size
+  unsigned long long blocks = 0, warps = 0;
+  if (!c->rb_cnt.empty()) {
+    warps = std::min<unsigned long long>(c->rb_cnt[0], (unsigned long long)c->sms * 64);
+    for (size_t b = 1; b < c->rb_cnt.size(); ++b)
+      blocks += std::min<unsigned long long>(c->rb_cnt[b], (unsigned long long)c->sms * 32);
+  }
+  unsigned long long cap = bound + blocks * kTriListChunk + warps * kTriListWarpChunk;
   if (cap * 8 > c->buf[B_TLREC].cap) {  // growing: stay within FGLT_TL_MEM_FRAC of free memory
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
@@ -771,7 +807,7 @@ void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
   t.pieces = c->ensure<TriPiece>(B_TLPIECES, t.pieces_cap);
   t.fail = c->ensure<unsigned char>(B_TLFAIL, (size_t)c->n);
   CK(cudaMemsetAsync(t.fail, 0, (size_t)c->n, c->stream));
-  t.chunks_cap = (unsigned)std::min<unsigned long long>(cap / kTriListWarpChunk + blocks * 8 + 1024,
+  t.chunks_cap = (unsigned)std::min<unsigned long long>(cap / kTriListWarpChunk + warps + 1024,
                                                         1ull << 31);
   t.chunks = c->ensure<TriChunk>(B_TLCHUNKS, t.chunks_cap);
   t.nchunks = reinterpret_cast<unsigned*>(d_bound + 3);
@@ -1099,7 +1135,7 @@ void fill_stats(fglt_ctx* c, fglt_stats* st, const std::vector<std::pair<std::st
   st->largest_aux_alloc_words = c->largest / 8;
   st->threads_used = 1;
   st->device = c->device;
-  st->kernel_launches = c->launches;
+  st->kernel_launches = c->launches - c->launches_at_call;
 }
 
 std::vector<std::pair<std::string, double>> collect_marks(fglt_ctx* c) {
@@ -1179,20 +1215,26 @@ int fglt_build_csr(fglt_ctx* c, const int64_t* eu, const int64_t* ev, int64_t ne
     }
     c->d_small = c->ensure<u64>(B_SMALL, 64);
     CK(cudaMemsetAsync(c->d_small + 40, 0, 8 * sizeof(u64), c->stream));
-    u64 h[3] = {0, 0, 0};
+    CK(cudaMemsetAsync(c->d_small + 43, 0xff, sizeof(u64), c->stream));
+    u64 h[4] = {0, 0, 0, ~0ull};
     if (ne > 0) {
       k_ingest_scan<<<c->grid(ne, 256), 256, 0, c->stream>>>(du, dv, ne, c->d_small + 40);
       check_launch();
       c->launched();
-      CK(cudaMemcpyAsync(h, c->d_small + 40, 24, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(h, c->d_small + 40, 32, cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
     }
+    // error order and messages of build_adjacency (proj/src/graph.cpp:192-249)
     if (h[0]) {
       set_err(err, FGLT_E_STRUCTURAL, -1, -1, "negative vertex id in edge collection");
       return FGLT_E_STRUCTURAL;
     }
     if (h[1] && !drop_self_loops) {
-      set_err(err, FGLT_E_STRUCTURAL, -1, -1, "self-loop present (drop_self_loops is off)");
+      long long v = -1;
+      CK(cudaMemcpyAsync(&v, du + h[3], 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      set_err(err, FGLT_E_STRUCTURAL, -1, (int64_t)v,
+              "self-loop at vertex %lld (drop_self_loops is off)", v);
       return FGLT_E_STRUCTURAL;
     }
     const int64_t n = std::max<int64_t>(declared_n, ne > 0 ? (int64_t)h[2] + 1 : 0);
@@ -1243,6 +1285,11 @@ int fglt_build_csr(fglt_ctx* c, const int64_t* eu, const int64_t* ev, int64_t ne
     k_ingest_rows<<<c->grid(nnz + 1, 256), 256, 0, c->stream>>>(keys, nnz, (int)n, rp, ci);
     check_launch();
     c->launched();
+    if (!mirror && nnz % 2) {
+      set_err(err, FGLT_E_STRUCTURAL, -1, -1,
+              "asymmetric input: odd number of directed entries with symmetrize off");
+      return FGLT_E_STRUCTURAL;
+    }
     if (!mirror && nnz > 0) {
       u64 init = ~0ull, bad = ~0ull;
       CK(cudaMemcpyAsync(c->d_small + 41, &init, 8, cudaMemcpyHostToDevice, c->stream));
@@ -1264,7 +1311,9 @@ int fglt_build_csr(fglt_ctx* c, const int64_t* eu, const int64_t* ev, int64_t ne
     if (n_out) *n_out = n;
     if (nnz_out) *nnz_out = nnz;
     if (self_loops) *self_loops = (int64_t)h[1];
-    if (duplicates) *duplicates = (int64_t)(mirror ? dups / 2 : dups);
+    // undirected edges merged away: removed directed entries / 2 in both
+    // modes, as the reference reports it (graph.cpp:227)
+    if (duplicates) *duplicates = (int64_t)(dups / 2);
     return FGLT_OK;
   } catch (const CudaFail& f) {
     set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
@@ -1393,6 +1442,7 @@ int fglt_ctx_transform(fglt_ctx* c, const int32_t* row_ptr, const int32_t* col_i
   if (rc) return rc;
   try {
     CK(cudaSetDevice(c->device));
+    c->begin_call();
     c->timing = (flags & FGLT_TIMINGS) != 0;
     c->marks.clear();
     const int* d_rp = row_ptr;
@@ -1461,6 +1511,11 @@ int fglt_transform_csr32(const int32_t* row_ptr, const int32_t* col_idx, int64_t
 
 int fglt_net_from_raw(fglt_ctx* c, const uint64_t* raw, int64_t n, uint32_t dict_mask,
                       int lenient, uint64_t* net, fglt_error* err) {
+  return fglt_net_from_raw_matrix(c, raw, n, dict_mask, nullptr, lenient, net, err);
+}
+
+int fglt_net_from_raw_matrix(fglt_ctx* c, const uint64_t* raw, int64_t n, uint32_t dict_mask,
+                             const uint64_t* U, int lenient, uint64_t* net, fglt_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (!c) {
     set_err(err, FGLT_E_NO_DEVICE, -1, -1, "null context");
@@ -1468,8 +1523,28 @@ int fglt_net_from_raw(fglt_ctx* c, const uint64_t* raw, int64_t n, uint32_t dict
   }
   try {
     CK(cudaSetDevice(c->device));
+    c->begin_call();
     c->dict = make_dict(dict_mask);
     const size_t k = (size_t)c->dict.k;
+    if (U) {  // the caller's unit upper-triangular matrix (ConversionMatrix, conversion.hpp:14-37)
+      for (size_t r = 0; r < k; ++r)
+        for (size_t col = 0; col <= r; ++col)
+          if (U[r * k + col] != (col == r ? 1u : 0u)) {
+            set_err(err, FGLT_E_STRUCTURAL, -1, -1,
+                    "conversion matrix is not unit upper triangular at (%zu,%zu)", r, col);
+            return FGLT_E_STRUCTURAL;
+          }
+      for (size_t r = 0; r < k; ++r) {
+        int t = 0;
+        for (size_t col = r + 1; col < k; ++col)
+          if (U[r * k + col]) {
+            c->dict.tail_col[r][t] = (int)col;
+            c->dict.tail_coef[r][t] = U[r * k + col];
+            ++t;
+          }
+        c->dict.ntail[r] = t;
+      }
+    }
     c->d_dict = c->ensure<DictInfo>(B_DICT, 1);
     CK(cudaMemcpyAsync(c->d_dict, &c->dict, sizeof(DictInfo), cudaMemcpyHostToDevice, c->stream));
     c->d_small = c->ensure<u64>(B_SMALL, 64);
@@ -1499,6 +1574,7 @@ int fglt_stage_prepare(fglt_ctx* c, const int32_t* d_row_ptr, const int32_t* d_c
   if (rc) return rc;
   try {
     CK(cudaSetDevice(c->device));
+    c->begin_call();
     c->timing = false;
     prepare(c, d_row_ptr, d_col_idx, n, nnz, dict_mask, lenient);
     if (n > 0) {
@@ -1653,6 +1729,7 @@ struct ApiCall {
 void api_begin(ApiCall& a, const int32_t* rp, const int32_t* ci, int64_t n, int64_t nnz) {
   fglt_ctx* c = a.c;
   CK(cudaSetDevice(c->device));
+  c->begin_call();
   c->timing = false;
   c->d_small = c->ensure<u64>(B_SMALL, 64);
   u64 init = ~0ull;

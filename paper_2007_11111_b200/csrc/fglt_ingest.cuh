@@ -10,18 +10,24 @@
 
 namespace fglt {
 
-// flags[0] = negative id seen, flags[1] = self-loops, flags[2] = max id
+// flags[0] = negative id seen, flags[1] = self-loops, flags[2] = max id,
+// flags[3] = input index of the first self-loop (init ~0; the reference
+// reports the first one in input order, graph.cpp:207-209)
 __global__ void k_ingest_scan(const long long* __restrict__ eu, const long long* __restrict__ ev,
                               long long ne, u64* __restrict__ flags) {
   long long mx = -1;
-  u64 loops = 0, neg = 0;
+  u64 loops = 0, neg = 0, first = ~0ull;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ne;
        i += (long long)gridDim.x * blockDim.x) {
     const long long u = eu[i], v = ev[i];
     neg |= (u < 0) | (v < 0);
-    loops += (u == v);
+    if (u == v) {
+      ++loops;
+      if ((u64)i < first) first = (u64)i;
+    }
     mx = max(mx, max(u, v));
   }
+  if (first != ~0ull) atomicMin(flags + 3, first);
   loops = warp_sum_u64(loops);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

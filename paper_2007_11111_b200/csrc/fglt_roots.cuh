@@ -1156,7 +1156,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
 // (pool or piece table exhausted, or |S| > kTriListMaxS) are flagged and keep
 // the probing diamond pass; pieces of flagged roots are ignored.
 constexpr int kTriListMaxS = 8192;              // member ids fit 16 bits, sD fits smem
-constexpr unsigned long long kTriListChunk = 1ull << 16;  // records per pool grab
+constexpr unsigned long long kTriListChunk = 1ull << 13;  // records per pool grab (64 KB)
 
 struct TriPiece {
   unsigned long long start;  // first record
@@ -2057,7 +2057,7 @@ struct DictInfo {
   unsigned mask;
   int ntail[16];          // per dictionary position r, number of tail entries
   int tail_col[16][16];   // positions c > r with U[ids[r]][ids[c]] != 0
-  unsigned tail_coef[16][16];
+  unsigned long long tail_coef[16][16];  // U(s,s) or a caller's ConversionMatrix
 };
 
 __device__ __forceinline__ bool mul_ov(u64 a, u64 b, u64* r) {

@@ -473,63 +473,16 @@ EdgeCollection parse_matrix_market(std::istream& in) {
 }
 
 namespace {
-bool device_ingest(const EdgeCollection& ec, const SanitizeOptions& opt, BuildResult* out);
+BuildResult device_ingest(const EdgeCollection& ec, const SanitizeOptions& opt);
 }  // namespace
 
+// Sanitised CSR from an edge collection: mirror, drop self-loops, sort,
+// dedupe, offsets — all on the device (fglt_build_csr, fglt_ingest.cuh), with
+// build_adjacency's error classes, messages and BuildReport
+// (proj/src/graph.cpp:192-249). There is no host path: without a CUDA device
+// this throws, like every other entry point.
 BuildResult build_adjacency(const EdgeCollection& ec, const SanitizeOptions& opt) {
-  // Large inputs are sanitised on the device (fglt_build_csr); small ones, or a
-  // machine without a CUDA device, use the host sort below (ingest only —
-  // graphlet counting itself has no host path).
-  {
-    BuildResult dev;
-    if (device_ingest(ec, opt, &dev)) return dev;
-  }
-  vertex_t n = ec.declared_n.value_or(0);
-  for (const auto& [u, v] : ec.edges) {
-    if (u < 0 || v < 0) throw StructuralError("negative vertex id in edge collection");
-    n = std::max(n, std::max(u, v) + 1);
-  }
-  BuildResult out;
-  const bool mirror = opt.symmetrize || ec.declared_symmetric();
-  // pack (u, v) into one sortable 64-bit key per directed entry
-  std::vector<std::pair<vertex_t, vertex_t>> dir;
-  dir.reserve(ec.edges.size() * (mirror ? 2 : 1));
-  for (const auto& [u, v] : ec.edges) {
-    if (u == v) {
-      if (!opt.drop_self_loops)
-        throw StructuralError("self-loop at vertex " + std::to_string(u) +
-                              " (drop_self_loops is off)");
-      ++out.report.self_loops_dropped;
-      continue;
-    }
-    dir.emplace_back(u, v);
-    if (mirror) dir.emplace_back(v, u);
-  }
-  std::sort(dir.begin(), dir.end());
-  const std::size_t before = dir.size();
-  dir.erase(std::unique(dir.begin(), dir.end()), dir.end());
-  if (dir.size() != before) {
-    if (!opt.dedupe) throw StructuralError("duplicate edges present (dedupe is off)");
-    out.report.duplicates_merged = static_cast<count_t>(before - dir.size()) / 2;
-  }
-  std::vector<std::int64_t> off(static_cast<std::size_t>(n) + 1, 0);
-  std::vector<vertex_t> col(dir.size());
-  for (std::size_t k = 0; k < dir.size(); ++k) {
-    ++off[static_cast<std::size_t>(dir[k].first) + 1];
-    col[k] = dir[k].second;
-  }
-  for (std::size_t i = 1; i < off.size(); ++i) off[i] += off[i - 1];
-  out.graph = SparseAdjacency(std::move(off), std::move(col));
-  if (!mirror) {
-    // a non-symmetrised input must already be symmetric
-    const auto& g = out.graph;
-    for (vertex_t v = 0; v < g.num_vertices(); ++v)
-      for (vertex_t x : g.row(v))
-        if (!g.has_edge(x, v))
-          throw StructuralError("asymmetric adjacency at (" + std::to_string(v) + "," +
-                                std::to_string(x) + ")");
-  }
-  return out;
+  return device_ingest(ec, opt);
 }
 
 std::vector<count_t> degree_vector(const SparseAdjacency& g) {
@@ -640,29 +593,34 @@ fglt_ctx* context_for(int device) {
 
 [[noreturn]] void rethrow(int rc, const fglt_error& e);
 
-bool device_ingest(const EdgeCollection& ec, const SanitizeOptions& opt, BuildResult* out) {
-  if (ec.edges.size() < (std::size_t{1} << 16) || fglt_device_count() == 0) return false;
+BuildResult device_ingest(const EdgeCollection& ec, const SanitizeOptions& opt) {
   fglt_ctx* ctx = context_for(0);
-  std::vector<std::int64_t> eu(ec.edges.size()), ev(ec.edges.size());
-  for (std::size_t i = 0; i < ec.edges.size(); ++i) {
+  const std::size_t ne = ec.edges.size();
+  std::vector<std::int64_t> eu(ne), ev(ne);
+  for (std::size_t i = 0; i < ne; ++i) {
     eu[i] = ec.edges[i].first;
     ev[i] = ec.edges[i].second;
   }
   std::int64_t n = 0, nnz = 0, loops = 0, dups = 0;
   fglt_error err{};
-  std::lock_guard<std::mutex> lock(g_run_mu);
-  int rc = fglt_build_csr(ctx, eu.data(), ev.data(), static_cast<std::int64_t>(eu.size()),
-                          ec.declared_n.value_or(0), opt.symmetrize || ec.declared_symmetric(),
-                          opt.drop_self_loops, opt.dedupe, 0, &n, &nnz, &loops, &dups, &err);
-  if (rc) rethrow(rc, err);
-  std::vector<std::int32_t> rp(static_cast<std::size_t>(n) + 1), ci(static_cast<std::size_t>(nnz));
-  rc = fglt_csr_fetch(ctx, rp.data(), ci.data(), 0, &err);
-  if (rc) rethrow(rc, err);
-  out->graph = SparseAdjacency(std::vector<std::int64_t>(rp.begin(), rp.end()),
-                               std::vector<vertex_t>(ci.begin(), ci.end()));
-  out->report.self_loops_dropped = static_cast<count_t>(loops);
-  out->report.duplicates_merged = static_cast<count_t>(dups);
-  return true;
+  std::vector<std::int32_t> rp, ci;
+  {
+    std::lock_guard<std::mutex> lock(g_run_mu);
+    int rc = fglt_build_csr(ctx, eu.data(), ev.data(), static_cast<std::int64_t>(ne),
+                            ec.declared_n.value_or(0), opt.symmetrize || ec.declared_symmetric(),
+                            opt.drop_self_loops, opt.dedupe, 0, &n, &nnz, &loops, &dups, &err);
+    if (rc) rethrow(rc, err);
+    rp.resize(static_cast<std::size_t>(n) + 1);
+    ci.resize(static_cast<std::size_t>(nnz));
+    rc = fglt_csr_fetch(ctx, rp.data(), ci.data(), 0, &err);
+    if (rc) rethrow(rc, err);
+  }
+  BuildResult out;
+  out.graph = SparseAdjacency(std::vector<std::int64_t>(rp.begin(), rp.end()),
+                              std::vector<vertex_t>(ci.begin(), ci.end()));
+  out.report.self_loops_dropped = static_cast<count_t>(loops);
+  out.report.duplicates_merged = static_cast<count_t>(dups);
+  return out;
 }
 
 [[noreturn]] void rethrow(int rc, const fglt_error& e) {
@@ -739,13 +697,19 @@ NetFrequencyField net_from_raw(const RawFrequencyField& raw, const ConversionMat
     throw Error("conversion matrix does not match the field's dictionary");
   NetFrequencyField net(raw.num_vertices(), raw.dictionary());
   if (raw.num_vertices() == 0) return net;
+  // the matrix the caller passed, not the built-in U16(s,s) (conversion.cpp:80-116)
+  const std::size_t k = U.dim();
+  std::vector<count_t> dense(k * k);
+  for (std::size_t r = 0; r < k; ++r)
+    for (std::size_t c = 0; c < k; ++c) dense[r * k + c] = U.coeff(r, c);
   fglt_ctx* ctx = context_for(0);
   fglt_error err{};
   int rc;
   {
     std::lock_guard<std::mutex> lock(g_run_mu);
-    rc = fglt_net_from_raw(ctx, raw.data().data(), raw.num_vertices(), raw.dictionary().mask(),
-                           lenient ? 1 : 0, net.mutable_data(), &err);
+    rc = fglt_net_from_raw_matrix(ctx, raw.data().data(), raw.num_vertices(),
+                                  raw.dictionary().mask(), dense.data(), lenient ? 1 : 0,
+                                  net.mutable_data(), &err);
   }
   if (rc) rethrow(rc, err);
   return net;

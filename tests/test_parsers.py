@@ -26,17 +26,27 @@ def _edge_text(m, n, seed, noise=True):
     return "\n".join(lines), u, v
 
 
-def _same_graph(g, u, v, n):
-    ref = gt.from_edges(np.stack([u, v], axis=1).astype(np.int64), n)
-    assert (g.num_vertices, g.num_edges) == (ref.num_vertices, ref.num_edges)
-    for x in range(0, n, max(1, n // 200)):
-        assert g.neighbors(x) == ref.neighbors(x)
+def _same_edges(text, fmt, u, v):
+    """The parallel host parser returns exactly the pairs, in input order."""
+    e, _, _ = gt.parse_text(text, fmt)
+    np.testing.assert_array_equal(e[:, 0], u)
+    np.testing.assert_array_equal(e[:, 1], v)
 
 
 def test_edge_list_multi_chunk():
     text, u, v = _edge_text(400_000, 50_000, 3)  # several MB: several chunks
     assert len(text) > 4 << 20
-    _same_graph(gt.from_text(text, "edges"), u, v, 50_000)
+    _same_edges(text, "edges", u, v)
+
+
+@pytest.mark.gpu
+def test_edge_list_graph_via_device_ingest():
+    text, u, v = _edge_text(200_000, 30_000, 5)
+    g = gt.from_text(text, "edges")
+    ref = gt.from_edges(np.stack([u, v], axis=1).astype(np.int64), 30_000)
+    assert (g.num_vertices, g.num_edges) == (ref.num_vertices, ref.num_edges)
+    for x in range(0, 30_000, 150):
+        assert g.neighbors(x) == ref.neighbors(x)
 
 
 def test_edge_list_first_error_line():
@@ -46,13 +56,13 @@ def test_edge_list_first_error_line():
     lines[350_000] = "1 2 3"
     lines[123_456] = "7 x"
     with pytest.raises(gt.ParseError, match=r"^line 123457: malformed vertex id 'x'$"):
-        gt.from_text("\n".join(lines), "edges")
+        gt.parse_text("\n".join(lines), "edges")
     lines[123_456] = "7 8"
     with pytest.raises(gt.ParseError, match=r"^line 350001: expected 'u v', got 3 tokens$"):
-        gt.from_text("\n".join(lines), "edges")
+        gt.parse_text("\n".join(lines), "edges")
     lines[350_000] = "-1 2"
     with pytest.raises(gt.ParseError, match=r"^line 350001: negative vertex id$"):
-        gt.from_text("\n".join(lines), "edges")
+        gt.parse_text("\n".join(lines), "edges")
 
 
 def _mtx(entries, n, nnz=None, field="pattern", extra=()):
@@ -71,11 +81,12 @@ def test_matrix_market_multi_chunk_and_truncation():
     n, m = 60_000, 500_000
     u, v = rng.integers(0, n, m), rng.integers(0, n, m)
     ents = list(zip(u.tolist(), v.tolist()))
-    g = gt.from_text(_mtx(ents, n, field="real"), "mtx")
-    _same_graph(g, u, v, n)
+    _same_edges(_mtx(ents, n, field="real"), "mtx", u, v)
+    e, declared, sym = gt.parse_text(_mtx(ents, n, field="real"), "mtx")
+    assert declared == n and not sym
     # only nnz entries are read: trailing garbage after them is never parsed
-    g2 = gt.from_text(_mtx(ents, n, nnz=m - 10, extra=["garbage here", "1"]), "mtx")
-    _same_graph(g2, u[: m - 10], v[: m - 10], n)
+    _same_edges(_mtx(ents, n, nnz=m - 10, extra=["garbage here", "1"]), "mtx", u[: m - 10],
+                v[: m - 10])
 
 
 def test_matrix_market_errors():
@@ -86,10 +97,10 @@ def test_matrix_market_errors():
     bad = 4 + 250_000 + 250_000 // 101 + 1  # 1-based line of entry 250000
     lines[bad - 1] = "3 99"
     with pytest.raises(gt.ParseError, match=rf"^line {bad}: entry \(3,99\) out of declared range 50$"):
-        gt.from_text("\n".join(lines), "mtx")
+        gt.parse_text("\n".join(lines), "mtx")
     with pytest.raises(gt.ParseError, match=r"unexpected end of stream: got 300000 of 300001 entries"):
-        gt.from_text(_mtx(ents, 50, nnz=300_001), "mtx")
+        gt.parse_text(_mtx(ents, 50, nnz=300_001), "mtx")
     with pytest.raises(gt.ParseError, match=r"^line 1: only coordinate format is supported, got 'array'$"):
-        gt.from_text("%%MatrixMarket matrix array real general\n2 2\n", "mtx")
+        gt.parse_text("%%MatrixMarket matrix array real general\n2 2\n", "mtx")
     with pytest.raises(gt.ParseError, match=r"^line 4: expected 2 tokens per entry$"):
-        gt.from_text("%%MatrixMarket matrix coordinate pattern general\n3 3 2\n1 2\n# not a comment\n", "mtx")
+        gt.parse_text("%%MatrixMarket matrix coordinate pattern general\n3 3 2\n1 2\n# not a comment\n", "mtx")

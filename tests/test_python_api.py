@@ -13,7 +13,9 @@ import paper_2007_11111_b200 as gt
 
 
 def demo_graph():
-    return gt.from_edges(gu.DEMO_EDGES)
+    """The Fig. 2 graph wrapped from its CSR (host only, no ingest)."""
+    rp, ci = gu.demo()
+    return gt.from_csr(rp, ci)
 
 
 def test_graph_basics():
@@ -26,15 +28,26 @@ def test_graph_basics():
     assert "n=6" in repr(g)
 
 
+def test_from_csr_validates():
+    with pytest.raises(gt.StructuralError):
+        gt.from_csr([0, 1, 1], [1])            # asymmetric
+    with pytest.raises(gt.StructuralError):
+        gt.from_csr([0, 1], [0])               # self-loop
+    g = gt.from_csr([0, 1], [0], validate=False)
+    assert g.num_vertices == 1
+
+
+@pytest.mark.gpu
 def test_edges_as_array_equal_list():
     a = gt.from_edges(np.asarray(gu.DEMO_EDGES, dtype=np.int64))
-    b = demo_graph()
+    b = gt.from_edges(gu.DEMO_EDGES)
     assert (a.num_vertices, a.num_edges) == (b.num_vertices, b.num_edges)
     for v in range(6):
-        assert a.neighbors(v) == b.neighbors(v)
+        assert a.neighbors(v) == b.neighbors(v) == demo_graph().neighbors(v)
 
 
-def test_text_parsing_edge_list_and_mtx_host():
+@pytest.mark.gpu
+def test_text_parsing_edge_list_and_mtx():
     text = "\n".join(f"{u} {v}" for (u, v) in gu.DEMO_EDGES)
     g = gt.from_text(text)
     assert g.num_vertices == 6 and g.num_edges == 9
@@ -44,11 +57,15 @@ def test_text_parsing_edge_list_and_mtx_host():
     assert g2.num_vertices == 6 and g2.num_edges == 9
 
 
-def test_sanitization_and_errors_host():
+@pytest.mark.gpu
+def test_sanitization_and_errors():
     g = gt.from_edges([(0, 1), (1, 0), (0, 1), (2, 2)])
     assert g.num_vertices == 3 and g.num_edges == 1
     with pytest.raises(ValueError):
         gt.from_edges([(0, 1)], symmetrize=False)
+
+
+def test_parse_and_dictionary_errors_host():
     with pytest.raises(ValueError):
         gt.from_text("0 x")
     with pytest.raises(gt.ParseError):
@@ -57,6 +74,26 @@ def test_sanitization_and_errors_host():
         gt.graphlet_ids("4-2")
     with pytest.raises(gt.ParseError):
         gt.graphlet_ids("1,")
+
+
+def test_oracle_tables_host():
+    """The brute-force oracle (host, csrc/brute.cpp) reproduces the Fig. 2
+    tables and equals the reference's own oracle on random graphs."""
+    g = demo_graph()
+    np.testing.assert_array_equal(gt.oracle_raw(g), gu.DEMO_RAW)
+    np.testing.assert_array_equal(gt.oracle_net(g), gu.DEMO_NET)
+    with pytest.raises(gt.StructuralError):
+        gt.oracle_raw(g, cap=5)
+    from oracle import binding as ob
+    if not ob.have_ref():
+        pytest.skip("oracle/_ref not built")
+    for t in range(40):
+        n = 3 + t % 30
+        rp, ci = ob.ref_er_graph(n, (0.1, 0.25, 0.5)[t % 3], 77 + t)
+        h = gt.from_csr(rp, ci)
+        rraw, rnet = ob.ref_oracle(rp, ci)
+        np.testing.assert_array_equal(gt.oracle_raw(h), rraw)
+        np.testing.assert_array_equal(gt.oracle_net(h), rnet)
 
 
 def test_dictionary_specs():
@@ -80,6 +117,12 @@ def test_graphlet_names():
     assert len(names) == 16
     assert names[0] == "singleton"
     assert "claw" in names[8]
+
+
+@pytest.mark.gpu
+def test_cross_check_legs():
+    ok, report = gt.cross_check(demo_graph())
+    assert ok and "all legs pass" in report, report
 
 
 @pytest.mark.gpu
