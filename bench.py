@@ -31,7 +31,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "input edges/sec for full Σ16 FGlT (raw+net) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "edges/s"
-REF_SAMPLE_SCALE = 13  # reference arm sample: same R-MAT generator, scale 13
 
 
 def b_alg(n: int, nnz: int, W: int) -> int:
@@ -109,101 +108,172 @@ def ncu_summary(cfg: int):
         return json.load(f)
 
 
-# SURVEY.md §8(d) terms of B_alg charged to each reference step (bytes)
-PHASE_BYTES = {
-    "four-cycle rows": lambda nnz, W: 4 * nnz + 4 * W,   # two-hop base col + index reads
-    "triangles": lambda nnz, W: 8 * nnz + 4 * W,         # edge pass col + C3 write + intersections
-    "diamond rows": lambda nnz, W: 4 * W,                # C3 values read alongside (D4 term)
+def compulsory_bytes(n: int, nnz: int) -> int:
+    """Algorithm-specific lower bound on HBM bytes of one transform step
+    (DESIGN.md §6): read the int32 CSR (4n + 4nnz), write + read the
+    relabelled CSR (2 x (4n + 4nnz)), write + read the per-edge uint32 C3
+    (8 nnz), write + read ten per-vertex uint64 columns (160 n), write the raw
+    and net n x 16 uint64 tables (256 n). Enumeration traffic (wedges,
+    probes) is served on chip / from L2 and is not charged."""
+    return 3 * (4 * n + 4 * nnz) + 8 * nnz + 160 * n + 256 * n
+
+
+def phase_table(stats):
+    """Mean seconds and work units per device phase over the timed steps."""
+    acc = {}
+    for st in stats:
+        for name, secs, units in st.get("phases", []):
+            a = acc.setdefault(name, [0.0, 0, 0])
+            a[0] += secs
+            a[1] += units
+            a[2] += 1
+    return {k: {"ms": v[0] / v[2] * 1e3, "units": v[1] // v[2]} for k, v in acc.items()}
+
+
+# device phases that are one kernel family each (the "dominant kernel" pick)
+KERNEL_PHASES = {
+    "c4 dense": "fglt::k_c4_dense (dense shared-memory tiles)",
+    "c4 hash": "fglt::k_c4_warp / k_c4_block (hash tables)",
+    "triangle pass": "fglt::k_roots_block / k_roots_warp <kC3> (triangles, C3, 4-cliques)",
+    "diamond list": "fglt::k_diamond_list / k_diamond_wlist",
+    "diamond probe": "fglt::k_roots_block <kD13> (probing diamond pass)",
+    "prepare": "relabel + CUB sorts + split/mirror",
+    "sweeps B/C": "fglt::k_rows_group / k_rows_block (SweepB, SweepC)",
+    "sweep A": "fglt::k_rows_group / k_rows_block (SweepA)",
+    "column fill": "fglt::k_epilogue_rank (column fill + raw->net)",
 }
 
 
-def dominant_phase(dom, step_ms: float, nnz: int, W: int, peak_gbs: float):
-    """The longest reference step, timed live (CUDA events on the launch
-    stream), with its share of B_alg and the implied fraction of the HBM
-    roofline (work-reduced vs the paper formulation, like the step total)."""
-    name, ms = dom
-    out = {"name": name, "ms": ms, "share": ms / step_ms if ms else None}
-    f = PHASE_BYTES.get(name)
-    if f and ms:
-        b = f(nnz, W)
-        out.update({"alg_bytes": b, "achieved_gbs": b / (ms * 1e-3) / 1e9,
-                    "frac": b / (ms * 1e-3) / 1e9 / peak_gbs})
-    return out
-
-
-def dominant_kernel(summary, step_ms: float, peak_gbs: float):
-    """The top kernel of the ncu launch list: its share of the step (ncu's
-    per-launch times are cold-cache and serialised, so the share, not the
-    absolute, carries over), its DRAM bytes per step and the DRAM bandwidth
-    that implies at the live step time — the honest HBM fraction of a kernel
-    whose bound is on-chip (shared-memory atomics, L2 gathers), not HBM."""
-    if not summary or not summary.get("kernels"):
-        return None
-    k = summary["kernels"][0]
-    ms = k["share"] * step_ms
-    dram = k["dram_read"] + k["dram_write"]
-    gbs = dram / (ms * 1e-3) / 1e9 if ms > 0 else None
-    return {"name": k["name"], "share_of_step": k["share"], "ms_at_live_step": ms,
-            "dram_bytes_per_step": dram, "dram_gbs": gbs,
-            "dram_frac_of_peak": gbs / peak_gbs if gbs else None,
-            "bound": "shared-memory atomics + L2 gathers + tile barriers (see profiles/)"}
-
-
 # ----------------------------------------------------------------- reference
+REF_D15_CAP_S = 60  # wall-clock cap of the reference's compute_d15 on configs 3/4
+
+
+def _host_facts():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def _read_config_files(cfg: int, tmp: str):
+    """The config's CSR from the standalone generator (paper_2007_11111_b200/
+    fglt_gen, a plain executable): the reference arm never imports the
+    package or loads its libraries; the CSR bytes are the GPU arm's."""
+    exe = os.path.join(ROOT, "paper_2007_11111_b200", "fglt_gen")
+    out = subprocess.run([exe, str(cfg), os.path.join(tmp, "g")], capture_output=True, text=True,
+                         check=True)
+    meta = json.loads(out.stdout.strip().splitlines()[-1])
+    rp = np.fromfile(os.path.join(tmp, "g.rp.i32"), dtype=np.int32)
+    ci = np.fromfile(os.path.join(tmp, "g.ci.i32"), dtype=np.int32)
+    return meta["workload"], rp, ci
+
+
+def _capped_ref_d15(tmp: str, cap_s: int):
+    """The reference's compute_d15 on the same CSR in a child process killed
+    after cap_s seconds: returns seconds, or None on DNF."""
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from oracle import binding as ob; "
+            "rp = np.fromfile(%r, np.int32); ci = np.fromfile(%r, np.int32); "
+            "ob.ref_d15(rp, ci, 0)") % (ROOT, os.path.join(tmp, "g.rp.i32"),
+                                        os.path.join(tmp, "g.ci.i32"))
+    t0 = time.time()
+    try:
+        subprocess.run([sys.executable, "-c", code], timeout=cap_s, check=True,
+                       capture_output=True)
+    except subprocess.TimeoutExpired:
+        return None
+    return time.time() - t0
+
+
 def reference_arm(args):
+    """The UNMODIFIED reference graphlet::transform (oracle/_ref, compiled from
+    /root/reference/proj/src by oracle/Makefile) on the host cores, on the
+    GPU arm's config and CSR bytes. Configs 3 and 4: the
+    reference's tetrahedra step is out of reach (≈24 / ≈700 core-hours,
+    SURVEY §6), so each step is the full transform with dictionary all − {15}
+    (every other step, dictionary.cpp:156) — an UPPER bound on its full-Σ16
+    rate — and compute_d15 is run under a cap and reported DNF. Those
+    configs take one timed step (one step is minutes of CPU work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle import binding as ob
-    from paper_2007_11111_b200 import graphs
+    import tempfile
+    from oracle import binding as ob  # loads oracle/_ref/libfglt_ref.so only
     if not ob.have_ref():
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libfglt_ref.so not built (reference sources absent)"}))
         return 0
-    rp, ci = graphs.rmat(REF_SAMPLE_SCALE, 16, seed=1)
-    m = len(ci) // 2
-    threads = os.cpu_count() or 1
-    for _ in range(min(args.warmup, 1)):
-        ob.ref_transform(rp, ci, 0xFFFF, False, 0)
-    times = []
-    t_start = time.time()
-    for _ in range(args.steps):
-        _, _, secs, _ = ob.ref_transform(rp, ci, 0xFFFF, False, 0)
-        times.append(secs)
-        if time.time() - t_start > 150:  # keep the arm within a few minutes
-            break
+    cfg = args.config
+    big = cfg in (3, 4)
+    mask = 0x7FFF if big else 0xFFFF
+    with tempfile.TemporaryDirectory() as tmp:
+        name, rp, ci = _read_config_files(cfg, tmp)
+        n, m = len(rp) - 1, len(ci) // 2
+        threads = os.cpu_count() or 1
+        warm = 0 if big else min(args.warmup, 1)
+        for _ in range(warm):
+            ob.ref_transform(rp, ci, mask, big, 0)
+        times, stats = [], None
+        t_start = time.time()
+        for _ in range(1 if big else args.steps):
+            # all - {15} is an incomplete family: lenient (net clamped, raw unchanged)
+            _, _, secs, stats = ob.ref_transform(rp, ci, mask, big, 0)
+            times.append(secs)
+            if time.time() - t_start > 150:  # keep the arm within a few minutes
+                break
+        d15 = None
+        if big:
+            t = _capped_ref_d15(tmp, REF_D15_CAP_S)
+            d15 = {"status": "DNF" if t is None else "done", "cap_s": REF_D15_CAP_S,
+                   "seconds": t, "projection": "≈24 core-hours at config 3, ≈700 at config 4 "
+                   "(SURVEY §6 cost model calibrated on R-MAT 16)"}
     t = statistics.mean(times)
     value = m / t
-    sample = (f"full Sigma16 reference graphlet::transform (unmodified, oracle/_ref) on R-MAT "
-              f"scale {REF_SAMPLE_SCALE} (config-3 generator and parameters, n={len(rp) - 1}, m={m}),"
-              f" {threads} threads; the reference's edges/s falls with scale (d15 is superlinear),"
-              f" so this overstates its config-3 rate")
+    dict_txt = "all − {15} (d15 DNF, see d15)" if big else "all (Σ16)"
+    sample = (f"unmodified reference graphlet::transform (oracle/_ref) on config {cfg} "
+              f"({name}, n={n}, m={m}), dictionary {dict_txt}, {threads} threads, "
+              f"{len(times)} timed step(s)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
-            "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": t * 1e3,
+            "steps": len(times), "warmup": warm, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic",
-            "config": {"workload": f"rmat scale {REF_SAMPLE_SCALE} (sample of config 3)",
-                       "n": len(rp) - 1, "m": m},
+            "config": {"workload": f"config {cfg}: {name}", "n": n, "m": m, "nnz": len(ci),
+                       "dictionary": dict_txt, "same_config": True,
+                       "input": "the GPU arm's CSR bytes (fglt_gen), wrapped with "
+                                "SparseAdjacency(row_offsets, col_indices)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "kernel_times": stats.get("kernel_times") if stats else None,
+            "d15": d15, "host": _host_facts(),
+            "note": "value is an upper bound on the reference's full-Σ16 rate where d15 is "
+                    "excluded" if big else "full Σ16"}
     print(json.dumps(line))
     return 0
 
 
-def cpu_baseline_leg():
+def cpu_baseline_leg(rp, ci, name, cfg):
+    """Rank 0, N=1: a bounded sample (~10-30 s of host CPU) of the same
+    workload — the unmodified reference on the SAME CSR with the dictionary
+    0-11 (degrees, triangles, two-/three-paths, column fill: every step but
+    the W-quadratic four-cycle / diamond / tetrahedra ones) on configs 3/4,
+    the full Σ16 elsewhere. An upper bound on the reference's full rate."""
     from oracle import binding as ob
-    from paper_2007_11111_b200 import graphs
     if not ob.have_ref():
         return None
-    rp, ci = graphs.rmat(REF_SAMPLE_SCALE, 16, seed=1)
+    mask = 0x0FFF if cfg in (3, 4) else 0xFFFF
     m = len(ci) // 2
-    _, _, secs, st = ob.ref_transform(rp, ci, 0xFFFF, False, 0)
+    _, _, secs, st = ob.ref_transform(rp, ci, mask, True, 0)  # sub-family: lenient net
     return {"value": m / secs, "unit": UNIT, "cores": st.get("threads_used", os.cpu_count()),
             "kind": "reference",
-            "sample": f"unmodified reference transform, full Sigma16, R-MAT scale "
-                      f"{REF_SAMPLE_SCALE} (config-3 generator, m={m}), {secs:.2f} s"}
+            "sample": f"unmodified reference transform on config {cfg} ({name}, m={m}), "
+                      f"dictionary {'0-11' if cfg in (3, 4) else 'all'}, {secs:.2f} s",
+            "kernel_times": st.get("kernel_times")}
 
 
 # ---------------------------------------------------------------------- ours
@@ -353,23 +423,69 @@ def main():
         return 0
 
     # per-phase averages over the timed steps (CUDA events on the launch stream)
-    phases = {}
+    steps_ref = {}
     launches = 0
     for st in stats:
-        launches += st.get("kernel_launches", 0)
+        launches += st.get("kernel_launches", 0)  # per-call counts (fglt_stats)
         for k, v in st.get("kernel_times", []):
-            phases[k] = phases.get(k, 0.0) + v
-    phases = {k: v / len(stats) * 1e3 for k, v in phases.items()}
+            steps_ref[k] = steps_ref.get(k, 0.0) + v
+    steps_ref = {k: v / len(stats) * 1e3 for k, v in steps_ref.items()}
+    phases = phase_table(stats)
     W = int(stats[0].get("W", 0)) if stats and stats[0].get("W") else int(
         (np.diff(rp_h).astype(np.int64) ** 2).sum())
     dmax = int(np.diff(rp_h).max()) if n else 0
-    balg = b_alg(n, nnz, W)
     peak, peak_kind = peaks()
-    achieved = balg / (t_ms * 1e-3) / 1e9 / world
-    dom = max(phases.items(), key=lambda kv: kv[1]) if phases else (None, None)
     summ = ncu_summary(args.config)
     traffic = summ.get("dram_bytes_per_step") if summ else None
     traffic_src = summ.get("source") if summ else None
+    bc = compulsory_bytes(n, nnz)
+    balg = b_alg(n, nnz, W)
+    step_s = t_ms * 1e-3
+    # dominant kernel: the longest single-kernel phase of the live timed steps
+    dom_name, dom = None, None
+    for k in KERNEL_PHASES:
+        if k in phases and (dom is None or phases[k]["ms"] > dom["ms"]):
+            dom_name, dom = k, phases[k]
+    dominant = None
+    if dom:
+        dominant = {"phase": dom_name, "kernel": KERNEL_PHASES[dom_name], "ms": dom["ms"],
+                    "share_of_step": dom["ms"] / t_ms}
+        if dom_name == "c4 dense" and dom["units"]:
+            rate = ctx.smem_atomic_rate() if world == 1 else None
+            ach = dom["units"] / (dom["ms"] * 1e-3)
+            dominant["onchip"] = {
+                "resource": "shared-memory atomicAdd, one per wedge, random address (the "
+                            "count pass; the attribution pass re-reads each wedge)",
+                "wedges_per_launch": dom["units"], "achieved_gops": ach / 1e9,
+                "peak_gops": rate / 1e9 if rate else None,
+                "peak_kind": "measured live (fglt_probe_smem_atomics: 96 KB tiles, 2 x 512 "
+                             "threads per SM)",
+                "frac": ach / rate if rate else None}
+        if summ:
+            for kk in summ.get("kernels", []):
+                if kk["name"].startswith("void fglt::k_c4_dense") and dom_name == "c4 dense":
+                    dram = kk["dram_read"] + kk["dram_write"]
+                    dominant["dram_bytes_per_step"] = dram
+                    dominant["dram_frac"] = dram / (dom["ms"] * 1e-3) / 1e9 / peak
+                    break
+    roofline = {
+        "bound": "hbm", "unit": "GB/s", "peak": peak, "peak_kind": peak_kind,
+        "achieved": (traffic / step_s / 1e9) if traffic else None,
+        "frac": (traffic / step_s / 1e9 / peak) if traffic else None,
+        "traffic": traffic, "traffic_source": traffic_src,
+        "scope": "whole transform step: measured DRAM bytes per step (ncu launch list of the "
+                 "same build, profiles/) / live CUDA-event step time",
+        "alg_model": {"name": "compulsory HBM bytes (bench.compulsory_bytes, DESIGN.md §6)",
+                      "bytes": bc, "achieved_gbs": bc / step_s / 1e9,
+                      "frac": bc / step_s / 1e9 / peak},
+        "paper_formulation": {"bytes": balg, "frac": balg / step_s / 1e9 / peak,
+                              "note": "SURVEY §8d B_alg = 292n + 48nnz + 12W charges the "
+                                      "paper's W-cost SpGEMM traffic; the degree-oriented "
+                                      "kernels do far less work, so this is NOT a roofline"},
+        "dominant_kernel": dominant,
+        "phases_ms": {k: v["ms"] for k, v in phases.items()},
+        "reference_steps_ms": steps_ref,
+    }
 
     # device ingest: raw edge sample -> sanitised CSR
     ingest = None
@@ -390,7 +506,7 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_leg()
+        cpu = cpu_baseline_leg(rp_h, ci_h, name, args.config)
 
     value = m / (t_ms * 1e-3)
     line = {
@@ -407,17 +523,7 @@ def main():
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "api": "fglt_ctx_transform (C-ABI) with pinned host buffers" if world == 1
                 else "sharded_transform with rank-0 pinned host copies"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "scope": "whole transform step (all kernels); B_alg = 292n + 48nnz + 12W "
-                              f"= {balg} bytes (SURVEY §8d paper formulation)",
-                     "note": "work-reduced vs paper formulation: degree-oriented enumeration "
-                             "does less than the 12W index/value traffic the model charges",
-                     "peak_kind": peak_kind, "traffic_source": traffic_src,
-                     "dominant_phase": dominant_phase(dom, t_ms, nnz, W, peak),
-                     "dominant_kernel": dominant_kernel(summ, t_ms, peak),
-                     "measured_dram_gbs": (traffic / (t_ms * 1e-3) / 1e9) if traffic else None,
-                     "phases_ms": phases},
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "ingest": ingest,
         "gpu_launches": launches,

@@ -62,6 +62,7 @@ typedef struct fglt_error {
 } fglt_error;
 
 #define FGLT_MAX_STEPS 12
+#define FGLT_MAX_PHASES 16
 /* Mirrors TransformStats (kernels.hpp:105-112) plus device facts. */
 typedef struct fglt_stats {
   int32_t num_steps;
@@ -75,7 +76,15 @@ typedef struct fglt_stats {
   int32_t device;
   uint64_t W;                /* sum_v d_v^2                              */
   uint64_t d_max;
-  uint64_t kernel_launches;  /* kernels this library launched            */
+  uint64_t kernel_launches;  /* kernels this library launched (this call) */
+  /* FGLT_TIMINGS only: device phases of this call (CUDA events on the
+   * context's stream), finer than the reference steps, e.g. "c4 dense" =
+   * the dense-tile 4-cycle kernels; phase_units = their algorithmic work
+   * units (wedges for the 4-cycle phases, 0 when not defined). */
+  int32_t num_phases;
+  char phase_names[FGLT_MAX_PHASES][32];
+  double phase_seconds[FGLT_MAX_PHASES];
+  uint64_t phase_units[FGLT_MAX_PHASES];
 } fglt_stats;
 
 /* Opaque per-device context: stream, workspace, cached preprocessing. One
@@ -198,6 +207,10 @@ int fglt_kernel_d13(fglt_ctx* ctx, const int32_t* row_ptr, const int32_t* col_id
                     int64_t nnz, const uint64_t* C3, uint64_t* d13, fglt_error* err);
 /* Number of kernels this context has launched so far (CUB calls count 1). */
 uint64_t fglt_ctx_kernel_launches(const fglt_ctx* ctx);
+/* Device buffers the last call used, one "name bytes [staging]" line each
+ * (staging = the graph copy, the output tables and their raw columns, which
+ * TransformStats.peak_aux_words does not count). */
+int fglt_ctx_scratch_report(const fglt_ctx* ctx, char* out, int len);
 
 /* Test hooks: force one internal code path for every root so small graphs
  * exercise paths that otherwise only large graphs reach. Results must be
@@ -208,6 +221,11 @@ uint64_t fglt_ctx_kernel_launches(const fglt_ctx* ctx);
 #define FGLT_DEBUG_HUB 4       /* 0 auto, 1 no hub rows, 2 hub rows for every hub member */
 #define FGLT_DEBUG_TRILIST 5   /* 0 auto, 1 no triangle list, 2 tiny list pool (fallbacks) */
 int fglt_ctx_set_debug(fglt_ctx* ctx, int key, int value);
+
+/* Measured random-address shared-memory atomicAdd rate (ops/s) of this
+ * device at the dense 4-cycle kernel's tile size and occupancy: the on-chip
+ * roofline denominator bench.py reports for that kernel. */
+int fglt_probe_smem_atomics(fglt_ctx* ctx, double* ops_per_s, fglt_error* err);
 
 /* Library facts */
 const char* fglt_version(void);

@@ -26,7 +26,8 @@ EXPORTS = [
     "fglt_stage_local", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
     "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug", "fglt_build_csr",
     "fglt_csr_fetch", "fglt_kernel_p2", "fglt_kernel_c3", "fglt_kernel_p3", "fglt_kernel_d7",
-    "fglt_kernel_d8", "fglt_kernel_d9_d10_d11", "fglt_kernel_d13",
+    "fglt_kernel_d8", "fglt_kernel_d9_d10_d11", "fglt_kernel_d13", "fglt_probe_smem_atomics",
+    "fglt_ctx_scratch_report",
 ]
 
 DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB, DEBUG_TRILIST = 1, 2, 3, 4, 5
@@ -39,6 +40,7 @@ class FgltError(ctypes.Structure):
 
 
 MAX_STEPS = 12
+MAX_PHASES = 16
 
 
 class FgltStats(ctypes.Structure):
@@ -49,7 +51,11 @@ class FgltStats(ctypes.Structure):
                 ("peak_aux_words", ctypes.c_uint64), ("largest_aux_alloc_words", ctypes.c_uint64),
                 ("threads_used", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("W", ctypes.c_uint64), ("d_max", ctypes.c_uint64),
-                ("kernel_launches", ctypes.c_uint64)]
+                ("kernel_launches", ctypes.c_uint64),
+                ("num_phases", ctypes.c_int32),
+                ("phase_names", (ctypes.c_char * 32) * MAX_PHASES),
+                ("phase_seconds", ctypes.c_double * MAX_PHASES),
+                ("phase_units", ctypes.c_uint64 * MAX_PHASES)]
 
     def as_dict(self):
         return {
@@ -60,6 +66,8 @@ class FgltStats(ctypes.Structure):
             "largest_aux_alloc_words": self.largest_aux_alloc_words,
             "threads_used": self.threads_used, "device": self.device, "W": self.W,
             "d_max": self.d_max, "kernel_launches": self.kernel_launches,
+            "phases": [(self.phase_names[i].value.decode(), self.phase_seconds[i],
+                        int(self.phase_units[i])) for i in range(self.num_phases)],
         }
 
 
@@ -122,6 +130,11 @@ def lib():
         L.fglt_ctx_set_debug.argtypes = [vp, ctypes.c_int, ctypes.c_int]
         L.fglt_ctx_kernel_launches.restype = ctypes.c_uint64
         L.fglt_ctx_kernel_launches.argtypes = [vp]
+        L.fglt_ctx_scratch_report.restype = ctypes.c_int
+        L.fglt_ctx_scratch_report.argtypes = [vp, ctypes.c_char_p, ctypes.c_int]
+        L.fglt_probe_smem_atomics.restype = ctypes.c_int
+        L.fglt_probe_smem_atomics.argtypes = [vp, ctypes.POINTER(ctypes.c_double),
+                                              ctypes.POINTER(FgltError)]
         L.fglt_version.restype = ctypes.c_char_p
         L.fglt_version.argtypes = []
         L.fglt_device_count.restype = ctypes.c_int
@@ -193,6 +206,25 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(self._L.fglt_ctx_kernel_launches(self._h))
+
+    def scratch_report(self):
+        """{buffer: (bytes, staging)} of the last call (see fglt.h)."""
+        buf = ctypes.create_string_buffer(1 << 14)
+        self._L.fglt_ctx_scratch_report(self._h, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            f = line.split()
+            out[f[0]] = (int(f[1]), len(f) > 2)
+        return out
+
+    def smem_atomic_rate(self) -> float:
+        """Measured random shared-memory atomicAdd ops/s (on-chip roofline)."""
+        out = ctypes.c_double(0)
+        err = FgltError()
+        rc = self._L.fglt_probe_smem_atomics(self._h, ctypes.byref(out), ctypes.byref(err))
+        if rc:
+            _raise(rc, err)
+        return float(out.value)
 
     def release_workspace(self):
         """Free the device workspace kept between calls (see include/fglt.h)."""

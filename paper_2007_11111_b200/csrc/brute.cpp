@@ -183,7 +183,7 @@ CrossCheckReport cross_check(const SparseAdjacency& g, const RawFrequencyField& 
 count_t count_triangles(const SparseAdjacency& g) {
   count_t t = 0;
   for_each_connected_set(g, [&](const std::array<vertex_t, 4>&, int k, unsigned em) {
-    t += k == 3 && em == 7u;
+    t += k == 3 && em == 0xBu;  // pairs (0,1), (0,2), (1,2) = bits 0, 1, 3
   });
   return t;
 }

@@ -38,6 +38,9 @@ namespace {
 #ifndef FGLT_TL_MEM_FRAC
 #define FGLT_TL_MEM_FRAC 0.70  // triangle-list pool: at most this share of the free HBM
 #endif
+#ifndef FGLT_TL_MIN_RECORDS
+#define FGLT_TL_MIN_RECORDS (1ull << 20)  // smaller record bounds: no triangle list
+#endif
 #ifndef FGLT_MIRROR_SORT_DEG
 #define FGLT_MIRROR_SORT_DEG 8  // mean degree from which mirror slots come from a transpose sort
 #endif
@@ -61,17 +64,29 @@ enum Buf {
   B_COUNT
 };
 
+const char* const kBufName[] = {
+  "rp_in", "ci_in", "keys", "keys2", "perm", "inv", "ndeg", "nrp", "nci", "tmp_c3",
+  "split", "outdeg", "orp", "mir", "ce_row", "ce_pos", "vec", "work", "binkey", "lists",
+  "cub", "cursor", "tbnd", "bigrows", "hub", "hubbase", "rowof", "keysout", "gbm", "raw", "net",
+  "dict", "small", "rlists", "rkey",
+  "ing_e", "ing_k", "ing_k2", "ing_rp", "ing_ci", "send", "sortk", "sortv",
+  "api0", "api1", "api2", "api3", "api4", "api5", "tb", "tlrec", "tlpieces", "tlfail", "tbs",
+  "tbnds", "cursors", "tlchunks"};
+static_assert(sizeof(kBufName) / sizeof(kBufName[0]) == B_COUNT, "buffer names");
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
   uint64_t call = 0;  // last call that used this buffer (per-call accounting)
 };
 
-// Staging copies of the caller's CSR and of the output tables: the graph and
-// the result fields, which the reference's MemoryTracker does not count as
-// auxiliary scratch (proj/include/graphlet/instrumentation.hpp:9-15).
+// Staging copies of the caller's CSR and of the output tables, and B_VEC (the
+// raw columns p2, d7, c3, ... before the fill): the graph and the result
+// fields, which the reference's MemoryTracker does not count as auxiliary
+// scratch either (proj/include/graphlet/instrumentation.hpp:9-15; its
+// per-vertex columns are untracked std::vectors, kernels.cpp:305-419).
 inline bool is_staging(int b) {
-  return b == B_RP_IN || b == B_CI_IN || b == B_RAW || b == B_NET;
+  return b == B_RP_IN || b == B_CI_IN || b == B_RAW || b == B_NET || b == B_VEC;
 }
 
 // Per-vertex vectors, each n u64, in B_VEC.
@@ -236,9 +251,13 @@ struct fglt_ctx {
   // timing
   bool timing = false;
   std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  // algorithmic work units of a phase, read after the call's final sync:
+  // phase name -> device u64 slot
+  std::vector<std::pair<std::string, const u64*>> unit_slots;
 
   void begin_call() {
     ++call;
+    unit_slots.clear();
     call_bytes = peak_scratch = largest = 0;
     launches_at_call = launches;
   }
@@ -772,14 +791,15 @@ void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
   if (!(P.c3 && P.d13) || c->tl_mode == 1 || u1 <= u0) return;
   unsigned long long* d_bound = reinterpret_cast<unsigned long long*>(c->d_small + 24);
   CK(cudaMemsetAsync(d_bound, 0, 4 * sizeof(u64), c->stream));
-  k_trilist_bound<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(c->split, c->send, (int)u0,
-                                                               (int)u1, d_bound);
+  k_trilist_bound<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(c->split, c->send, c->ci,
+                                                               (int)u0, (int)u1, d_bound);
   check_launch();
   c->launched();
   unsigned long long bound = 0;
   CK(cudaMemcpyAsync(&bound, d_bound, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  if (bound == 0) return;
+  // small graphs: the probing diamond pass is cheap, a pool is not worth it
+  if (bound < FGLT_TL_MIN_RECORDS && c->tl_mode != 2) return;
   // slack for the reservations the launched blocks and warps hold at once
   // (each grabs >= kTriListChunk / kTriListWarpChunk records): bounded by the
   // grids roots_pass actually launches, so the pool follows the graph size
@@ -846,9 +866,11 @@ void triangles(fglt_ctx* c, int64_t u0, int64_t u1) {
   setup_trilist(c, u0, u1);
   c->tl_u0 = u0;
   c->tl_u1 = u1;
+  c->mark("triangle pass:start");
   if (P.c3 && P.d15) roots_pass<true, false, true>(c);
   else if (P.c3) roots_pass<true, false, false>(c);
   else roots_pass<false, false, true>(c);
+  c->mark("triangle pass:end");
 }
 
 void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
@@ -873,9 +895,14 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       CK(cudaMemcpyAsync(bands, d_b, sizeof(bands), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
     }
+    unsigned long long* cw = reinterpret_cast<unsigned long long*>(c->d_small + 32);
+    CK(cudaMemsetAsync(cw, 0, 2 * sizeof(u64), c->stream));
+    c->unit_slots.push_back({"c4 dense", c->d_small + 32});
+    c->unit_slots.push_back({"c4 classes", c->d_small + 33});
+    c->mark("c4 classes:start");
     k_c4_class<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(
         c->rp, c->split, wc, (int)u0, (int)u1, bands[0], bands[1], bands[2], cls, parts,
-        c->force_c4_class, c->force_c4_parts);
+        c->force_c4_class, c->force_c4_parts, cw);
     check_launch();
     c->launched();
     std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6, 7}, lists, &stride);
@@ -884,7 +911,9 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     for (int bb = 3; bb <= 6; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc, wbits);
     int* queues = reinterpret_cast<int*>(c->d_small + 56);  // dynamic root queues
     CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
+    c->mark("c4 classes:end");
     c->mark("four-cycle rows:start");
+    c->mark("c4 hash:start");
     u64* c4 = c->V(V_C4);
     if (cnt[0] > 0) {  // class 1: warp tables of 512 slots
       const int wpb = 8;
@@ -941,6 +970,8 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       check_launch();
       c->launched();
     }
+    c->mark("c4 hash:end");
+    c->mark("c4 dense:start");
     // classes 5/6 (big tiles) and 7 (small tiles): banded tile starts
     // (dense_span) and the absolute tile boundaries of the active rows
     const long long nact = (long long)c->nact;
@@ -1025,14 +1056,19 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
       check_launch();
       c->launched();
     }
+    c->mark("c4 dense:end");
     c->mark("four-cycle rows:end");
   }
   if (P.d13) {
     root_bins(c, u0, u1);
     c->mark("roots:start");
     if (c->tl_u0 != u0 || c->tl_u1 != u1) c->tl = TriList{};  // list of another range
+    c->mark("diamond list:start");
     diamond_list(c);
+    c->mark("diamond list:end");
+    c->mark("diamond probe:start");
     roots_pass<false, true, false>(c);
+    c->mark("diamond probe:end");
     c->mark("roots:end");
   }
 }
@@ -1136,6 +1172,25 @@ void fill_stats(fglt_ctx* c, fglt_stats* st, const std::vector<std::pair<std::st
   st->threads_used = 1;
   st->device = c->device;
   st->kernel_launches = c->launches - c->launches_at_call;
+  // every measured phase (reference steps and the finer device phases)
+  std::vector<std::pair<std::string, u64>> units;
+  if (!t.empty())
+    for (auto& us : c->unit_slots) {
+    u64 v = 0;
+    CK(cudaMemcpy(&v, us.second, 8, cudaMemcpyDeviceToHost));
+    units.push_back({us.first, v});
+  }
+  int np = 0;
+  for (auto& kv : t) {
+    if (np >= FGLT_MAX_PHASES) break;
+    std::snprintf(st->phase_names[np], 32, "%s", kv.first.c_str());
+    st->phase_seconds[np] = kv.second;
+    st->phase_units[np] = 0;
+    for (auto& u : units)
+      if (u.first == kv.first) st->phase_units[np] = u.second;
+    ++np;
+  }
+  st->num_phases = np;
 }
 
 std::vector<std::pair<std::string, double>> collect_marks(fglt_ctx* c) {
@@ -1179,10 +1234,37 @@ int validate_shape(int64_t n, int64_t nnz, fglt_error* err) {
 
 }  // namespace
 
+__global__ void __launch_bounds__(512, 2) k_probe_smem_atomics(int iters, unsigned words,
+                                                                u64* __restrict__ sink) {
+  extern __shared__ unsigned Lp[];
+  for (unsigned i = threadIdx.x; i < words; i += blockDim.x) Lp[i] = 0;
+  __syncthreads();
+  unsigned x = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  for (int i = 0; i < iters; ++i) {
+    x ^= x << 13;
+    x ^= x >> 17;
+    x ^= x << 5;
+    atomicAdd(Lp + (x % words), 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sink[blockIdx.x] = Lp[0];
+}
+
 // =================================================================== C-ABI
 extern "C" {
 
 uint64_t fglt_ctx_kernel_launches(const fglt_ctx* c) { return c ? c->launches : 0; }
+
+int fglt_ctx_scratch_report(const fglt_ctx* c, char* out, int len) {
+  if (!c || !out || len <= 0) return FGLT_E_NO_DEVICE;
+  std::string r;
+  for (int b = 0; b < B_COUNT; ++b)
+    if (c->buf[b].p && c->buf[b].call == c->call)
+      r += std::string(kBufName[b]) + " " + std::to_string(c->buf[b].cap) +
+           (is_staging(b) ? " staging\n" : "\n");
+  std::snprintf(out, (size_t)len, "%s", r.c_str());
+  return FGLT_OK;
+}
 
 int fglt_build_csr(fglt_ctx* c, const int64_t* eu, const int64_t* ev, int64_t ne,
                    int64_t declared_n, int symmetrize, int drop_self_loops, int dedupe,
@@ -1352,7 +1434,41 @@ int fglt_ctx_set_debug(fglt_ctx* c, int key, int value) {
   }
 }
 
-const char* fglt_version(void) { return "fglt-b200 0.1 (sm_100a)"; }
+const char* fglt_version(void) { return "fglt-b200 0.2 (sm_100a)"; }
+
+// Measured on-chip ceiling for the roofline of the dense 4-cycle kernel:
+// random-address 32-bit shared-memory atomicAdd throughput with that
+// kernel's tile size (96 KB) and occupancy (two 512-thread blocks per SM).
+int fglt_probe_smem_atomics(fglt_ctx* c, double* ops_per_s, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!c) return FGLT_E_NO_DEVICE;
+  try {
+    CK(cudaSetDevice(c->device));
+    constexpr int kNT = 512, kIters = 4096;
+    constexpr unsigned kWords = 98304 / 4;
+    const int g = c->sms * 2;
+    u64* sink = c->ensure<u64>(B_API5, (size_t)g);
+    set_smem(k_probe_smem_atomics, kWords * 4);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    k_probe_smem_atomics<<<g, kNT, kWords * 4, c->stream>>>(kIters, kWords, sink);  // warm-up
+    CK(cudaEventRecord(e0, c->stream));
+    k_probe_smem_atomics<<<g, kNT, kWords * 4, c->stream>>>(kIters, kWords, sink);
+    CK(cudaEventRecord(e1, c->stream));
+    check_launch();
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ops_per_s = (double)g * kNT * kIters / (ms * 1e-3);
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
 
 int fglt_device_count(void) {
   int c = 0;
@@ -1457,16 +1573,22 @@ int fglt_ctx_transform(fglt_ctx* c, const int32_t* row_ptr, const int32_t* col_i
       d_rp = a;
       d_ci = b;
     }
+    c->mark("prepare:start");
     prepare(c, d_rp, d_ci, n, nnz, dict_mask, lenient);
     if (c->plan.enumerate && !c->have_stats && n > 0) {
       // d_max sizes the 4-cycle cursor slices, max |N+(u)| the root bins
       read_graph_stats(c);
     }
+    c->mark("prepare:end");
+    c->mark("sweep A:start");
     sweep_a(c);
+    c->mark("sweep A:end");
     c->mark("degrees:end");
     c->mark("triangles:start");
     triangles(c, 0, n);
+    c->mark("sweeps B/C:start");
     local_sweeps(c);
+    c->mark("sweeps B/C:end");
     c->mark("triangles:end");
     roots(c, 0, n);
     const size_t k = (size_t)c->dict.k;

@@ -347,7 +347,10 @@ __host__ __device__ inline void dense_span(u64 u, u64 b4, u64 b8, u64 b16, u64 t
 __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
                            const u64* __restrict__ wc, int u0, int u1, int b4, int b8, int b16,
                            u64* __restrict__ cls, u64* __restrict__ parts, int force_cls,
-                           int force_parts) {
+                           int force_parts, unsigned long long* __restrict__ class_wedges) {
+  // class_wedges[0] += wedges of the dense-tile roots (classes 5/6/7),
+  // class_wedges[1] += all wedges (the 4-cycle phases' work units)
+  unsigned long long dense_w = 0, all_w = 0;
   for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1;
        u += gridDim.x * blockDim.x) {
     const u64 w = wc[u];
@@ -397,6 +400,14 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
     }
     cls[u] = c;
     parts[u] = P;
+    all_w += w;
+    if (c >= 5 && c <= 7) dense_w += w;
+  }
+  dense_w = warp_sum_u64(dense_w);
+  all_w = warp_sum_u64(all_w);
+  if ((threadIdx.x & 31) == 0) {
+    if (dense_w) atomicAdd(class_wedges, dense_w);
+    if (all_w) atomicAdd(class_wedges + 1, all_w);
   }
 }
 
@@ -2033,12 +2044,29 @@ k_diamond_wlist(const TriChunk* __restrict__ chunks, const unsigned* __restrict_
 
 // Sum over roots u in [u0, u1) with 2 <= |N+(u)| <= kTriListMaxS of
 // C(|N+(u)|, 2) (+1 header for warp roots): an upper bound of the records.
+#ifndef FGLT_TL_TIGHT
+#define FGLT_TL_TIGHT 1
+#endif
 __global__ void k_trilist_bound(const int* __restrict__ split, const int* __restrict__ send,
-                                int u0, int u1, unsigned long long* __restrict__ out) {
+                                const int* __restrict__ ci, int u0, int u1,
+                                unsigned long long* __restrict__ out) {
   unsigned long long acc = 0;
   for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1; u += gridDim.x * blockDim.x) {
     const unsigned long long s = (unsigned long long)(send[u] - split[u]);
-    if (s >= 2 && s <= (unsigned long long)kTriListMaxS) acc += s * (s - 1) / 2 + (s <= 32);
+    if (s >= 2 && s <= (unsigned long long)kTriListMaxS) {
+      unsigned long long b = s * (s - 1) / 2;
+#if FGLT_TL_TIGHT
+      // a triangle {u, x, y} (x < y) is found from x as y in N+(x): at most
+      // sum_x |N+(x)| of them
+      unsigned long long o = 0;
+      for (int p = split[u]; p < send[u] && o < b; ++p) {
+        const int x = ci[p];
+        o += (unsigned long long)(send[x] - split[x]);
+      }
+      b = o < b ? o : b;
+#endif
+      acc += b + (s <= 32);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -2323,6 +2351,25 @@ __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue(EpilogueIn in, co
 // Whole-table variant (rows [0, n)): walks the vector rows r in order (every
 // vector read coalesced) and writes each row to its original id perm[r] as
 // whole 16-byte units (a full 128-byte line per table when k = 16).
+// Full dictionary, 16-byte aligned tables: a warp stages its 32 rows in
+// shared memory and writes every table row as one coalesced 128-byte line
+// (8 lanes x 16 bytes, 4 rows per store instruction) instead of 32 scattered
+// 16-byte pieces per instruction.
+constexpr int kEpiStride = 18;  // u64 per staged row: 16 + 2 (16-byte aligned, bank spread)
+__device__ __forceinline__ void epi_store_lines(const u64* __restrict__ st, int lane, int base,
+                                                int n, int v_lane, u64* __restrict__ table) {
+  const int c = lane & 7;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int j = it * 4 + (lane >> 3);
+    const int vj = __shfl_sync(0xffffffffu, v_lane, j);
+    if (base + j < n) {
+      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(st + j * kEpiStride + 2 * c);
+      *reinterpret_cast<ulonglong2*>(table + (long long)vj * 16 + 2 * c) = x;
+    }
+  }
+}
+
 template <bool kFull>
 __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue_rank(
     EpilogueIn in, const int* __restrict__ perm, const DictInfo* __restrict__ dict, int n,
@@ -2331,6 +2378,34 @@ __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue_rank(
   if (threadIdx.x == 0) D = *dict;
   __syncthreads();
   const int k = D.k;
+  if (kFull && ((reinterpret_cast<unsigned long long>(raw) |
+                 reinterpret_cast<unsigned long long>(net)) & 15ull) == 0) {
+    __shared__ __align__(16) u64 stage[kEpilogueThreads / 32][2][32 * kEpiStride];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    u64* sr = stage[wid][0];
+    u64* sn = stage[wid][1];
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) << 5; base < n;
+         base += warps << 5) {
+      const int r = base + lane;
+      int v = 0;
+      if (r < n) {
+        v = perm[r];
+        u64 rw[16], nt[16];
+        epi_row_full(in, D, v, r, lenient, net != nullptr, err, rw, nt);
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          *reinterpret_cast<ulonglong2*>(sr + lane * kEpiStride + i) = make_ulonglong2(rw[i], rw[i + 1]);
+          *reinterpret_cast<ulonglong2*>(sn + lane * kEpiStride + i) = make_ulonglong2(nt[i], nt[i + 1]);
+        }
+      }
+      __syncwarp();
+      if (raw) epi_store_lines(sr, lane, base, n, v, raw);
+      if (net) epi_store_lines(sn, lane, base, n, v, net);
+      __syncwarp();
+    }
+    return;
+  }
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const int v = perm[r];
     const long long o = (long long)v * k;
