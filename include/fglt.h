@@ -117,6 +117,21 @@ int fglt_transform_csr32(const int32_t* row_ptr, const int32_t* col_idx,
                          uint64_t* raw_out, uint64_t* net_out,
                          fglt_stats* stats, fglt_error* err);
 
+/* Single-process multi-GPU transform: the CSR is broadcast
+ * from devices[0] over NCCL, enumeration roots are split into blocks of equal
+ * exact work, the per-edge C3 and the c4/d13/d15 partials are all-reduced
+ * (NCCL), and each device writes its block of original-id rows straight
+ * into raw_out/net_out. FGLT_INPUT_DEVICE / FGLT_OUTPUT_DEVICE mean pointers
+ * on devices[0]. Bit-identical to fglt_ctx_transform for any device list.
+ * A list with repeated devices (e.g. {0, 0}) runs the ranks one after the
+ * other on the shared device with host-staged sums (the >1-rank path on a
+ * one-GPU machine). Contexts and communicators are cached per device list. */
+int fglt_transform_multi(const int32_t* row_ptr, const int32_t* col_idx,
+                         int64_t n, int64_t nnz, uint32_t dict_mask, int lenient,
+                         const int* devices, int num_devices, uint32_t flags,
+                         uint64_t* raw_out, uint64_t* net_out, fglt_stats* stats,
+                         fglt_error* err);
+
 /* Stand-alone raw -> net conversion on the device (net_from_raw,
  * conversion.cpp:80-116): raw/net are n x k host arrays for dict_mask. */
 int fglt_net_from_raw(fglt_ctx* ctx, const uint64_t* raw, int64_t n,

@@ -27,7 +27,7 @@ EXPORTS = [
     "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug", "fglt_build_csr",
     "fglt_csr_fetch", "fglt_kernel_p2", "fglt_kernel_c3", "fglt_kernel_p3", "fglt_kernel_d7",
     "fglt_kernel_d8", "fglt_kernel_d9_d10_d11", "fglt_kernel_d13", "fglt_probe_smem_atomics",
-    "fglt_ctx_scratch_report",
+    "fglt_ctx_scratch_report", "fglt_transform_multi",
 ]
 
 DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB, DEBUG_TRILIST = 1, 2, 3, 4, 5
@@ -130,6 +130,10 @@ def lib():
         L.fglt_ctx_set_debug.argtypes = [vp, ctypes.c_int, ctypes.c_int]
         L.fglt_ctx_kernel_launches.restype = ctypes.c_uint64
         L.fglt_ctx_kernel_launches.argtypes = [vp]
+        L.fglt_transform_multi.restype = ctypes.c_int
+        L.fglt_transform_multi.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32,
+                                           ctypes.c_int, vp, ctypes.c_int, ctypes.c_uint32, vp, vp,
+                                           ctypes.POINTER(FgltStats), ctypes.POINTER(FgltError)]
         L.fglt_ctx_scratch_report.restype = ctypes.c_int
         L.fglt_ctx_scratch_report.argtypes = [vp, ctypes.c_char_p, ctypes.c_int]
         L.fglt_probe_smem_atomics.restype = ctypes.c_int
@@ -165,6 +169,27 @@ class TransformFailed(RuntimeError):
 
 def _raise(rc, err):
     raise TransformFailed(rc, err.graphlet_id, err.vertex, err.msg.decode(errors="replace"))
+
+
+def transform_multi(rp: np.ndarray, ci: np.ndarray, devices, mask: int = 0xFFFF,
+                    lenient=False):
+    """fglt_transform_multi: host CSR in, host tables out, ranks on `devices`
+    (repeats = the host-staged emulation of more ranks than GPUs)."""
+    L = lib()
+    rp = np.ascontiguousarray(rp, dtype=np.int32)
+    ci = np.ascontiguousarray(ci, dtype=np.int32)
+    n, nnz = len(rp) - 1, len(ci)
+    k = len(mask_ids(mask))
+    raw = np.empty((n, k), dtype=np.uint64)
+    net = np.empty((n, k), dtype=np.uint64)
+    dev = (ctypes.c_int * len(devices))(*devices)
+    st, err = FgltStats(), FgltError()
+    rc = L.fglt_transform_multi(rp.ctypes.data, ci.ctypes.data if nnz else None, n, nnz, mask,
+                                int(lenient), dev, len(devices), 0, raw.ctypes.data,
+                                net.ctypes.data, ctypes.byref(st), ctypes.byref(err))
+    if rc:
+        _raise(rc, err)
+    return raw, net, st.as_dict()
 
 
 class Context:

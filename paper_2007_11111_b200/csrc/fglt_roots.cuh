@@ -2202,39 +2202,37 @@ __device__ __forceinline__ void epi_row_full(const EpilogueIn& in, const DictInf
   col[14] = in.d14 ? in.d14[r] : 0;
   col[15] = in.d15 ? in.d15[r] : 0;
   // full dictionary: identity column map and the constant U16, fully
-  // unrolled so every table stays in registers
+  // unrolled with no data-dependent control flow. Every row is computed; the
+  // reported failure is the first one of the reference's downward walk (the
+  // highest failing row: rows below it only see values the walk never
+  // produces).
 #pragma unroll
   for (int i = 0; i < 16; ++i) rw[i] = col[i];
-  bool stop = !want_net;
+  if (!want_net) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) nt[i] = 0;
+    return;
+  }
+  int bad_r = -1, bad_code = 0;
 #pragma unroll
   for (int rr = 15; rr >= 0; --rr) {
-    nt[rr] = 0;
-    if (stop) continue;
     u64 absorbed = 0;
-    bool bad = false;
+    bool ov = false;
 #pragma unroll
     for (int cc = rr + 1; cc < 16; ++cc) {
       if (u16_coef(rr, cc) == 0) continue;
       u64 prod;
-      if (!bad && (mul_ov((u64)u16_coef(rr, cc), nt[cc], &prod) || add_ov(absorbed, prod, &absorbed)))
-        bad = true;
+      ov |= mul_ov((u64)u16_coef(rr, cc), nt[cc], &prod);
+      ov |= add_ov(absorbed, prod, &absorbed);
     }
-    if (bad) {
-      offer_err(err, 6, v, 0, rr);
-      stop = true;
-      continue;
-    }
-    if (absorbed > rw[rr]) {
-      if (!lenient) {
-        offer_err(err, 6, v, 1, rr);
-        stop = true;
-        continue;
-      }
-      nt[rr] = 0;
-    } else {
-      nt[rr] = rw[rr] - absorbed;
+    const bool neg = absorbed > rw[rr];
+    nt[rr] = neg ? 0ull : rw[rr] - absorbed;
+    if (bad_r < 0 && (ov || (neg && !lenient))) {
+      bad_r = rr;
+      bad_code = ov ? 0 : 1;
     }
   }
+  if (bad_r >= 0) offer_err(err, 6, v, bad_code, bad_r);
 }
 
 __device__ __forceinline__ void epi_row(const EpilogueIn& in, const DictInfo& D, int v, int r,
@@ -2380,29 +2378,40 @@ __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue_rank(
   const int k = D.k;
   if (kFull && ((reinterpret_cast<unsigned long long>(raw) |
                  reinterpret_cast<unsigned long long>(net)) & 15ull) == 0) {
-    __shared__ __align__(16) u64 stage[kEpilogueThreads / 32][2][32 * kEpiStride];
+    __shared__ __align__(16) u64 stage[kEpilogueThreads / 32][32 * kEpiStride];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    u64* sr = stage[wid][0];
-    u64* sn = stage[wid][1];
+    u64* sr = stage[wid];
     const int warps = (gridDim.x * blockDim.x) >> 5;
     for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) << 5; base < n;
          base += warps << 5) {
       const int r = base + lane;
       int v = 0;
+      u64 rw[16], nt[16];
       if (r < n) {
         v = perm[r];
-        u64 rw[16], nt[16];
         epi_row_full(in, D, v, r, lenient, net != nullptr, err, rw, nt);
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          *reinterpret_cast<ulonglong2*>(sr + lane * kEpiStride + i) = make_ulonglong2(rw[i], rw[i + 1]);
-          *reinterpret_cast<ulonglong2*>(sn + lane * kEpiStride + i) = make_ulonglong2(nt[i], nt[i + 1]);
-        }
       }
-      __syncwarp();
-      if (raw) epi_store_lines(sr, lane, base, n, v, raw);
-      if (net) epi_store_lines(sn, lane, base, n, v, net);
-      __syncwarp();
+      // raw rows, then net rows, through the same staging lines
+      if (raw) {
+        if (r < n) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 2)
+            *reinterpret_cast<ulonglong2*>(sr + lane * kEpiStride + i) = make_ulonglong2(rw[i], rw[i + 1]);
+        }
+        __syncwarp();
+        epi_store_lines(sr, lane, base, n, v, raw);
+        __syncwarp();
+      }
+      if (net) {
+        if (r < n) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 2)
+            *reinterpret_cast<ulonglong2*>(sr + lane * kEpiStride + i) = make_ulonglong2(nt[i], nt[i + 1]);
+        }
+        __syncwarp();
+        epi_store_lines(sr, lane, base, n, v, net);
+        __syncwarp();
+      }
     }
     return;
   }
