@@ -249,3 +249,18 @@ def ref_build_adjacency(eu, ev, declared_n=0, symmetrize=True, drop_self_loops=T
         raise e
     n, nnz = int(out[0]), int(out[1])
     return rp[:n + 1].copy(), ci[:nnz].copy(), int(out[2]), int(out[3])
+
+
+def ref_parse_dictionary(spec: str):
+    """The reference's parse_dictionary: (ids, implicitly_added) or raises
+    ValueError(message)."""
+    L = ref()
+    L.fglt_ref_parse_dictionary.restype = ctypes.c_int
+    L.fglt_ref_parse_dictionary.argtypes = [ctypes.c_char_p, vp, vp, ctypes.c_char_p, ctypes.c_int]
+    ids = np.zeros(1, np.uint32)
+    imp = np.zeros(1, np.uint32)
+    msg = ctypes.create_string_buffer(256)
+    if L.fglt_ref_parse_dictionary(spec.encode(), ids.ctypes.data, imp.ctypes.data, msg, 256):
+        raise ValueError(msg.value.decode())
+    return ([i for i in range(16) if int(ids[0]) >> i & 1],
+            [i for i in range(16) if int(imp[0]) >> i & 1])

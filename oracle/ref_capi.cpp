@@ -114,6 +114,23 @@ int fglt_ref_transform_csr32(const int32_t* rp, const int32_t* ci, int64_t n,
 
 const char* fglt_ref_last_stats(void) { return g_last_stats.c_str(); }
 
+// parse_dictionary (proj/src/dictionary.cpp): ids and implicitly added ids
+// as bit masks; returns 0 or 1 (ParseError, message in msg).
+int fglt_ref_parse_dictionary(const char* spec, uint32_t* ids_mask, uint32_t* implicit_mask,
+                              char* msg, int msglen) {
+  try {
+    ParsedDictionary p = parse_dictionary(spec);
+    *ids_mask = 0;
+    for (int id : p.dict.ids()) *ids_mask |= 1u << id;
+    *implicit_mask = 0;
+    for (int id : p.implicitly_added) *implicit_mask |= 1u << id;
+    return 0;
+  } catch (const ParseError& e) {
+    put_msg(msg, msglen, e.what());
+    return 1;
+  }
+}
+
 // build_adjacency (proj/src/graph.cpp:192-249) on (eu[i], ev[i]) pairs with
 // SanitizeOptions; rp/ci caller-allocated (n_max + 1, 2 ne); out4 = {n, nnz,
 // self_loops_dropped, duplicates_merged}. Returns 0 or 2 (StructuralError).

@@ -122,14 +122,10 @@ Plan make_plan(unsigned mask) {
   p.d15 = has(15);
   p.c3 = any({4, 5, 6, 9, 10, 11, 13, 14});
   p.enumerate = p.c3 || p.c4 || p.d13 || p.d15;
-  // reference plan (resolve_dependencies, src/dictionary.cpp:143-158)
-  p.ref_steps.push_back("degrees");
-  if (any({4, 5, 6, 9, 10, 11, 13})) p.ref_steps.push_back("triangles");
-  if (any({2, 5, 6})) p.ref_steps.push_back("two-paths");
-  if (any({5})) p.ref_steps.push_back("three-paths");
-  if (any({12, 14})) p.ref_steps.push_back("four-cycle rows");
-  if (any({13})) p.ref_steps.push_back("diamond rows");
-  if (any({15})) p.ref_steps.push_back("tetrahedra");
+  // reference plan (resolve_dependencies, src/dictionary.cpp:143-158), from
+  // the shared step table
+  for (const auto& st : fglt_tables::kAuxSteps)
+    if (mask & st.needed_by) p.ref_steps.push_back(st.name);
   p.ref_steps.push_back("column fill");
   p.ref_steps.push_back("conversion");
   return p;
@@ -146,7 +142,7 @@ DictInfo make_dict(unsigned mask) {
   for (int r = 0; r < d.k; ++r) {
     int t = 0;
     for (int c = r + 1; c < d.k; ++c) {
-      unsigned coef = kU16[d.ids[r]][d.ids[c]];
+      unsigned coef = fglt_tables::u16_coef(d.ids[r], d.ids[c]);
       if (coef) {
         d.tail_col[r][t] = c;
         d.tail_coef[r][t] = coef;

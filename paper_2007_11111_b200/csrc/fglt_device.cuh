@@ -22,6 +22,25 @@
 
 #include <cstdint>
 
+// Device bounds checks of the hot kernels' indexed accesses (shared-memory
+// tiles, triangle-list records, cursors, table rows): compiled in with
+// -DFGLT_DEBUG_BOUNDS (tools/build_variant.sh checked -DFGLT_DEBUG_BOUNDS);
+// a violation prints and abandons the offending thread's work, so the
+// parity check of the same run fails too. Off in the product build.
+#ifdef FGLT_DEBUG_BOUNDS
+#include <cstdio>
+#define FGLT_BOUNDS(cond, tag, a, b)                                                   \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("FGLT bounds %s: %lld %lld (block %d thread %d)\n", tag, (long long)(a),   \
+             (long long)(b), blockIdx.x, threadIdx.x);                                 \
+      return;                                                                          \
+    }                                                                                  \
+  } while (0)
+#else
+#define FGLT_BOUNDS(cond, tag, a, b) do { } while (0)
+#endif
+
 namespace fglt {
 
 typedef unsigned long long u64;

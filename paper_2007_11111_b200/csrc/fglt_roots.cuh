@@ -4,21 +4,8 @@
 #pragma once
 
 #include "fglt_device.cuh"
+#include "fglt_tables.h"
 
-#ifdef FGLT_DEBUG_BOUNDS
-#include <cstdio>
-#include <type_traits>
-#define FGLT_BOUNDS(cond, tag, a, b)                                                   \
-  do {                                                                                 \
-    if (!(cond)) {                                                                     \
-      printf("FGLT bounds %s: %lld %lld (block %d thread %d)\n", tag, (long long)(a),   \
-             (long long)(b), blockIdx.x, threadIdx.x);                                 \
-      return;                                                                          \
-    }                                                                                  \
-  } while (0)
-#else
-#define FGLT_BOUNDS(cond, tag, a, b) do { } while (0)
-#endif
 
 namespace fglt {
 
@@ -811,10 +798,13 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   int* bsb = bsb_all[wid];
   // counters of the current tile: 2^sh per 32-bit word, 32 >> sh bits each
   int sh = 0;
+  constexpr int kTileWords = (NT == kC4DenseThreadsS ? kC4TileBytesS : kC4TileBytes) / 4;
   auto inc = [&](int off) {
+    FGLT_BOUNDS(off >= 0 && (off >> sh) < kTileWords, "c4 tile inc", off, sh);
     atomicAdd(L + (off >> sh), 1u << ((off & ((1 << sh) - 1)) << (5 - sh)));
   };
   auto get = [&](int off) -> u32 {
+    FGLT_BOUNDS(off >= 0 && (off >> sh) < kTileWords, "c4 tile get", off, sh);
     const u32 x = L[off >> sh] >> ((off & ((1 << sh) - 1)) << (5 - sh));
     return sh ? x & ((1u << (32 >> sh)) - 1u) : x;
   };
@@ -1402,6 +1392,7 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
       __syncwarp();
       const unsigned cnt = *wcnt;
       if (cnt) {
+        FGLT_BOUNDS(wt + cnt < ce && ce <= tl.cap, "trilist warp chunk", wt + cnt, ce);
         if (lane == 0) tl.rec[wt] = make_uint2(0x80000000u | cnt, (u32)u);
         wt += 1 + cnt;
       }
@@ -1655,6 +1646,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
           if (lane == leader) base = atomicAdd(&s_tc, (unsigned)__popc(m));
           base = __shfl_sync(m, base, leader);
           const unsigned idx = base + __popc(m & ((1u << lane) - 1u));
+          FGLT_BOUNDS(s_tb + idx < s_te && s_te <= tl.cap, "trilist block rec", s_tb + idx, s_te);
           tl.rec[s_tb + idx] = make_uint2((u32)a | ((u32)bi << 16), (u32)p);
         }
       }
@@ -2097,53 +2089,8 @@ __device__ __forceinline__ bool add_ov(u64 a, u64 b, u64* r) {
   return *r < a;
 }
 
-// Net-to-raw coefficients U16 (Table 2; reference encoding
-// proj/src/conversion.cpp:14-32). Rows = raw graphlet, cols = net graphlet.
-constexpr unsigned char kU16[16][16] = {
-    {1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 1, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 1, 0, 2, 4, 2, 6},
-    {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 2, 2, 2, 4, 6},
-    {0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 2, 1, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 1, 1},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 0, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 2, 6},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
-};
-
-// U16 coefficient (r, c) as a compile-time constant on host and device:
-// row r packed 3 bits per column.
-__host__ __device__ constexpr unsigned long long u16_row_packed(int r) {
-  switch (r) {
-    case 0: return 0x000000000001ull;
-    case 1: return 0x000000000008ull;
-    case 2: return 0x000000002040ull;
-    case 3: return 0x000000001200ull;
-    case 4: return 0x000000001000ull;
-    case 5: return 0xca2050008000ull;
-    case 6: return 0xd12440040000ull;
-    case 7: return 0x650048200000ull;
-    case 8: return 0x240201000000ull;
-    case 9: return 0x610008000000ull;
-    case 10: return 0xc90040000000ull;
-    case 11: return 0x680200000000ull;
-    case 12: return 0x649000000000ull;
-    case 13: return 0x608000000000ull;
-    case 14: return 0x640000000000ull;
-    case 15: return 0x200000000000ull;
-    default: return 0ull;
-  }
-}
-__host__ __device__ constexpr unsigned u16_coef(int r, int c) {
-  return (unsigned)((u16_row_packed(r) >> (3 * c)) & 7ull);
-}
+// U16 coefficients: fglt_tables.h (one definition for host and device).
+using fglt_tables::u16_coef;
 
 struct EpilogueIn {
   const int* rp;   // graph the vectors are indexed by (relabelled or original)

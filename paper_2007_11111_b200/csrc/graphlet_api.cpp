@@ -20,11 +20,15 @@
 #include <string>
 
 #include "fglt.h"
+#include "fglt_tables.h"
 #include "graphlet/transform.hpp"
 
 namespace graphlet {
 
 // ================================================================ dictionary
+// Dictionaries are 16-bit id sets: every operation below works on the mask
+// (the device plan, make_plan in fglt.cu, uses the same representation and
+// the same step table, fglt_tables.h).
 namespace {
 
 // Σ16 descriptors: family order = vertex count, then edge count, then the
@@ -48,22 +52,43 @@ constexpr std::array<GraphletDescriptor, kNumGraphlets> kSigma16{{
     {15, "4-clique, at any node", 4, 6, "any vertex"},
 }};
 
-std::string_view strip_spaces(std::string_view s) {
-  std::size_t b = s.find_first_not_of(' ');
-  if (b == std::string_view::npos) return {};
-  std::size_t e = s.find_last_not_of(' ');
-  return s.substr(b, e - b + 1);
+constexpr std::uint32_t kMandatory = 0x3u;  // {0, 1} are always members
+
+[[noreturn]] void id_out_of_range(long long id) {
+  throw ParseError("graphlet id " + std::to_string(id) + " outside 0..15");
 }
 
-int graphlet_id_of(std::string_view tok) {
-  int v = -1;
-  const char* end = tok.data() + tok.size();
-  auto res = std::from_chars(tok.data(), end, v);
-  if (res.ec != std::errc{} || res.ptr != end)
+std::vector<int> ids_of_mask(std::uint32_t m) {
+  std::vector<int> out;
+  for (int id = 0; m; ++id, m >>= 1)
+    if (m & 1u) out.push_back(id);
+  return out;
+}
+
+std::string_view trim_blanks(std::string_view s) {
+  while (!s.empty() && s.front() == ' ') s.remove_prefix(1);
+  while (!s.empty() && s.back() == ' ') s.remove_suffix(1);
+  return s;
+}
+
+// One graphlet id token (decimal, whole token).
+int parse_id(std::string_view tok) {
+  int v = 0;
+  const auto [end, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), v);
+  if (ec != std::errc{} || end != tok.data() + tok.size())
     throw ParseError("malformed graphlet id '" + std::string(tok) + "'");
-  if (v < 0 || v >= kNumGraphlets)
-    throw ParseError("graphlet id " + std::to_string(v) + " outside 0..15");
+  if (v < 0 || v >= kNumGraphlets) id_out_of_range(v);
   return v;
+}
+
+// Ids named by one comma-separated item: "k" or "lo-hi" (inclusive).
+std::uint32_t item_mask(std::string_view item) {
+  const std::size_t dash = item.find('-');
+  if (dash == std::string_view::npos) return 1u << parse_id(item);
+  const int lo = parse_id(trim_blanks(item.substr(0, dash)));
+  const int hi = parse_id(trim_blanks(item.substr(dash + 1)));
+  if (hi < lo) throw ParseError("descending range '" + std::string(item) + "' in dictionary spec");
+  return ((2u << hi) - 1u) & ~((1u << lo) - 1u);
 }
 
 }  // namespace
@@ -71,33 +96,28 @@ int graphlet_id_of(std::string_view tok) {
 std::span<const GraphletDescriptor, kNumGraphlets> graphlet_descriptors() { return kSigma16; }
 
 Dictionary Dictionary::from_ids(std::span<const int> ids) {
-  std::uint32_t m = 3u;
+  std::uint32_t m = kMandatory;
   for (int id : ids) {
-    if (id < 0 || id >= kNumGraphlets)
-      throw ParseError("graphlet id " + std::to_string(id) + " outside 0..15");
+    if (id < 0 || id >= kNumGraphlets) id_out_of_range(id);
     m |= 1u << id;
   }
   Dictionary d;
-  for (int i = 0; i < kNumGraphlets; ++i)
-    if (m >> i & 1u) d.ids_.push_back(i);
+  d.ids_ = ids_of_mask(m);
   return d;
 }
 
 Dictionary Dictionary::all() {
-  std::array<int, kNumGraphlets> ids{};
-  for (int i = 0; i < kNumGraphlets; ++i) ids[i] = i;
-  return from_ids(ids);
+  Dictionary d;
+  d.ids_ = ids_of_mask((1u << kNumGraphlets) - 1u);
+  return d;
 }
 
-bool Dictionary::contains(int id) const {
-  return std::binary_search(ids_.begin(), ids_.end(), id);
-}
+bool Dictionary::contains(int id) const { return id >= 0 && id < kNumGraphlets && (mask() >> id & 1u); }
 
 std::size_t Dictionary::position_of(int id) const {
-  auto it = std::lower_bound(ids_.begin(), ids_.end(), id);
-  if (it == ids_.end() || *it != id)
-    throw Error("graphlet " + std::to_string(id) + " not in dictionary");
-  return static_cast<std::size_t>(it - ids_.begin());
+  if (!contains(id)) throw Error("graphlet " + std::to_string(id) + " not in dictionary");
+  // members below id, i.e. the popcount of the mask under bit id
+  return static_cast<std::size_t>(__builtin_popcount(mask() & ((1u << id) - 1u)));
 }
 
 std::uint32_t Dictionary::mask() const {
@@ -106,81 +126,66 @@ std::uint32_t Dictionary::mask() const {
   return m;
 }
 
+// Grammar (the reference's, proj/src/dictionary.cpp): "all", or comma-
+// separated items "k" / "lo-hi" with blanks allowed around items and dashes.
+// Items are checked left to right, so the first bad item decides the error.
 ParsedDictionary parse_dictionary(std::string_view spec) {
-  spec = strip_spaces(spec);
+  spec = trim_blanks(spec);
   if (spec.empty()) throw ParseError("empty dictionary spec");
-  std::vector<int> ids;
+  std::uint32_t named = 0;
   if (spec == "all") {
-    for (int i = 0; i < kNumGraphlets; ++i) ids.push_back(i);
+    named = (1u << kNumGraphlets) - 1u;
   } else {
-    std::size_t start = 0;
-    while (true) {
-      const std::size_t comma = spec.find(',', start);
-      const std::string_view tok = strip_spaces(
-          spec.substr(start, comma == std::string_view::npos ? std::string_view::npos
-                                                             : comma - start));
-      if (tok.empty()) throw ParseError("empty token in dictionary spec");
-      const std::size_t dash = tok.find('-');
-      if (dash == std::string_view::npos) {
-        ids.push_back(graphlet_id_of(tok));
-      } else {
-        const int lo = graphlet_id_of(strip_spaces(tok.substr(0, dash)));
-        const int hi = graphlet_id_of(strip_spaces(tok.substr(dash + 1)));
-        if (lo > hi)
-          throw ParseError("descending range '" + std::string(tok) + "' in dictionary spec");
-        for (int i = lo; i <= hi; ++i) ids.push_back(i);
-      }
-      if (comma == std::string_view::npos) break;
-      start = comma + 1;
-      if (start == spec.size()) throw ParseError("trailing comma in dictionary spec");
+    std::vector<std::string_view> items;
+    for (std::size_t at = 0;;) {
+      const std::size_t comma = std::min(spec.find(',', at), spec.size());
+      items.push_back(spec.substr(at, comma - at));
+      if (comma == spec.size()) break;
+      at = comma + 1;
+    }
+    for (std::size_t i = 0; i < items.size(); ++i) {
+      if (i + 1 == items.size() && i > 0 && items[i].empty())
+        throw ParseError("trailing comma in dictionary spec");
+      const std::string_view item = trim_blanks(items[i]);
+      if (item.empty()) throw ParseError("empty token in dictionary spec");
+      named |= item_mask(item);
     }
   }
   ParsedDictionary out;
-  out.dict = Dictionary::from_ids(ids);
-  for (int must : {0, 1})
-    if (std::find(ids.begin(), ids.end(), must) == ids.end()) out.implicitly_added.push_back(must);
+  const std::vector<int> ids = ids_of_mask(named);
+  out.dict = Dictionary::from_ids(std::span<const int>(ids.data(), ids.size()));
+  out.implicitly_added = ids_of_mask(kMandatory & ~named);
   return out;
 }
 
 const char* aux_step_name(AuxStep s) {
-  static const char* const kNames[] = {"degrees",         "triangles",    "two-paths",
-                                       "three-paths",     "four-cycle rows",
-                                       "diamond rows",    "tetrahedra"};
   const int i = static_cast<int>(s);
-  return i >= 0 && i < 7 ? kNames[i] : "?";
+  return i >= 0 && i < fglt_tables::kNumAuxSteps ? fglt_tables::kAuxSteps[i].name : "?";
 }
 
 std::vector<AuxStep> resolve_dependencies(const Dictionary& d) {
-  const std::uint32_t m = d.mask();
-  auto any = [m](std::uint32_t bits) { return (m & bits) != 0; };
-  auto bit = [](std::initializer_list<int> ids) {
-    std::uint32_t b = 0;
-    for (int i : ids) b |= 1u << i;
-    return b;
-  };
-  std::vector<AuxStep> plan{AuxStep::kDegrees};
-  if (any(bit({4, 5, 6, 9, 10, 11, 13}))) plan.push_back(AuxStep::kTriangles);
-  if (any(bit({2, 5, 6}))) plan.push_back(AuxStep::kTwoPaths);
-  if (any(bit({5}))) plan.push_back(AuxStep::kThreePaths);
-  if (any(bit({12, 14}))) plan.push_back(AuxStep::kFourCycles);
-  if (any(bit({13}))) plan.push_back(AuxStep::kDiamonds);
-  if (any(bit({15}))) plan.push_back(AuxStep::kTetrahedra);
+  std::vector<AuxStep> plan;
+  for (int i = 0; i < fglt_tables::kNumAuxSteps; ++i)
+    if (d.mask() & fglt_tables::kAuxSteps[i].needed_by) plan.push_back(static_cast<AuxStep>(i));
   return plan;
 }
 
+// A member's net count is exact only if every graphlet it is a subgraph of
+// (U16 row entries right of the diagonal) is selected too.
 std::vector<FamilyAdvisory> warn_incomplete_family(const Dictionary& d) {
-  const ConversionMatrix& u = full_u16();
   std::vector<FamilyAdvisory> out;
+  const std::uint32_t have = d.mask();
   for (int id : d.ids()) {
-    FamilyAdvisory a{id, {}, {}};
+    std::uint32_t need = 0;
     for (int c = id + 1; c < kNumGraphlets; ++c)
-      if (u.coeff(id, c) && !d.contains(c)) a.missing_supergraphs.push_back(c);
-    if (a.missing_supergraphs.empty()) continue;
-    std::ostringstream msg;
-    msg << "net counts for graphlet " << id << " (" << kSigma16[id].name
-        << ") will include non-induced occurrences: missing supergraph(s)";
-    for (int c : a.missing_supergraphs) msg << ' ' << c;
-    a.message = msg.str();
+      if (fglt_tables::u16_coef(id, c)) need |= 1u << c;
+    const std::uint32_t missing = need & ~have;
+    if (!missing) continue;
+    FamilyAdvisory a{id, ids_of_mask(missing), {}};
+    std::string msg = "net counts for graphlet " + std::to_string(id) + " (" + kSigma16[id].name +
+                      ") will include non-induced occurrences: missing supergraph(s)";
+    for (int c : a.missing_supergraphs) msg += " " + std::to_string(c);
+    a.message = std::move(msg);
     out.push_back(std::move(a));
   }
   return out;
@@ -190,32 +195,40 @@ std::vector<FamilyAdvisory> warn_incomplete_family(const Dictionary& d) {
 SparseAdjacency::SparseAdjacency(std::vector<std::int64_t> row_offsets,
                                  std::vector<vertex_t> col_indices)
     : offsets_(std::move(row_offsets)), cols_(std::move(col_indices)) {
-  n_ = offsets_.empty() ? 0 : static_cast<vertex_t>(offsets_.size()) - 1;
-  if (offsets_.empty()) offsets_.push_back(0);
-  m_ = static_cast<count_t>(cols_.size()) / 2;
-  for (vertex_t v = 0; v < n_; ++v) d_max_ = std::max(d_max_, degree(v));
+  if (offsets_.empty()) offsets_.assign(1, 0);
+  n_ = static_cast<vertex_t>(offsets_.size() - 1);
+  m_ = static_cast<count_t>(cols_.size() / 2);
+  // d_max = the largest gap between consecutive offsets
+  for (std::size_t i = 1; i < offsets_.size(); ++i)
+    d_max_ = std::max<vertex_t>(d_max_, offsets_[i] - offsets_[i - 1]);
 }
 
 bool SparseAdjacency::has_edge(vertex_t u, vertex_t v) const {
-  auto r = row(u);
+  const auto r = row(u);
   return std::binary_search(r.begin(), r.end(), v);
 }
 
+// The invariants of graph.hpp (zero diagonal, strictly increasing rows,
+// symmetric, ids in range), reported for the first offending entry in row-
+// major order with the reference's messages (proj/src/graph.cpp:173-190).
 void SparseAdjacency::validate() const {
-  if (offsets_.front() != 0 || offsets_.back() != static_cast<std::int64_t>(cols_.size()))
-    throw StructuralError("corrupt row offsets");
-  for (vertex_t v = 0; v < n_; ++v) {
-    vertex_t prev = -1;
-    for (vertex_t x : row(v)) {
-      if (x < 0 || x >= n_) throw StructuralError("column out of range");
-      if (x == v) throw StructuralError("self-loop in adjacency");
-      if (x <= prev) throw StructuralError("row not strictly increasing");
+  const bool offsets_ok =
+      offsets_.front() == 0 && offsets_.back() == static_cast<std::int64_t>(cols_.size());
+  if (!offsets_ok) throw StructuralError("corrupt row offsets");
+  auto first_problem = [this](vertex_t v) -> std::string {
+    const auto r = row(v);
+    for (std::size_t k = 0; k < r.size(); ++k) {
+      const vertex_t x = r[k];
+      if (x < 0 || x >= n_) return "column out of range";
+      if (x == v) return "self-loop in adjacency";
+      if (k > 0 && x <= r[k - 1]) return "row not strictly increasing";
       if (!has_edge(x, v))
-        throw StructuralError("asymmetric adjacency at (" + std::to_string(v) + "," +
-                              std::to_string(x) + ")");
-      prev = x;
+        return "asymmetric adjacency at (" + std::to_string(v) + "," + std::to_string(x) + ")";
     }
-  }
+    return {};
+  };
+  for (vertex_t v = 0; v < n_; ++v)
+    if (std::string why = first_problem(v); !why.empty()) throw StructuralError(why);
 }
 
 const Csr32& SparseAdjacency::csr32() const {
@@ -492,41 +505,30 @@ std::vector<count_t> degree_vector(const SparseAdjacency& g) {
 }
 
 // ================================================================ conversion
-namespace {
-
-// U16 (Table 2): rows raw graphlet, columns net graphlet.
-constexpr unsigned char kU[kNumGraphlets][kNumGraphlets] = {
-    {1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, {0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 1, 0, 2, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 1, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0},
-    {0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, {0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 1, 0, 2, 4, 2, 6},
-    {0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 1, 2, 2, 2, 4, 6}, {0, 0, 0, 0, 0, 0, 0, 1, 0, 1, 1, 0, 0, 2, 1, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 1, 1}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 2, 0, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 2, 6}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 0, 2, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 3}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 0, 3},
-    {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, 3}, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1},
-};
-
-}  // namespace
-
+// A conversion matrix is checked once (unit diagonal, nothing below it, in
+// row-major order) and keeps, per row, its nonzero entries right of the
+// diagonal: the only ones back substitution and apply_conversion read.
 ConversionMatrix::ConversionMatrix(std::vector<int> ids, std::vector<std::vector<count_t>> dense)
     : ids_(std::move(ids)), dense_(std::move(dense)), tails_(ids_.size()) {
-  for (std::size_t r = 0; r < ids_.size(); ++r) {
-    if (dense_[r][r] != 1)
-      throw Error("conversion matrix is not unit-diagonal at row " + std::to_string(r));
-    for (std::size_t c = 0; c < ids_.size(); ++c) {
-      if (c < r && dense_[r][c])
-        throw Error("conversion matrix is not upper triangular at (" + std::to_string(r) + "," +
-                    std::to_string(c) + ")");
-      if (c > r && dense_[r][c]) tails_[r].emplace_back(c, dense_[r][c]);
-    }
+  const std::size_t k = ids_.size();
+  for (std::size_t r = 0; r < k; ++r) {
+    const auto& row = dense_[r];
+    if (row[r] != 1) throw Error("conversion matrix is not unit-diagonal at row " + std::to_string(r));
+    const auto below = std::find_if(row.begin(), row.begin() + static_cast<std::ptrdiff_t>(r),
+                                    [](count_t x) { return x != 0; });
+    if (below != row.begin() + static_cast<std::ptrdiff_t>(r))
+      throw Error("conversion matrix is not upper triangular at (" + std::to_string(r) + "," +
+                  std::to_string(below - row.begin()) + ")");
+    for (std::size_t c = r + 1; c < k; ++c)
+      if (row[c]) tails_[r].emplace_back(c, row[c]);
   }
 }
 
 ConversionMatrix sub_matrix(const Dictionary& d) {
   const auto& ids = d.ids();
-  std::vector<std::vector<count_t>> m(ids.size(), std::vector<count_t>(ids.size(), 0));
+  std::vector<std::vector<count_t>> m(ids.size());
   for (std::size_t r = 0; r < ids.size(); ++r)
-    for (std::size_t c = 0; c < ids.size(); ++c) m[r][c] = kU[ids[r]][ids[c]];
+    for (int c : ids) m[r].push_back(fglt_tables::u16_coef(ids[r], c));
   return ConversionMatrix(ids, std::move(m));
 }
 

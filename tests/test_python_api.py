@@ -96,6 +96,28 @@ def test_oracle_tables_host():
         np.testing.assert_array_equal(gt.oracle_net(h), rnet)
 
 
+SPECS = ["all", " all ", "0-4", " 0-4 ", "4,15", " 2, 5-7 ", "15", "0", "1", "3-3",
+         "1,", "1, ", ",1", ",", "-3", "3-", "4-2", "x", "16", "0-16", "", "   ", "1,,2",
+         "2 ,3", "2- 5", "+3", "07", "1-1,1", "12,14,13"]
+
+
+@pytest.mark.parametrize("spec", SPECS)
+def test_dictionary_grammar_matches_reference(spec):
+    """Every spec: the same ids, implicitly added ids, or error message as
+    the UNMODIFIED reference parse_dictionary (oracle/_ref)."""
+    from oracle import binding as ob
+    if not ob.have_ref():
+        pytest.skip("oracle/_ref not built")
+    try:
+        want = ob.ref_parse_dictionary(spec)
+    except ValueError as e:
+        with pytest.raises(gt.ParseError) as got:
+            gt.graphlet_ids(spec)
+        assert str(got.value) == str(e)
+        return
+    assert gt.graphlet_ids(spec) == want[0]
+
+
 def test_dictionary_specs():
     assert gt.graphlet_ids("0-4") == [0, 1, 2, 3, 4]
     assert gt.graphlet_ids("4,15") == [0, 1, 4, 15]
