@@ -38,6 +38,9 @@ namespace {
 #ifndef FGLT_TL_MEM_FRAC
 #define FGLT_TL_MEM_FRAC 0.70  // triangle-list pool: at most this share of the free HBM
 #endif
+#ifndef FGLT_TINY_DMAX
+#define FGLT_TINY_DMAX 64  // graphs with d_max up to this run tiny roots thread-per-root
+#endif
 #ifndef FGLT_TL_MIN_RECORDS
 #define FGLT_TL_MIN_RECORDS (1ull << 20)  // smaller record bounds: no triangle list
 #endif
@@ -393,6 +396,33 @@ void launch_c4_hashp(fglt_ctx* c, int g, int block, size_t sm, const int* roots,
     default: FN<32>(__VA_ARGS__); break;     \
   }
 
+template <int G>
+void launch_fill_rows(fglt_ctx* c, const int* rp, const int* ci, const int* perm, const int* inv,
+                      const int* nrp, int n, int* out, int* row_of) {
+  k_fill_rows<G><<<c->grid((int64_t)n * G, 256), 256, 0, c->stream>>>(rp, ci, perm, inv, nrp, n,
+                                                                      c->d_small + 4, out, row_of);
+  check_launch();
+  c->launched();
+}
+
+template <int G>
+void launch_mirror(fglt_ctx* c, const int* split, const int* send, const int* orp, int n, int* mir,
+                   int* ce_row, int* ce_pos) {
+  k_mirror<G><<<c->grid((int64_t)n * G, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, send, orp,
+                                                                   n, mir, ce_row, ce_pos);
+  check_launch();
+  c->launched();
+}
+
+template <int G>
+void launch_canon(fglt_ctx* c, const int* split, const int* send, const int* orp, int n,
+                  int* ce_row, int* ce_pos) {
+  k_canon<G><<<c->grid((int64_t)n * G, 256), 256, 0, c->stream>>>(split, send, orp, n, ce_row,
+                                                                  ce_pos);
+  check_launch();
+  c->launched();
+}
+
 // ------------------------------------------------------------------ prepare
 void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t nnz,
              unsigned mask, int lenient) {
@@ -428,14 +458,18 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   }
   if (!c->plan.enumerate || n == 0) return;
 
-  // ---- degree relabel: rank by (degree, id)
-  u64* keys = c->ensure<u64>(B_KEYS, n);
-  u64* keys2 = c->ensure<u64>(B_KEYS2, n);
-  k_degree_keys<<<c->grid(n, 256), 256, 0, c->stream>>>(d_rp, N, keys);
+  // ---- degree relabel: rank by (degree, id) = stable sort of the ids by
+  // the degree key (k_degree_keys), over the key's live bits only
+  int* keys = c->ensure<int>(B_KEYS, 2 * (size_t)n);   // keys | ids
+  int* keys2 = c->ensure<int>(B_KEYS2, 2 * (size_t)n); // sorted keys | sorted ids
+  int key_bits = 1;
+  while (key_bits < 31 && ((int64_t)1 << key_bits) <= n + 1) ++key_bits;
+  k_degree_keys<<<c->grid(n, 256), 256, 0, c->stream>>>(d_rp, N, keys, keys + n);
   check_launch();
   c->launched();
   size_t tmp_bytes = 0, t2 = 0;
-  CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys, keys2, N, 0, 64, c->stream));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, keys + n, keys2 + n, N, 0,
+                                     key_bits, c->stream));
   int* perm = c->ensure<int>(B_PERM, n);
   int* inv = c->ensure<int>(B_INV, n);
   int* ndeg = c->ensure<int>(B_NDEG, n + 1);
@@ -454,19 +488,18 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   tmp_bytes = std::max(tmp_bytes, t3);
   void* cub_tmp = c->ensure<unsigned char>(B_CUB, tmp_bytes);
   size_t tb = c->buf[B_CUB].cap;
-  CK(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, keys, keys2, N, 0, 64, c->stream));
+  CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, keys, keys2, keys + n, keys2 + n, N, 0, key_bits,
+                                     c->stream));
   c->launched();
   CK(cudaMemsetAsync(ndeg + n, 0, sizeof(int), c->stream));
-  k_perm<<<c->grid(n, 256), 256, 0, c->stream>>>(keys2, N, perm, inv, ndeg);
+  k_perm<<<c->grid(n, 256), 256, 0, c->stream>>>(keys2 + n, d_rp, N, perm, inv, ndeg);
   check_launch();
   c->launched();
   tb = c->buf[B_CUB].cap;
   CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ndeg, nrp, N + 1, c->stream));
   c->launched();
-  k_fill_rows<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(d_rp, d_ci, perm, inv, nrp, N,
-                                                           c->d_small + 4, tmp, row_of);
-  check_launch();
-  c->launched();
+  const int G = group_for((double)nnz / (double)std::max<int64_t>(n, 1));
+  DISPATCH_G(G, launch_fill_rows, c, d_rp, d_ci, perm, inv, nrp, N, tmp, row_of);
   tb = c->buf[B_CUB].cap;
   if (nnz > 0) {  // stable sort by neighbour id: rows come out sorted (see k_fill_rows)
     CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, tmp, keys_out, row_of, nci, (int)nnz, 0,
@@ -496,10 +529,7 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   int* ce_pos = c->ensure<int>(B_CE_POS, std::max<int64_t>(c->m, 1));
   const bool sort_mirror = nnz >= FGLT_MIRROR_SORT_DEG * n;  // else per-edge binary searches
   if (nnz > 0 && !sort_mirror) {
-    k_mirror<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, send, orp, N, mir,
-                                                          ce_row, ce_pos);
-    check_launch();
-    c->launched();
+    DISPATCH_G(G, launch_mirror, c, split, send, orp, N, mir, ce_row, ce_pos);
   } else if (nnz > 0) {
     // mirror positions by a second stable transpose: the sorted CSR read
     // r-major as (key = neighbour y, value = own position j) sorts into
@@ -512,9 +542,7 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
     CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, nci, keys_out, row_of, mir, (int)nnz, 0,
                                        id_bits, c->stream));
     c->launched();
-    k_canon<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(split, send, orp, N, ce_row, ce_pos);
-    check_launch();
-    c->launched();
+    DISPATCH_G(G, launch_canon, c, split, send, orp, N, ce_row, ce_pos);
   }
   c->split = split;
   c->send = send;
@@ -658,6 +686,7 @@ void build_hubs(fglt_ctx* c) {
   if (c->force_hub == 1 || nact < 2) return;
   const int R = (int)std::min<int64_t>(nact, kHubMax);
   c->hub_hb = (int)(nact - R);
+  if (c->force_hub != 2 && c->dmax < (u64)kHubMinDegree) return;  // no hubs: no readback
   if (c->force_hub != 2) {  // only graphs with real hubs: the smallest hub's degree
     int h[2];
     CK(cudaMemcpyAsync(h, c->rp + c->hub_hb, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -719,12 +748,20 @@ void roots_pass(fglt_ctx* c) {
   int* queues = reinterpret_cast<int*>(c->d_small + 60);  // one dynamic queue per bin
   CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
   if (cnt[0] > 0) {
+    // thread-per-root for the smallest roots of low-degree graphs only
+    const int tiny_s = c->dmax <= (u64)FGLT_TINY_DMAX ? kRootsTiny : 0;
+    if (tiny_s) {
+      k_roots_tiny<kC3, kD13, kD15><<<c->grid(cnt[0], 256), 256, 0, c->stream>>>(
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[0], cnt[0], tiny_s, d13, d15);
+      check_launch();
+      c->launched();
+    }
     const int wpb = 8;
     const size_t sm = (size_t)wpb * (32 * 8 + kRootsWarpInts * 4);
     const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
     k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(
         c->rp, c->ci, c->split, c->send, c->C3f, lists[0], cnt[0], d13, d15, c->hub, c->hub_base,
-        c->hub_hb, c->force_hub == 2, c->tl);
+        c->hub_hb, c->force_hub == 2, c->tl, tiny_s);
     check_launch();
     c->launched();
   }
@@ -883,7 +920,9 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     DISPATCH_G(G, launch_root_work, c, wc);
     // degree bands of the dense counters (4 / 8 / 16-or-32 bits)
     int bands[3] = {0, 0, 0};
-    if (c->nact > 0) {
+    if (c->nact > 0 && c->dmax <= 15) {  // every active id in the 4-bit band: no readback
+      bands[0] = bands[1] = bands[2] = (int)c->nact;
+    } else if (c->nact > 0) {
       int* d_b = reinterpret_cast<int*>(c->d_small + 41);
       k_degree_bands<<<1, 32, 0, c->stream>>>(c->rp, (int)c->nact, d_b);
       check_launch();
@@ -911,7 +950,11 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     c->mark("four-cycle rows:start");
     c->mark("c4 hash:start");
     u64* c4 = c->V(V_C4);
-    if (cnt[0] > 0) {  // class 1: warp tables of 512 slots
+    if (cnt[0] > 0) {  // class 1: thread per root up to kC4Tiny wedges, else warp tables of 512 slots
+      k_c4_tiny<<<c->grid(cnt[0], 256), 256, 0, c->stream>>>(c->rp, c->ci, c->split, c->mir,
+                                                             lists[0], cnt[0], wc, c4);
+      check_launch();
+      c->launched();
       const int wpb = 8;
       const size_t sm = (size_t)wpb * ((1 << kWarpHashLog) * 2 + 100) * 4;
       k_c4_warp<kWarpHashLog><<<c->grid((int64_t)cnt[0] * 32, wpb * 32), wpb * 32, sm, c->stream>>>(
@@ -1085,8 +1128,13 @@ void epilogue(fglt_ctx* c, int64_t v0, int64_t v1, u64* raw, u64* net) {
   in.c4 = P.c4 ? c->V(V_C4) : nullptr;
   in.d13 = P.d13 ? c->V(V_D13) : nullptr;
   in.d15 = P.d15 ? c->V(V_D15) : nullptr;
+  const bool aligned =
+      ((reinterpret_cast<uintptr_t>(raw) | reinterpret_cast<uintptr_t>(net)) & 15u) == 0;
   if (v0 == 0 && v1 == c->n && c->perm && c->inv)  // whole table: walk rows in vector order
-    if (c->dict.mask == 0xFFFFu)
+    if (c->dict.mask == 0xFFFFu && aligned)
+      k_epilogue_lines<<<c->grid(v1, kEpilogueThreads, 12), kEpilogueThreads, 0, c->stream>>>(
+          in, c->perm, (int)v1, c->lenient, raw, net, c->d_small);
+    else if (c->dict.mask == 0xFFFFu)
       k_epilogue_rank<true><<<c->grid(v1, kEpilogueThreads), kEpilogueThreads, 0, c->stream>>>(
           in, c->perm, c->d_dict, (int)v1, c->lenient, raw, net, c->d_small);
     else

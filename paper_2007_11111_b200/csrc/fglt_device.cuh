@@ -145,21 +145,26 @@ __device__ __forceinline__ u64 seg_sum_runs(int row, u64 v, bool* tail) {
 // Vertices of degree <= 1 lie on no triangle or cycle: they are ranked LAST
 // (bit 31 of the degree field), so the enumeration id range [0, n_active)
 // holds only vertices of degree >= 2 and the 4-cycle tiles shrink with it.
-__global__ void k_degree_keys(const int* __restrict__ rp, int n, u64* __restrict__ keys) {
+// Rank order of the relabel: degree ascending with degree <= 1 vertices last
+// (degree 0 before 1), ties by id. As a STABLE sort of the ids by one int key
+// (CUB radix sort is stable): key = d for d >= 2, n + d below (d <= n - 1,
+// so every leaf key is above every active one).
+__global__ void k_degree_keys(const int* __restrict__ rp, int n, int* __restrict__ keys,
+                              int* __restrict__ ids) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const u64 d = (u64)(rp[i + 1] - rp[i]);
-    keys[i] = ((d < 2 ? d | 0x80000000ull : d) << 32) | (u64)i;
+    const int d = rp[i + 1] - rp[i];
+    keys[i] = d >= 2 ? d : n + d;
+    ids[i] = i;
   }
 }
 
-__global__ void k_perm(const u64* __restrict__ keys, int n, int* __restrict__ perm,
-                       int* __restrict__ inv, int* __restrict__ ndeg) {
+__global__ void k_perm(const int* __restrict__ sorted_ids, const int* __restrict__ rp, int n,
+                       int* __restrict__ perm, int* __restrict__ inv, int* __restrict__ ndeg) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    u64 k = keys[r];
-    int old = (int)(k & 0xffffffffu);
+    const int old = sorted_ids[r];
     perm[r] = old;
     inv[old] = r;
-    ndeg[r] = (int)((k >> 32) & 0x7fffffffull);
+    ndeg[r] = rp[old + 1] - rp[old];
   }
 }
 
@@ -182,6 +187,7 @@ __device__ __forceinline__ int first_long_row(const int* __restrict__ nrp, int n
 
 constexpr int kLongRow = 1024;  // rows longer than this get a whole block
 
+template <int G>  // lanes per short row (from the mean degree)
 __global__ void k_fill_rows(const int* __restrict__ rp, const int* __restrict__ ci,
                             const int* __restrict__ perm, const int* __restrict__ inv,
                             const int* __restrict__ nrp, int n,
@@ -197,13 +203,13 @@ __global__ void k_fill_rows(const int* __restrict__ rp, const int* __restrict__ 
       row_of[w + (p - b)] = r;
     }
   }
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+  const int lane = threadIdx.x & (G - 1);
+  const int groups = (gridDim.x * blockDim.x) / G;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) / G; r < n; r += groups) {
     if (r >= fl && r < nact) continue;
     const int o = perm[r];
     const int b = rp[o], e = rp[o + 1], w = nrp[r];
-    for (int p = b + lane; p < e; p += 32) {
+    for (int p = b + lane; p < e; p += G) {
       out[w + (p - b)] = inv[ci[p]];
       row_of[w + (p - b)] = r;
     }
@@ -229,24 +235,28 @@ __global__ void k_split(const int* __restrict__ rp, const int* __restrict__ ci, 
     outdeg[r] = e - s;
     mo = max(mo, (unsigned long long)(e - s));
   }
-  if (mo) atomicMax(maxout, mo);
+  // one atomic per warp: every thread hitting the same word serialises
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mo = max(mo, __shfl_xor_sync(0xffffffffu, mo, o));
+  if ((threadIdx.x & 31) == 0 && mo) atomicMax(maxout, mo);
 }
 
 // Low-degree graphs (binary searches are short): warp per row; for each
 // canonical position p (row r, v = ci[p] > r) find the mirror position q of
 // r in row v (a prefix entry) and record both; also emit the compact
 // canonical edge list (row, position), index e = orp[r] + offset.
+template <int G>  // lanes per row (from the mean degree)
 __global__ void k_mirror(const int* __restrict__ rp, const int* __restrict__ ci,
                          const int* __restrict__ split, const int* __restrict__ send,
                          const int* __restrict__ orp, int n, int* __restrict__ mir,
                          int* __restrict__ ce_row, int* __restrict__ ce_pos) {
   // canonical edges between active vertices only: edges to the pendant tail
   // carry no triangles (their C3 stays 0 in both slots)
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+  const int lane = threadIdx.x & (G - 1);
+  const int groups = (gridDim.x * blockDim.x) / G;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) / G; r < n; r += groups) {
     const int s = split[r], e = send[r], base = orp[r];
-    for (int p = s + lane; p < e; p += 32) {
+    for (int p = s + lane; p < e; p += G) {
       const int v = ci[p];
       const int q = lower_bound_i32(ci, rp[v], split[v], r);
       mir[p] = q;
@@ -260,14 +270,15 @@ __global__ void k_mirror(const int* __restrict__ rp, const int* __restrict__ ci,
 // Compact canonical edge list of the active-active upper entries: for row r,
 // positions [split[r], send[r]) go to e = orp[r] + offset as (row, position).
 // (The mirror positions come from a second stable transpose sort, prepare().)
+template <int G>  // lanes per row (from the mean degree)
 __global__ void k_canon(const int* __restrict__ split, const int* __restrict__ send,
                         const int* __restrict__ orp, int n, int* __restrict__ ce_row,
                         int* __restrict__ ce_pos) {
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+  const int lane = threadIdx.x & (G - 1);
+  const int groups = (gridDim.x * blockDim.x) / G;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) / G; r < n; r += groups) {
     const int s = split[r], e = send[r], base = orp[r];
-    for (int p = s + lane; p < e; p += 32) {
+    for (int p = s + lane; p < e; p += G) {
       ce_row[base + (p - s)] = r;
       ce_pos[base + (p - s)] = p;
     }

@@ -108,6 +108,69 @@ __device__ __forceinline__ u32 hash_get_claim(const int* keys, u32* vals, int lo
 // Warp per root (wc <= 256): a table of 2^hlog <= 2^LOGCAP slots sized to the
 // root; the rows of N-(u) are walked 32 at a time with segment flattening so
 // every lane streams one wedge per step.
+// Class-1 roots with at most kC4Tiny wedges (most roots of low-degree graphs,
+// e.g. RGG's ~2-5): thread per root, the wedge targets in registers (static
+// indexing via shift insertion), L[w] by pairwise equality. No shared table to
+// clear and no warp-wide bookkeeping per root; k_c4_warp skips these roots.
+#ifndef FGLT_C4_TINY
+#define FGLT_C4_TINY 8
+#endif
+constexpr int kC4Tiny = FGLT_C4_TINY;
+__global__ void __launch_bounds__(256) k_c4_tiny(const int* __restrict__ rp,
+                                                 const int* __restrict__ ci,
+                                                 const int* __restrict__ split,
+                                                 const int* __restrict__ mir,
+                                                 const int* __restrict__ roots, int nroots,
+                                                 const u64* __restrict__ wcv,
+                                                 u64* __restrict__ c4) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nroots; k += gridDim.x * blockDim.x) {
+    const int u = roots[k];
+    if (wcv[u] > (u64)kC4Tiny) continue;
+    int wl[kC4Tiny], vl[kC4Tiny];
+#pragma unroll
+    for (int i = 0; i < kC4Tiny; ++i) wl[i] = -1 - i;  // distinct sentinels never match
+    int cnt = 0;
+    const int b = rp[u], s = split[u];
+    for (int q = b; q < s; ++q) {
+      const int v = ci[q];
+      const int e = mir[q];
+      for (int p = rp[v]; p < e; ++p) {
+        const int w = __ldg(ci + p);
+#pragma unroll
+        for (int i = kC4Tiny - 1; i > 0; --i) {
+          wl[i] = wl[i - 1];
+          vl[i] = vl[i - 1];
+        }
+        wl[0] = w;
+        vl[0] = v;
+        ++cnt;
+      }
+    }
+    u64 cu = 0;
+#pragma unroll
+    for (int i = 0; i < kC4Tiny; ++i) {
+      if (i >= cnt) break;
+      u32 L = 0;
+      bool first = true;
+#pragma unroll
+      for (int j = 0; j < kC4Tiny; ++j) {
+        const bool eq = wl[j] == wl[i];
+        L += eq;
+        first &= !(eq && j < i);
+      }
+      if (L >= 2) {
+        if (first) {
+          const u64 c = (u64)L * (L - 1) / 2;
+          cu += c;
+          atomicAdd(c4 + wl[i], c);
+        }
+        atomicAdd(c4 + vl[i], (u64)(L - 1));
+      }
+    }
+    if (cu) atomicAdd(c4 + u, cu);
+  }
+}
+
 template <int LOGCAP>
 __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci,
                           const int* __restrict__ split, const int* __restrict__ mir,
@@ -126,6 +189,7 @@ __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
     const int u = roots[k];
+    if (wcv[u] <= (u64)kC4Tiny) continue;  // k_c4_tiny
     int hlog = 5;
     while (hlog < LOGCAP && ((u64)1 << hlog) < 2 * wcv[u]) ++hlog;
     const int cap = 1 << hlog;
@@ -1190,6 +1254,101 @@ struct TriList {
   unsigned chunks_cap = 0;
 };
 
+// Thread per root for |S| <= tiny_s <= kRootsTiny (most roots of low-degree
+// graphs: RGG's mean |N+(u)| is 1.5; the host enables it when d_max is small,
+// since on power-law graphs the members' probe lists are long and a thread
+// walking them serially loses to the warp): S, the sums and G[S] (8 x 8 bits)
+// live in registers (static indexing only); the same per-triangle updates as
+// k_roots_warp. Tiny roots never use the triangle list: the diamond pass
+// re-probes them with this kernel (kD13), and k_roots_warp skips them in
+// both passes.
+#ifndef FGLT_ROOTS_TINY
+#define FGLT_ROOTS_TINY 8
+#endif
+constexpr int kRootsTiny = FGLT_ROOTS_TINY;
+static_assert(kRootsTiny <= 8, "G[S] rows are 8-bit fields of one u64");
+template <bool kC3, bool kD13, bool kD15>
+__global__ void __launch_bounds__(256) k_roots_tiny(const int* __restrict__ rp,
+                                                    const int* __restrict__ ci,
+                                                    const int* __restrict__ split,
+                                                    const int* __restrict__ send,
+                                                    u32* __restrict__ C3f,
+                                                    const int* __restrict__ roots, int nroots,
+                                                    int tiny_s, u64* __restrict__ d13,
+                                                    u64* __restrict__ d15) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nroots; k += gridDim.x * blockDim.x) {
+    const int u = roots[k];
+    const int s0 = split[u];
+    const int s = send[u] - s0;
+    if (s > tiny_s) continue;  // k_roots_warp
+    int S[kRootsTiny];
+    u32 cu[kRootsTiny];  // kD13: C3(u, S[a]); kC3: triangles on edge (u, S[a])
+    u64 da[kRootsTiny];  // kD13: d13 partial of S[a]
+#pragma unroll
+    for (int a = 0; a < kRootsTiny; ++a) {
+      S[a] = a < s ? __ldg(ci + s0 + a) : -1;
+      cu[a] = kD13 && a < s ? C3f[s0 + a] : 0u;
+      da[a] = 0;
+    }
+    const int smax = __ldg(ci + s0 + s - 1);
+    u64 g = 0;  // G[S]: bit 8a + b
+    u64 tu = 0;
+#pragma unroll
+    for (int a = 0; a + 1 < kRootsTiny; ++a) {
+      if (a + 1 >= s) break;
+      const int x = S[a];
+      const int e = rp[x + 1];
+      for (int p = split[x]; p < e; ++p) {
+        const int y = __ldg(ci + p);
+        if (y > smax) break;
+        int bi = -1;
+#pragma unroll
+        for (int b = a + 1; b < kRootsTiny; ++b)
+          if (S[b] == y) bi = b;
+        if (bi < 0) continue;
+        // triangle {u, S[a], S[bi]}; (S[a], S[bi]) is CSR slot p
+        if (kD15) g |= (1ull << (8 * a + bi)) | (1ull << (8 * bi + a));
+        if (kC3) {
+          atomicAdd(C3f + p, 1u);
+          ++cu[a];
+#pragma unroll
+          for (int b = a + 1; b < kRootsTiny; ++b) cu[b] += b == bi;
+        }
+        if (kD13) {
+          tu += (u64)__ldg(C3f + p) - 1;
+          u32 cb = 0;
+#pragma unroll
+          for (int b = a + 1; b < kRootsTiny; ++b) {
+            if (b == bi) {
+              cb = cu[b];
+              da[b] += (u64)cu[a] - 1;
+            }
+          }
+          da[a] += (u64)cb - 1;
+        }
+      }
+    }
+    u64 tot = 0;
+#pragma unroll
+    for (int a = 0; a < kRootsTiny; ++a) {
+      if (a >= s) break;
+      if (kC3 && cu[a]) atomicAdd(C3f + s0 + a, cu[a]);
+      if (kD13 && da[a]) atomicAdd(d13 + S[a], da[a]);
+      if (kD15) {
+        const u32 row = (u32)(g >> (8 * a)) & 0xffu;
+        u32 t = 0;
+#pragma unroll
+        for (int b = 0; b < kRootsTiny; ++b)
+          if (row >> b & 1u) t += __popc(row & ((u32)(g >> (8 * b)) & 0xffu));
+        if (t / 2) atomicAdd(d15 + S[a], (u64)(t / 2));
+        tot += t / 2;
+      }
+    }
+    if (kD13 && tu) atomicAdd(d13 + u, tu);
+    if (kD15 && tot) atomicAdd(d15 + u, tot / 3);
+  }
+}
+
 // Warp per root, |S| <= 32: rows are single words.
 constexpr int kRootsWarpInts = 32 * 5 + 33 + 1;  // sS, sC, rows, fbase, foff(33), fsplit, wcnt
 template <bool kC3, bool kD13, bool kD15>
@@ -1200,7 +1359,7 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
                              u64* __restrict__ d13, u64* __restrict__ d15,
                              const unsigned long long* __restrict__ hub,
                              const int* __restrict__ hub_base, int hb, int hub_force,
-                             TriList tl) {
+                             TriList tl, int tiny_s) {
   // kC3: per-edge triangle counts (atomics into C3f) — the triangle pass.
   // kD13: diamonds from the final C3 — a later pass (needs complete C3).
   // Members that are hubs may test their pairs against the hub rows instead
@@ -1232,6 +1391,7 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
     if (kD13 && tl.rec && !tl.fail[u]) continue;  // listed: k_diamond_wlist handles it
     const int s0 = split[u];
     const int s = send[u] - s0;
+    if (s <= tiny_s) continue;  // k_roots_tiny (both passes)
     // reserve room for a header and up to C(s,2) records of this root
     bool listing = false;
     if (kC3 && tl.rec) {
@@ -2300,7 +2460,7 @@ __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue(EpilogueIn in, co
 // shared memory and writes every table row as one coalesced 128-byte line
 // (8 lanes x 16 bytes, 4 rows per store instruction) instead of 32 scattered
 // 16-byte pieces per instruction.
-constexpr int kEpiStride = 18;  // u64 per staged row: 16 + 2 (16-byte aligned, bank spread)
+constexpr int kEpiStride = 17;  // u64 per staged row: odd, so lanes' rows spread over banks
 __device__ __forceinline__ void epi_store_lines(const u64* __restrict__ st, int lane, int base,
                                                 int n, int v_lane, u64* __restrict__ table) {
   const int c = lane & 7;
@@ -2309,8 +2469,107 @@ __device__ __forceinline__ void epi_store_lines(const u64* __restrict__ st, int 
     const int j = it * 4 + (lane >> 3);
     const int vj = __shfl_sync(0xffffffffu, v_lane, j);
     if (base + j < n) {
-      const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(st + j * kEpiStride + 2 * c);
-      *reinterpret_cast<ulonglong2*>(table + (long long)vj * 16 + 2 * c) = x;
+      const u64* src = st + j * kEpiStride + 2 * c;
+      *reinterpret_cast<ulonglong2*>(table + (long long)vj * 16 + 2 * c) =
+          make_ulonglong2(src[0], src[1]);
+    }
+  }
+}
+
+// Full-dictionary row of vertex v (vector row r) computed straight into the
+// staging row `row` (shared memory): raw columns (kernels.cpp:384-412), and
+// after the raw line is stored, the net back substitution IN PLACE (row r of
+// U16 only reads net entries c > r, already overwritten) — no 32-u64 register
+// arrays, so the kernel runs at high occupancy.
+__device__ __forceinline__ void epi_raw_into(const EpilogueIn& in, int v, int r, u64* err,
+                                             u64* __restrict__ row) {
+  const u64 d = (u64)(in.rp[r + 1] - in.rp[r]);
+  u64 t;
+  row[0] = 1;
+  row[1] = d;
+  const u64 p2 = in.p2 ? in.p2[r] : 0;
+  row[2] = p2;
+  u64 c2 = 0;
+  if (d >= 2) {
+    if (mul_ov(d, d - 1, &t)) offer_err(err, 1, v, 0, 3);
+    c2 = t / 2;
+  }
+  row[3] = c2;
+  const u64 c3v = in.c3 ? in.c3[r] : 0;
+  row[4] = c3v;
+  row[5] = in.p3 ? in.p3[r] : 0;
+  if (mul_ov(p2, sat_sub(d, 1), &t)) offer_err(err, 2, v, 0, 6);
+  row[6] = sat_sub(t, 2 * c3v);
+  row[7] = in.d7 ? in.d7[r] : 0;
+  u64 c8 = 0;
+  if (d >= 3) {  // choose3: unchecked d(d-1)/2, checked *(d-2)
+    if (mul_ov(d * (d - 1) / 2, d - 2, &t)) offer_err(err, 4, v, 0, 8);
+    c8 = t / 3;
+  }
+  row[8] = c8;
+  row[9] = in.d9 ? in.d9[r] : 0;
+  row[10] = in.d10 ? in.d10[r] : 0;
+  if (mul_ov(sat_sub(d, 2), c3v, &t)) offer_err(err, 5, v, 0, 11);
+  row[11] = t;
+  row[12] = in.c4 ? in.c4[r] : 0;
+  row[13] = in.d13 ? in.d13[r] : 0;
+  row[14] = in.d14 ? in.d14[r] : 0;
+  row[15] = in.d15 ? in.d15[r] : 0;
+}
+
+__device__ __forceinline__ void epi_net_in_place(int v, int lenient, u64* err,
+                                                 u64* __restrict__ row) {
+  int bad_r = -1, bad_code = 0;
+#pragma unroll
+  for (int rr = 15; rr >= 0; --rr) {
+    u64 absorbed = 0;
+    bool ov = false;
+#pragma unroll
+    for (int cc = rr + 1; cc < 16; ++cc) {
+      if (u16_coef(rr, cc) == 0) continue;
+      u64 prod;
+      ov |= mul_ov((u64)u16_coef(rr, cc), row[cc], &prod);
+      ov |= add_ov(absorbed, prod, &absorbed);
+    }
+    const u64 x = row[rr];
+    const bool neg = absorbed > x;
+    row[rr] = neg ? 0ull : x - absorbed;
+    if (bad_r < 0 && (ov || (neg && !lenient))) {
+      bad_r = rr;
+      bad_code = ov ? 0 : 1;
+    }
+  }
+  if (bad_r >= 0) offer_err(err, 6, v, bad_code, bad_r);
+}
+
+// Full dictionary, 16-byte aligned tables (the common case): a warp stages
+// its 32 rows in shared memory, writes every table row as one coalesced
+// 128-byte line, and converts raw -> net in place between the two stores.
+// Few live registers: 12 blocks of 128 threads per SM.
+__global__ void __launch_bounds__(kEpilogueThreads, 12) k_epilogue_lines(
+    EpilogueIn in, const int* __restrict__ perm, int n, int lenient, u64* __restrict__ raw,
+    u64* __restrict__ net, u64* __restrict__ err) {
+  __shared__ u64 stage[kEpilogueThreads / 32][32 * kEpiStride];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  u64* sr = stage[wid];
+  u64* mine = sr + lane * kEpiStride;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) << 5; base < n;
+       base += warps << 5) {
+    const int r = base + lane;
+    int v = 0;
+    if (r < n) {
+      v = perm[r];
+      epi_raw_into(in, v, r, err, mine);
+    }
+    __syncwarp();
+    if (raw) epi_store_lines(sr, lane, base, n, v, raw);
+    __syncwarp();
+    if (net) {
+      if (r < n) epi_net_in_place(v, lenient, err, mine);
+      __syncwarp();
+      epi_store_lines(sr, lane, base, n, v, net);
+      __syncwarp();
     }
   }
 }
@@ -2323,45 +2582,6 @@ __global__ void __launch_bounds__(kEpilogueThreads) k_epilogue_rank(
   if (threadIdx.x == 0) D = *dict;
   __syncthreads();
   const int k = D.k;
-  if (kFull && ((reinterpret_cast<unsigned long long>(raw) |
-                 reinterpret_cast<unsigned long long>(net)) & 15ull) == 0) {
-    __shared__ __align__(16) u64 stage[kEpilogueThreads / 32][32 * kEpiStride];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    u64* sr = stage[wid];
-    const int warps = (gridDim.x * blockDim.x) >> 5;
-    for (int base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) << 5; base < n;
-         base += warps << 5) {
-      const int r = base + lane;
-      int v = 0;
-      u64 rw[16], nt[16];
-      if (r < n) {
-        v = perm[r];
-        epi_row_full(in, D, v, r, lenient, net != nullptr, err, rw, nt);
-      }
-      // raw rows, then net rows, through the same staging lines
-      if (raw) {
-        if (r < n) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 2)
-            *reinterpret_cast<ulonglong2*>(sr + lane * kEpiStride + i) = make_ulonglong2(rw[i], rw[i + 1]);
-        }
-        __syncwarp();
-        epi_store_lines(sr, lane, base, n, v, raw);
-        __syncwarp();
-      }
-      if (net) {
-        if (r < n) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 2)
-            *reinterpret_cast<ulonglong2*>(sr + lane * kEpiStride + i) = make_ulonglong2(nt[i], nt[i + 1]);
-        }
-        __syncwarp();
-        epi_store_lines(sr, lane, base, n, v, net);
-        __syncwarp();
-      }
-    }
-    return;
-  }
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const int v = perm[r];
     const long long o = (long long)v * k;
