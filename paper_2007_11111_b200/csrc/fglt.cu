@@ -230,7 +230,7 @@ struct fglt_ctx {
   // root bins by |N+(u)| (shared by the triangle and diamond passes)
   int64_t rb_u0 = -1, rb_u1 = -1;
   std::vector<int> rb_cnt;
-  int* rb_lists[8] = {};
+  int* rb_lists[9] = {};
 
   // test hooks (fglt_ctx_set_debug): force one code path for every root
   int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1, force_hub = 0;
@@ -589,7 +589,7 @@ std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
                            const std::vector<u64>& thr, int** lists, int64_t* stride,
                            Buf which = B_LISTS) {
   const int nb = (int)thr.size() + 1;
-  if (nb > 8) throw CudaFail{FGLT_E_CUDA, "internal: at most 8 root bins"};
+  if (nb > 9) throw CudaFail{FGLT_E_CUDA, "internal: at most 9 root bins"};
   const int64_t span = std::max<int64_t>(u1 - u0, 1);
   int* lst = c->ensure<int>(which, (size_t)nb * span);
   u64* d_thr = c->d_small + 8;
@@ -597,15 +597,15 @@ std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
   std::vector<u64> th(thr);
   th.resize(8, ~0ull);
   CK(cudaMemcpyAsync(d_thr, th.data(), 8 * sizeof(u64), cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemsetAsync(counts, 0, 8 * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(counts, 0, 10 * sizeof(int), c->stream));  // slots 16..20
   if (u1 > u0) {
     k_bin<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(key, (int)u0, (int)u1, d_thr, nb, counts,
                                                        lst, span);
     check_launch();
     c->launched();
   }
-  std::vector<int> h(8);
-  CK(cudaMemcpyAsync(h.data(), counts, 8 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  std::vector<int> h(9);
+  CK(cudaMemcpyAsync(h.data(), counts, 9 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   for (int b = 0; b < nb; ++b) lists[b] = lst + (int64_t)b * span;
   *stride = span;
@@ -648,7 +648,11 @@ constexpr int kSlabThreads = FGLT_SLAB_THREADS;
 #define FGLT_BIN2 256  // |S| cap of the 128-thread root bin
 #define FGLT_BIN3 512
 #endif
-constexpr u64 kRootThr[] = {(u64)kSmallS, FGLT_BIN1, FGLT_BIN2, FGLT_BIN3, (u64)kBlockS};
+// root bins by |N+(u)|: 0 tiny (thread per root on low-degree graphs, else
+// warp), 1 warp, 2..5 shared-memory block bins, 6 global slab
+constexpr u64 kRootThr[] = {(u64)kRootsTiny, (u64)kSmallS, FGLT_BIN1, FGLT_BIN2, FGLT_BIN3,
+                            (u64)kBlockS};
+constexpr int kFirstBlockBin = 2;
 
 __global__ void k_gather_keys(const int* __restrict__ list, int cnt, const u64* __restrict__ w,
                               u64* __restrict__ keys) {
@@ -729,7 +733,7 @@ void root_bins(fglt_ctx* c, int64_t u0, int64_t u1) {
                         c->rb_lists, &stride, B_RLISTS);
   // keys are |N+(u)| <= max out-degree (or a forced bin key <= 1025)
   const int kbits = 64 - __builtin_clzll(std::max<u64>(std::max<u64>(c->maxout, 1025), 1));
-  for (int b = 1; b < (int)c->rb_cnt.size(); ++b)
+  for (int b = kFirstBlockBin; b < (int)c->rb_cnt.size(); ++b)
     sort_by_work_desc(c, c->rb_lists[b], c->rb_cnt[b], key, kbits);
   c->rb_u0 = u0;
   c->rb_u1 = u1;
@@ -747,25 +751,26 @@ void roots_pass(fglt_ctx* c) {
   int** lists = c->rb_lists;
   int* queues = reinterpret_cast<int*>(c->d_small + 60);  // one dynamic queue per bin
   CK(cudaMemsetAsync(queues, 0, 8 * sizeof(int), c->stream));
-  if (cnt[0] > 0) {
-    // thread-per-root for the smallest roots of low-degree graphs only
-    const int tiny_s = c->dmax <= (u64)FGLT_TINY_DMAX ? kRootsTiny : 0;
-    if (tiny_s) {
+  // thread-per-root for the tiny bin of low-degree graphs only (on power-law
+  // graphs the members' probe lists are long: the warp kernel wins there)
+  const bool tiny = c->dmax <= (u64)FGLT_TINY_DMAX;
+  for (int b = 0; b < kFirstBlockBin; ++b) {
+    if (cnt[b] == 0) continue;
+    if (b == 0 && tiny) {
       k_roots_tiny<kC3, kD13, kD15><<<c->grid(cnt[0], 256), 256, 0, c->stream>>>(
-          c->rp, c->ci, c->split, c->send, c->C3f, lists[0], cnt[0], tiny_s, d13, d15);
-      check_launch();
-      c->launched();
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[0], cnt[0], d13, d15);
+    } else {
+      const int wpb = 8;
+      const size_t sm = (size_t)wpb * (32 * 8 + kRootsWarpInts * 4);
+      const int g = c->grid((int64_t)cnt[b] * 32, wpb * 32);
+      k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(
+          c->rp, c->ci, c->split, c->send, c->C3f, lists[b], cnt[b], d13, d15, c->hub,
+          c->hub_base, c->hub_hb, c->force_hub == 2, c->tl);
     }
-    const int wpb = 8;
-    const size_t sm = (size_t)wpb * (32 * 8 + kRootsWarpInts * 4);
-    const int g = c->grid((int64_t)cnt[0] * 32, wpb * 32);
-    k_roots_warp<kC3, kD13, kD15><<<g, wpb * 32, sm, c->stream>>>(
-        c->rp, c->ci, c->split, c->send, c->C3f, lists[0], cnt[0], d13, d15, c->hub, c->hub_base,
-        c->hub_hb, c->force_hub == 2, c->tl, tiny_s);
     check_launch();
     c->launched();
   }
-  for (int b = 1; b < (int)cnt.size(); ++b) {
+  for (int b = kFirstBlockBin; b < (int)cnt.size(); ++b) {
     if (cnt[b] == 0) continue;
     const bool global = b == (int)cnt.size() - 1;  // s > kBlockS
     RootsLayout L;
@@ -778,7 +783,9 @@ void roots_pass(fglt_ctx* c) {
     // their 257..1024 bins take 512-thread blocks (R-MAT 23 -7 %; R-MAT 20,
     // max |S| 777, keeps 256: +12 % otherwise)
     const int big_nt = c->maxout > (u64)kBlockS ? 512 : kRootsThreads;
-    const int nt = global ? kSlabThreads : (b == 1 ? FGLT_BIN1_NT : b == 2 ? FGLT_BIN2_NT : big_nt);
+    const int nt = global ? kSlabThreads
+                          : (b == kFirstBlockBin ? FGLT_BIN1_NT
+                                                 : b == kFirstBlockBin + 1 ? FGLT_BIN2_NT : big_nt);
     L.nwarps = nt / 32;
     L.stride_cap = bitmap_stride((L.s_cap + 31) / 32);
     size_t sm = L.bytes_core();
@@ -838,8 +845,9 @@ void setup_trilist(fglt_ctx* c, int64_t u0, int64_t u1) {
   // grids roots_pass actually launches, so the pool follows the graph size
   unsigned long long blocks = 0, warps = 0;
   if (!c->rb_cnt.empty()) {
-    warps = std::min<unsigned long long>(c->rb_cnt[0], (unsigned long long)c->sms * 64);
-    for (size_t b = 1; b < c->rb_cnt.size(); ++b)
+    for (int b = 0; b < kFirstBlockBin; ++b)
+      warps += std::min<unsigned long long>(c->rb_cnt[b], (unsigned long long)c->sms * 64);
+    for (size_t b = kFirstBlockBin; b < c->rb_cnt.size(); ++b)
       blocks += std::min<unsigned long long>(c->rb_cnt[b], (unsigned long long)c->sms * 32);
   }
   unsigned long long cap = bound + blocks * kTriListChunk + warps * kTriListWarpChunk;
@@ -913,7 +921,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   u64* wc = work;
   u64* cls = work + c->n;
   u64* parts = work + 2 * c->n;
-  int* lists[8];
+  int* lists[9];
   int64_t stride = 0;
   if (P.c4) {
     const int G = group_for((double)c->nnz / (double)c->n);
@@ -940,7 +948,7 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
         c->force_c4_class, c->force_c4_parts, cw);
     check_launch();
     c->launched();
-    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6, 7}, lists, &stride);
+    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6, 7, 8}, lists, &stride);
     // wc(u) <= W = sum of squared degrees
     const int wbits = 64 - __builtin_clzll(std::max<u64>(c->W, 1));
     for (int bb = 3; bb <= 6; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc, wbits);
@@ -950,11 +958,13 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     c->mark("four-cycle rows:start");
     c->mark("c4 hash:start");
     u64* c4 = c->V(V_C4);
-    if (cnt[0] > 0) {  // class 1: thread per root up to kC4Tiny wedges, else warp tables of 512 slots
-      k_c4_tiny<<<c->grid(cnt[0], 256), 256, 0, c->stream>>>(c->rp, c->ci, c->split, c->mir,
-                                                             lists[0], cnt[0], wc, c4);
+    if (cnt[8] > 0) {  // class 9: thread per root, at most kC4Tiny wedges
+      k_c4_tiny<<<c->grid(cnt[8], 256), 256, 0, c->stream>>>(c->rp, c->ci, c->split, c->mir,
+                                                             lists[8], cnt[8], wc, c4);
       check_launch();
       c->launched();
+    }
+    if (cnt[0] > 0) {  // class 1: warp tables of 512 slots
       const int wpb = 8;
       const size_t sm = (size_t)wpb * ((1 << kWarpHashLog) * 2 + 100) * 4;
       k_c4_warp<kWarpHashLog><<<c->grid((int64_t)cnt[0] * 32, wpb * 32), wpb * 32, sm, c->stream>>>(

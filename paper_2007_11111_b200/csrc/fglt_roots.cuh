@@ -125,7 +125,6 @@ __global__ void __launch_bounds__(256) k_c4_tiny(const int* __restrict__ rp,
                                                  u64* __restrict__ c4) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nroots; k += gridDim.x * blockDim.x) {
     const int u = roots[k];
-    if (wcv[u] > (u64)kC4Tiny) continue;
     int wl[kC4Tiny], vl[kC4Tiny];
 #pragma unroll
     for (int i = 0; i < kC4Tiny; ++i) wl[i] = -1 - i;  // distinct sentinels never match
@@ -189,7 +188,6 @@ __global__ void k_c4_warp(const int* __restrict__ rp, const int* __restrict__ ci
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nroots; k += warps) {
     const int u = roots[k];
-    if (wcv[u] <= (u64)kC4Tiny) continue;  // k_c4_tiny
     int hlog = 5;
     while (hlog < LOGCAP && ((u64)1 << hlog) < 2 * wcv[u]) ++hlog;
     const int cap = 1 << hlog;
@@ -308,6 +306,7 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 }
 
 // Cost-model classes for roots with wc(u) > 0 (k_c4_class):
+//   9 thread per root (k_c4_tiny)        wc <= kC4Tiny
 //   1 warp table, 512 slots              wc <= 256
 //   8 small block table (128 threads, 1024 slots), wc <= 512
 //   2 small block table (128 threads, 2048 slots), wc <= 1024
@@ -408,6 +407,8 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
     u64 c = 0, P = 1;
     if (w == 0) {
       c = 0;
+    } else if (w <= (u64)kC4Tiny) {
+      c = 9;  // thread per root (k_c4_tiny)
     } else if (w <= 256) {
       c = 1;
     } else if (w <= 512) {
@@ -1274,13 +1275,12 @@ __global__ void __launch_bounds__(256) k_roots_tiny(const int* __restrict__ rp,
                                                     const int* __restrict__ send,
                                                     u32* __restrict__ C3f,
                                                     const int* __restrict__ roots, int nroots,
-                                                    int tiny_s, u64* __restrict__ d13,
-                                                    u64* __restrict__ d15) {
+                                                    u64* __restrict__ d13, u64* __restrict__ d15) {
+  // roots: the tiny bin, |N+(u)| <= kRootsTiny
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nroots; k += gridDim.x * blockDim.x) {
     const int u = roots[k];
     const int s0 = split[u];
     const int s = send[u] - s0;
-    if (s > tiny_s) continue;  // k_roots_warp
     int S[kRootsTiny];
     u32 cu[kRootsTiny];  // kD13: C3(u, S[a]); kC3: triangles on edge (u, S[a])
     u64 da[kRootsTiny];  // kD13: d13 partial of S[a]
@@ -1359,7 +1359,7 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
                              u64* __restrict__ d13, u64* __restrict__ d15,
                              const unsigned long long* __restrict__ hub,
                              const int* __restrict__ hub_base, int hb, int hub_force,
-                             TriList tl, int tiny_s) {
+                             TriList tl) {
   // kC3: per-edge triangle counts (atomics into C3f) — the triangle pass.
   // kD13: diamonds from the final C3 — a later pass (needs complete C3).
   // Members that are hubs may test their pairs against the hub rows instead
@@ -1391,7 +1391,6 @@ __global__ void __launch_bounds__(256, 8) k_roots_warp(const int* __restrict__ r
     if (kD13 && tl.rec && !tl.fail[u]) continue;  // listed: k_diamond_wlist handles it
     const int s0 = split[u];
     const int s = send[u] - s0;
-    if (s <= tiny_s) continue;  // k_roots_tiny (both passes)
     // reserve room for a header and up to C(s,2) records of this root
     bool listing = false;
     if (kC3 && tl.rec) {
