@@ -360,7 +360,8 @@ void launch_sweep_a(fglt_ctx* c) {
 
 template <int G>
 void launch_sweep_bc(fglt_ctx* c) {
-  SweepB fb{c->rp, c->ci, c->C3f, c->plan.p3 ? c->V(V_P2) : nullptr, c->V(V_C3),
+  SweepB fb{c->rp, c->ci, c->C3f, c->mir, (int)c->nact, c->plan.p3 ? c->V(V_P2) : nullptr,
+            c->V(V_C3),
             c->plan.d14 ? c->V(V_D14) : nullptr, c->plan.d10 ? c->V(V_D10) : nullptr,
             c->plan.p3 ? c->V(V_P3) : nullptr};
   run_rows<G>(c, fb);
@@ -572,9 +573,12 @@ void sweep_a(fglt_ctx* c) {
 }
 
 
-void local_sweeps(fglt_ctx* c) {
+// Vertex sweeps over the per-edge triangle counts. The counts stay at the
+// canonical slots (SweepB reads lower neighbours through mir); the per-kernel
+// API, which hands C3 out in CSR order, mirrors them first.
+void local_sweeps(fglt_ctx* c, bool mirror_c3 = false) {
   if (!c->plan.c3 || c->n == 0) return;
-  if (c->m > 0) {
+  if (mirror_c3 && c->m > 0) {
     k_c3_mirror<<<c->grid(c->m, 256), 256, 0, c->stream>>>(c->ce_pos, c->mir, c->orp + c->n,
                                                           c->C3f);
     check_launch();
@@ -1961,7 +1965,7 @@ void api_c3(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t nn
   if (n == 0) return;
   read_graph_stats(c);
   triangles(c, 0, n);
-  local_sweeps(c);
+  local_sweeps(c, true);
   k_api_map_c3<<<c->grid(n * 32, 256), 256, 0, c->stream>>>(d_rp, d_ci, (int)n, c->inv, c->rp,
                                                            c->ci, c->C3f, c->V(V_C3), C3, c3);
   check_launch();

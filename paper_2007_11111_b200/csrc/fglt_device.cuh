@@ -397,19 +397,25 @@ __global__ void k_c3_mirror(const int* __restrict__ ce_pos, const int* __restric
 // p3 = sum p2_j - (d(d-1) + 2 c3) rectified   (kernels.cpp:91-107, :176-205)
 // Sweep B: c3 = sum C3 / 2; d14 = sum C(C3,2); d10 = sum C3 * (d_j - 2)+;
 // p3 = sum p2_j - (d(d-1) + 2 c3) rectified   (kernels.cpp:91-107, :176-205)
+// C3f holds each edge's count at its canonical slot only (row min(u,v)'s
+// suffix, where the triangle pass adds); a lower neighbour j < r reads it
+// through mir. Rows r >= n_active (degree <= 1) have no triangles: their
+// slots stay 0 and have no mirror entry.
 struct SweepB {
   static constexpr int NV = 4;
   const int* rp;
   const int* ci;
   const u32* C3f;
+  const int* mir;
+  int nact;
   const u64* p2;
   u64* c3;
   u64* d14;
   u64* d10;
   u64* p3;
-  __device__ void elem(int, int p, u64 (&acc)[NV]) const {
+  __device__ void elem(int r, int p, u64 (&acc)[NV]) const {
     const int j = ci[p];
-    const u64 c = C3f[p];
+    const u64 c = C3f[j < r && r < nact ? mir[p] : p];
     acc[0] += c;
     acc[1] += c * (c - (c > 0)) / 2;
     const u64 dj = (u64)(rp[j + 1] - rp[j]);

@@ -113,7 +113,7 @@ __device__ __forceinline__ u32 hash_get_claim(const int* keys, u32* vals, int lo
 // indexing via shift insertion), L[w] by pairwise equality. No shared table to
 // clear and no warp-wide bookkeeping per root; k_c4_warp skips these roots.
 #ifndef FGLT_C4_TINY
-#define FGLT_C4_TINY 8
+#define FGLT_C4_TINY 16
 #endif
 constexpr int kC4Tiny = FGLT_C4_TINY;
 __global__ void __launch_bounds__(256) k_c4_tiny(const int* __restrict__ rp,
