@@ -58,8 +58,14 @@ class Clocks:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.lines = []
+        self.reader = None
+        self.t0 = None
 
     def start(self):
+        """Start sampling every 100 ms; returns once the first sample is in,
+        so the samples taken after mark() cover the timed region."""
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -67,15 +73,29 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
+
+        def read():
+            for line in self.proc.stdout:
+                self.lines.append((time.time(), line))
+        self.reader = threading.Thread(target=read, daemon=True)
+        self.reader.start()
+        t_end = time.time() + 5
+        while not self.lines and time.time() < t_end:
+            time.sleep(0.02)
+
+    def mark(self):
+        self.t0 = time.time()
 
     def stop(self):
         if not self.proc:
             return None
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
+        self.reader.join(timeout=10)
+        t0 = self.t0 or 0.0
         sm, smax, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in (ln for t, ln in self.lines if t >= t0):
             f = [x.strip() for x in line.split(",")]
             if len(f) < 8:
                 continue
@@ -280,7 +300,7 @@ def cpu_baseline_leg(rp, ci, name, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -355,6 +375,7 @@ def main():
     clocks = Clocks(local)
     clocks.start()
     barrier()
+    clocks.mark()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)

@@ -2207,12 +2207,15 @@ __global__ void k_trilist_bound(const int* __restrict__ split, const int* __rest
     if (s >= 2 && s <= (unsigned long long)kTriListMaxS) {
       unsigned long long b = s * (s - 1) / 2;
 #if FGLT_TL_TIGHT
-      // a triangle {u, x, y} (x < y) is found from x as y in N+(x): at most
-      // sum_x |N+(x)| of them
+      // a triangle {u, S[a], y} (y > S[a]) is found from member a as y in
+      // N+(S[a]) ∩ S[a+1..]: at most min(|N+(S[a])|, s - 1 - a) of them
       unsigned long long o = 0;
-      for (int p = split[u]; p < send[u] && o < b; ++p) {
-        const int x = ci[p];
-        o += (unsigned long long)(send[x] - split[x]);
+      const int s0 = split[u];
+      for (int a = 0; a < (int)s && o < b; ++a) {
+        const int x = ci[s0 + a];
+        const unsigned long long out = (unsigned long long)(send[x] - split[x]);
+        const unsigned long long rest = s - 1 - (unsigned long long)a;
+        o += out < rest ? out : rest;
       }
       b = o < b ? o : b;
 #endif

@@ -35,6 +35,7 @@ struct Args {
   std::string input, format = "auto", dict = "all", output, emit = "net", separator = "tab";
   bool header = false, symmetrize = true, lenient = false, timing = false, oracle = false;
   int threads = 0, device = 0;
+  std::vector<int> devices;  // --devices 0,1,...: single-process multi-GPU
 };
 
 const char* kUsage =
@@ -42,7 +43,7 @@ const char* kUsage =
     "usage: glt INPUT [--format auto|edgelist|mtx] [--dict SPEC] [-o FILE]\n"
     "           [--emit raw|net|both] [--separator tab|comma] [--header]\n"
     "           [--symmetrize|--no-symmetrize] [--lenient] [--threads N] [--timing]\n"
-    "           [--oracle] [--device D]\n";
+    "           [--oracle] [--device D] [--devices D0,D1,...]\n";
 
 struct UsageError {
   std::string msg;
@@ -101,6 +102,13 @@ Args parse_args(int argc, char** argv) {
       a.threads = integer(s, val(s));
     } else if (s == "--device") {
       a.device = integer(s, val(s));
+    } else if (s == "--devices") {
+      const std::string list = val(s);
+      for (std::size_t at = 0; at <= list.size();) {
+        const std::size_t comma = std::min(list.find(',', at), list.size());
+        a.devices.push_back(integer(s, list.substr(at, comma - at)));
+        at = comma + 1;
+      }
     } else if (s == "--timing") {
       a.timing = true;
     } else if (s == "--oracle") {
@@ -228,6 +236,7 @@ int run(const Args& a) {
   t.threads = threads;
   t.lenient = a.lenient;
   t.device = a.device;
+  t.devices = a.devices;
   if (a.oracle) {
     t.dict = graphlet::Dictionary::all();
     auto r = graphlet::transform(g, t);

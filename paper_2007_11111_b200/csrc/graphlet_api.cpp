@@ -683,6 +683,19 @@ RawFrequencyField raw_frequencies(const SparseAdjacency& g, const Dictionary& di
 TransformResult transform(const SparseAdjacency& g, const TransformOptions& opt) {
   TransformResult r{RawFrequencyField(g.num_vertices(), opt.dict),
                     NetFrequencyField(g.num_vertices(), opt.dict), {}};
+  if (opt.devices.size() > 1) {  // single-process multi-GPU (fglt_multi.cpp)
+    const Csr32& c = g.csr32();
+    fglt_stats st{};
+    fglt_error err{};
+    const int rc = fglt_transform_multi(
+        c.row_ptr.data(), c.col_idx.data(), g.num_vertices(),
+        static_cast<std::int64_t>(c.col_idx.size()), opt.dict.mask(), opt.lenient ? 1 : 0,
+        opt.devices.data(), static_cast<int>(opt.devices.size()), 0u, r.raw.mutable_data(),
+        r.net.mutable_data(), &st, &err);
+    if (rc) rethrow(rc, err);
+    r.stats = stats_of(st);
+    return r;
+  }
   run(g, opt.dict, opt.lenient, opt.device, r.raw.mutable_data(), r.net.mutable_data(), &r.stats);
   return r;
 }

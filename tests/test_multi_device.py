@@ -67,3 +67,31 @@ def test_multi_nccl_clique_when_available(ctx):
     raw1, net1, _ = ctx.transform_host(rp, ci, 0xFFFF)
     raw, net, _ = _capi.transform_multi(rp, ci, list(range(n)))
     assert np.array_equal(raw, raw1) and np.array_equal(net, net1)
+
+
+def test_python_and_cli_devices_option(tmp_path):
+    """graphlet::transform with TransformOptions::devices (the Python
+    `devices=` keyword and `glt --devices`) routes to fglt_transform_multi."""
+    import os
+    import subprocess
+
+    import paper_2007_11111_b200 as gt
+    rp, ci = CASES["sbm"]
+    g = gt.from_csr(rp, ci)
+    raw1, net1 = gt.transform(g)
+    raw2, net2 = gt.transform(g, devices=[0, 0])
+    assert np.array_equal(raw1, raw2) and np.array_equal(net1, net2)
+    edges = tmp_path / "g.edges"
+    with open(edges, "w") as f:
+        for u in range(len(rp) - 1):
+            for v in ci[rp[u]:rp[u + 1]]:
+                if v > u:
+                    f.write(f"{u} {v}\n")
+    glt = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "paper_2007_11111_b200", "glt")
+    outs = []
+    for extra in ([], ["--devices", "0,0,0"]):
+        out = tmp_path / ("o" + str(len(extra)))
+        subprocess.run([glt, str(edges), "--emit", "both", "-o", str(out), *extra], check=True)
+        outs.append(open(str(out) + ".raw").read() + open(str(out) + ".net").read())
+    assert outs[0] == outs[1]
