@@ -372,6 +372,9 @@ constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many w
 #ifndef FGLT_QUADS
 #define FGLT_QUADS 2
 #endif
+#ifndef FGLT_BATCH_LANE_ROW
+#define FGLT_BATCH_LANE_ROW 1  // dense long-row batches: lane per row instead of flattened quads
+#endif
 constexpr int kQuadsInFlight = FGLT_QUADS;          // 16-byte loads in flight per lane (dense batches)
 constexpr int kC4BlockThreads = FGLT_C4B_THREADS;  // class-4 block (one 128 KB table per SM)
 
@@ -993,6 +996,28 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
           }
           segend[q] = se;
         }
+#if FGLT_BATCH_LANE_ROW
+        // lane per row: the batch's rows are consecutive in N-(u), so their
+        // degrees (and tile segments) are similar; each lane streams its own
+        // segment with 16-byte loads, no flattening bookkeeping per quad
+        if (se > st) {
+          int p = st;
+          for (; p < se && (p & 3); ++p) inc(__ldg(ci + p) - lo);
+          for (; p + 8 <= se; p += 8) {
+            const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
+            const int4 y = __ldg(reinterpret_cast<const int4*>(ci + p + 4));
+            inc(x.x - lo); inc(x.y - lo); inc(x.z - lo); inc(x.w - lo);
+            inc(y.x - lo); inc(y.y - lo); inc(y.z - lo); inc(y.w - lo);
+          }
+          if (p + 4 <= se) {
+            const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
+            inc(x.x - lo); inc(x.y - lo); inc(x.z - lo); inc(x.w - lo);
+            p += 4;
+          }
+          for (; p < se; ++p) inc(__ldg(ci + p) - lo);
+        }
+        continue;
+#endif
         // flattened over 16-byte quads of ci: quad k of row r is ci[4 (bst[r] + k)]
         // + 0..3, elements outside [st, se) masked
         const int qa = st >> 2;
@@ -1120,6 +1145,33 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         const bool valid = q < qg;
         const int st = valid ? cur[q] : 0;
         const int se = valid ? segend[q] : 0;
+#if FGLT_BATCH_LANE_ROW
+        {
+          u64 sv = 0;
+          typename std::conditional<PACK, u32, u64>::type ps = 0;
+          int p = st;
+          for (; p < se && (p & 3); ++p) ps += get(__ldg(ci + p) - lo) - 1;
+          for (; p + 8 <= se; p += 8) {
+            const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
+            const int4 y = __ldg(reinterpret_cast<const int4*>(ci + p + 4));
+            ps += get(x.x - lo) + get(x.y - lo) + get(x.z - lo) + get(x.w - lo) - 4;
+            ps += get(y.x - lo) + get(y.y - lo) + get(y.z - lo) + get(y.w - lo) - 4;
+            if (PACK) { sv += ps; ps = 0; }
+          }
+          if (p + 4 <= se) {
+            const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
+            ps += get(x.x - lo) + get(x.y - lo) + get(x.z - lo) + get(x.w - lo) - 4;
+            p += 4;
+          }
+          for (; p < se; ++p) ps += get(__ldg(ci + p) - lo) - 1;
+          sv += ps;
+          if (valid) {
+            if (sv) atomicAdd(c4 + ci[b + q], sv);
+            cur[q] = se;
+          }
+        }
+        continue;
+#endif
         const int qa = st >> 2;
         const int nqd = se > st ? ((se + 3) >> 2) - qa : 0;
         int T;

@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-bash tools/run_variants.sh 5 msort64 c4t16
-bash tools/run_variants.sh 2 msort64 c4t16
-bash tools/run_variants.sh 3 msort64
-timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_kernels_api.py tests/test_multi_device.py -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_par.log 2>&1
-echo "pytest rc=$?"; tail -3 gpurun_out/pytest_par.log
+bash tools/run_variants.sh 3 lanerow
+bash tools/run_variants.sh 4 lanerow
+export FGLT_LIB_OVERRIDE=$PWD/variants/lanerow/libfglt.so
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "forced or rmat or full_size or golden" > gpurun_out/pytest_lanerow.log 2>&1
+echo "pytest lanerow rc=$?"; tail -3 gpurun_out/pytest_lanerow.log
