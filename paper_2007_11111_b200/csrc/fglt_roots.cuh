@@ -372,9 +372,17 @@ constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many w
 #ifndef FGLT_QUADS
 #define FGLT_QUADS 2
 #endif
+#ifndef FGLT_ROOTS_LANE_MEMBER
+#define FGLT_ROOTS_LANE_MEMBER 0  // root probes: thread per member instead of block-flattened quads
+#endif
 #ifndef FGLT_BATCH_LANE_ROW
 #define FGLT_BATCH_LANE_ROW 1  // dense long-row batches: lane per row instead of flattened quads
 #endif
+#ifndef FGLT_BATCH_G
+#define FGLT_BATCH_G 2  // lanes per row in lane-row batches (1, 2, 4, 8)
+#endif
+constexpr int kBatchG = FGLT_BATCH_LANE_ROW ? FGLT_BATCH_G : 1;
+constexpr int kBatchRows = 32 / kBatchG;
 constexpr int kQuadsInFlight = FGLT_QUADS;          // 16-byte loads in flight per lane (dense batches)
 constexpr int kC4BlockThreads = FGLT_C4B_THREADS;  // class-4 block (one 128 KB table per SM)
 
@@ -913,7 +921,8 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
       if (rp[v + 1] - rp[v] < giant_deg) lo_q = mid + 1; else hi_q = mid;
     }
     const int qg = lo_q;
-    const int nb = (qg - qs + 31) >> 5;  // batches of 32 long rows
+    // batches of kBatchRows long rows (kBatchG lanes per row in lane-row mode)
+    const int nb = (qg - qs + kBatchRows - 1) / kBatchRows;
     // short rows walk with per-row cursors across the tiles; a split item
     // (one tile of a root) takes their segments from the tile boundaries
     if (!split_kt)
@@ -980,7 +989,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         bt = __shfl_sync(0xffffffffu, bt, 0);
         if (bt >= nb) break;
         bt = nb - 1 - bt;  // largest rows first
-        const int q = qs + (bt << 5) + lane;
+        const int q = qs + bt * kBatchRows + lane / kBatchG;
         const bool valid = q < qg;
         int st = 0, se = 0;
         if (valid) {
@@ -989,11 +998,15 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
             const int v = ci[b + q];
             st = bnd[kb_lo * bnd_stride + v];
             se = hi >= u ? em : min(em, bnd[kb_hi * bnd_stride + v]);
-            cur[q] = st;
           } else {
             st = cur[q];
             se = hi >= u ? em : lower_bound_i32(ci, st, em, hi);
           }
+        }
+        // a row's lanes all read the old cursor before any of them writes
+        __syncwarp();
+        if (valid && (lane & (kBatchG - 1)) == 0) {
+          cur[q] = st;
           segend[q] = se;
         }
 #if FGLT_BATCH_LANE_ROW
@@ -1001,20 +1014,21 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         // degrees (and tile segments) are similar; each lane streams its own
         // segment with 16-byte loads, no flattening bookkeeping per quad
         if (se > st) {
-          int p = st;
-          for (; p < se && (p & 3); ++p) inc(__ldg(ci + p) - lo);
-          for (; p + 8 <= se; p += 8) {
+          const int sub = lane & (kBatchG - 1);
+          const int a0 = min(se, (st + 3) & ~3), a1 = max(a0, se & ~3);
+          for (int p = st + sub; p < a0; p += kBatchG) inc(__ldg(ci + p) - lo);
+          int p = a0 + 4 * sub;
+          for (; p + 4 * kBatchG < a1; p += 8 * kBatchG) {
             const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
-            const int4 y = __ldg(reinterpret_cast<const int4*>(ci + p + 4));
+            const int4 y = __ldg(reinterpret_cast<const int4*>(ci + p + 4 * kBatchG));
             inc(x.x - lo); inc(x.y - lo); inc(x.z - lo); inc(x.w - lo);
             inc(y.x - lo); inc(y.y - lo); inc(y.z - lo); inc(y.w - lo);
           }
-          if (p + 4 <= se) {
+          if (p < a1) {
             const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
             inc(x.x - lo); inc(x.y - lo); inc(x.z - lo); inc(x.w - lo);
-            p += 4;
           }
-          for (; p < se; ++p) inc(__ldg(ci + p) - lo);
+          for (int pt = a1 + sub; pt < se; pt += kBatchG) inc(__ldg(ci + pt) - lo);
         }
         continue;
 #endif
@@ -1141,31 +1155,36 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         bt = __shfl_sync(0xffffffffu, bt, 0);
         if (bt >= nb) break;
         bt = nb - 1 - bt;  // largest rows first
-        const int q = qs + (bt << 5) + lane;
+        const int q = qs + bt * kBatchRows + lane / kBatchG;
         const bool valid = q < qg;
         const int st = valid ? cur[q] : 0;
         const int se = valid ? segend[q] : 0;
 #if FGLT_BATCH_LANE_ROW
         {
+          const int sub = lane & (kBatchG - 1);
           u64 sv = 0;
           typename std::conditional<PACK, u32, u64>::type ps = 0;
-          int p = st;
-          for (; p < se && (p & 3); ++p) ps += get(__ldg(ci + p) - lo) - 1;
-          for (; p + 8 <= se; p += 8) {
-            const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
-            const int4 y = __ldg(reinterpret_cast<const int4*>(ci + p + 4));
-            ps += get(x.x - lo) + get(x.y - lo) + get(x.z - lo) + get(x.w - lo) - 4;
-            ps += get(y.x - lo) + get(y.y - lo) + get(y.z - lo) + get(y.w - lo) - 4;
-            if (PACK) { sv += ps; ps = 0; }
+          if (se > st) {
+            const int a0 = min(se, (st + 3) & ~3), a1 = max(a0, se & ~3);
+            for (int p = st + sub; p < a0; p += kBatchG) ps += get(__ldg(ci + p) - lo) - 1;
+            int p = a0 + 4 * sub;
+            for (; p + 4 * kBatchG < a1; p += 8 * kBatchG) {
+              const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
+              const int4 y = __ldg(reinterpret_cast<const int4*>(ci + p + 4 * kBatchG));
+              ps += get(x.x - lo) + get(x.y - lo) + get(x.z - lo) + get(x.w - lo) - 4;
+              ps += get(y.x - lo) + get(y.y - lo) + get(y.z - lo) + get(y.w - lo) - 4;
+              if (PACK) { sv += ps; ps = 0; }
+            }
+            if (p < a1) {
+              const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
+              ps += get(x.x - lo) + get(x.y - lo) + get(x.z - lo) + get(x.w - lo) - 4;
+            }
+            for (int pt = a1 + sub; pt < se; pt += kBatchG) ps += get(__ldg(ci + pt) - lo) - 1;
           }
-          if (p + 4 <= se) {
-            const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
-            ps += get(x.x - lo) + get(x.y - lo) + get(x.z - lo) + get(x.w - lo) - 4;
-            p += 4;
-          }
-          for (; p < se; ++p) ps += get(__ldg(ci + p) - lo) - 1;
           sv += ps;
-          if (valid) {
+#pragma unroll
+          for (int o = kBatchG / 2; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+          if (valid && sub == 0) {
             if (sv) atomicAdd(c4 + ci[b + q], sv);
             cur[q] = se;
           }
@@ -1916,6 +1935,24 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         block_flatten(nqd, qa, f_off, f_st, f_wtot,
                       [&](int T) { tl_reserve(4ull * (unsigned long long)T); });
       }
+#if FGLT_ROOTS_LANE_MEMBER
+      if (!pairs && se > st) {  // thread per member: stream its own probe list
+        to_row(c0, threadIdx.x);
+        auto one = [&](int pp, int y) {
+          const int bi = s_hash_find(hkeys, hidx, hlog, y);
+          if (bi >= 0) hit(a_me, bi, pp);
+        };
+        int p = st;
+        for (; p < se && (p & 3); ++p) one(p, __ldg(ci + p));
+        for (; p + 4 <= se; p += 4) {
+          const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
+          one(p, x.x); one(p + 1, x.y); one(p + 2, x.z); one(p + 3, x.w);
+        }
+        for (; p < se; ++p) one(p, __ldg(ci + p));
+        flush(c0);
+      }
+      if (false)
+#endif
       {
         const int T = f_off[NT];
         const int per = (T + NWB - 1) / NWB;

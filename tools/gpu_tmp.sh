@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-bash tools/run_variants.sh 3 lanerow
-bash tools/run_variants.sh 4 lanerow
-export FGLT_LIB_OVERRIDE=$PWD/variants/lanerow/libfglt.so
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "forced or rmat or full_size or golden" > gpurun_out/pytest_lanerow.log 2>&1
-echo "pytest lanerow rc=$?"; tail -3 gpurun_out/pytest_lanerow.log
+bash tools/run_variants.sh 3 g1 g2 g4
+bash tools/run_variants.sh 4 g2 g4
