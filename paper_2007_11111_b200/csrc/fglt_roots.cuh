@@ -339,7 +339,10 @@ constexpr u64 kC4HashFill = 3ull << (kC4HashLog - 2);  // distinct targets per p
 constexpr int kC4DenseThreads = FGLT_DENSE_THREADS;     // big: one block per SM
 constexpr int kC4TileBytes = FGLT_DENSE_TILE_BYTES;     // big: counter tile (192 KB)
 constexpr int kC4DenseThreadsS = 512;                   // small: two blocks per SM
-constexpr int kC4TileBytesS = 98304;                    // small: 96 KB tiles
+#ifndef FGLT_TILE_BYTES_S
+#define FGLT_TILE_BYTES_S 98304
+#endif
+constexpr int kC4TileBytesS = FGLT_TILE_BYTES_S;        // small: 96 KB tiles
 #ifndef FGLT_ROW_TILE
 #define FGLT_ROW_TILE 1  // cost of one row's segment setup per tile, in wedges
 #endif
@@ -855,7 +858,9 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   const int split_kt = SPLIT ? split_kt_arg : 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ u64 red[32];
-  constexpr int NW = NT / 32;
+  // per-warp flattening tables of the quad-flattened batches (unused, and
+  // reduced to one row, in lane-row mode: more shared memory for the tiles)
+  constexpr int NW = FGLT_BATCH_LANE_ROW ? 1 : NT / 32;
   __shared__ u64 rsum[NW][32];
   __shared__ int bst_all[NW][32];
   __shared__ int boff_all[NW][33];
@@ -867,11 +872,11 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   int* cur = cursor + (long long)blockIdx.x * 2 * cursor_stride;
   int* segend = cur + cursor_stride;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  u64* rs = rsum[wid];
-  int* bst = bst_all[wid];
-  int* boff = boff_all[wid];
-  int* bsa = bsa_all[wid];
-  int* bsb = bsb_all[wid];
+  u64* rs = rsum[wid % NW];
+  int* bst = bst_all[wid % NW];
+  int* boff = boff_all[wid % NW];
+  int* bsa = bsa_all[wid % NW];
+  int* bsb = bsb_all[wid % NW];
   // counters of the current tile: 2^sh per 32-bit word, 32 >> sh bits each
   int sh = 0;
   constexpr int kTileWords = (NT == kC4DenseThreadsS ? kC4TileBytesS : kC4TileBytes) / 4;
