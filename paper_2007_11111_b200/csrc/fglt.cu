@@ -979,11 +979,11 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     if (cnt[1] > 0) {  // class 2: block-flattened tables of <= 2048 slots
       constexpr int NT2 = FGLT_C4_CLASS2_THREADS;
       const size_t sm = (size_t)(1 << kWarpHashLog2) * 8;
-      set_smem(k_c4_block<NT2>, sm);
+      set_smem(k_c4_block<NT2, true>, sm);
       int occ = 1;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<NT2>, NT2, sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<NT2, true>, NT2, sm));
       const int g = std::min(cnt[1], c->sms * std::max(occ, 1));
-      k_c4_block<NT2><<<g, NT2, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[1], cnt[1],
+      k_c4_block<NT2, true><<<g, NT2, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[1], cnt[1],
                                                 wc, parts, kWarpHashLog2, queues + 4, c4);
       check_launch();
       c->launched();
@@ -991,22 +991,22 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     if (cnt[7] > 0) {  // class 8: block-flattened tables of <= 1024 slots
       constexpr int NT8 = FGLT_C4_CLASS8_THREADS;
       const size_t sm = (size_t)(1 << (kWarpHashLog2 - 1)) * 8;
-      set_smem(k_c4_block<NT8>, sm);
+      set_smem(k_c4_block<NT8, true>, sm);
       int occ = 1;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<NT8>, NT8, sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<NT8, true>, NT8, sm));
       const int g = std::min(cnt[7], c->sms * std::max(occ, 1));
-      k_c4_block<NT8><<<g, NT8, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[7], cnt[7],
+      k_c4_block<NT8, true><<<g, NT8, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[7], cnt[7],
                                                 wc, parts, kWarpHashLog2 - 1, queues + 6, c4);
       check_launch();
       c->launched();
     }
     if (cnt[2] > 0) {  // class 3: 256-thread block-flattened tables of <= 4096 slots
       const size_t sm = (size_t)(1 << kC4SmallLog) * 8;
-      set_smem(k_c4_block<256>, sm);
+      set_smem(k_c4_block<256, true>, sm);
       int occ = 1;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<256>, 256, sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_c4_block<256, true>, 256, sm));
       const int g = std::min(cnt[2], c->sms * std::max(occ, 1));
-      k_c4_block<256><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[2], cnt[2],
+      k_c4_block<256, true><<<g, 256, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, lists[2], cnt[2],
                                                 wc, parts, kC4SmallLog, queues + 0, c4);
       check_launch();
       c->launched();

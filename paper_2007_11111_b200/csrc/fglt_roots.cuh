@@ -664,7 +664,7 @@ __device__ __forceinline__ int upper_row(const int* g_off, int k, int n) {
 // chunks of NT rows; each warp owns an equal contiguous share of the quads
 // (one binary search per lane to find its first row, then a forward walk), so
 // a root's work is balanced across all warps with no per-row serial loops.
-template <int NT>
+template <int NT, bool LANEROW = false>
 __global__ void __launch_bounds__(NT)
 k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
@@ -754,13 +754,46 @@ k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
           v4[i] = make_uint4(0, 0, 0, 0);
         }
       }
-      // count pass (block_flatten's barriers order the clear before inserts)
-      for (int c0 = b; c0 < s; c0 += NT) {
-        const int T = flatten(c0);
-        sweep_quads(T, [&](int, int w) {
-          if (P == 1 || part_of(w, P) == part) hash_insert(keys, vals, hlog, w);
-        });
+      // LANEROW (the <= 2048-wedge classes, whose rows have similar degree):
+      // rows of a chunk in lane groups: G = the largest power of two with
+      // rows x G <= NT lanes per row, each group streaming its row's
+      // segment (16-byte loads at stride G) — no per-quad row search/masks
+      auto group_stream = [&](int c0, auto&& f) {
+        const int nrows = min(NT, s - c0);
+        int G = 1;
+        while (G < 32 && nrows * (G * 2) <= NT) G *= 2;
+        const int row = threadIdx.x / G, sub = threadIdx.x & (G - 1);
+        const int q = c0 + row;
+        if (row < nrows) {
+          const int st = rp[ci[q]], se = mir[q];
+          if (se > st) {
+            const int a0 = min(se, (st + 3) & ~3), a1 = max(a0, se & ~3);
+            for (int p = st + sub; p < a0; p += G) f(__ldg(ci + p));
+            for (int p = a0 + 4 * sub; p < a1; p += 4 * G) {
+              const int4 x = __ldg(reinterpret_cast<const int4*>(ci + p));
+              f(x.x); f(x.y); f(x.z); f(x.w);
+            }
+            for (int p = a1 + sub; p < se; p += G) f(__ldg(ci + p));
+          }
+        }
+        return G;
+      };
+      if (LANEROW) {
+        __syncthreads();  // the clear before any insert
+        for (int c0 = b; c0 < s; c0 += NT)
+          group_stream(c0, [&](int w) {
+            if (P == 1 || part_of(w, P) == part) hash_insert(keys, vals, hlog, w);
+          });
         __syncthreads();
+      } else {
+        // count pass (block_flatten's barriers order the clear before inserts)
+        for (int c0 = b; c0 < s; c0 += NT) {
+          const int T = flatten(c0);
+          sweep_quads(T, [&](int, int w) {
+            if (P == 1 || part_of(w, P) == part) hash_insert(keys, vals, hlog, w);
+          });
+          __syncthreads();
+        }
       }
       for (int i = threadIdx.x; i < cap; i += NT) {
         const u32 l = vals[i];
@@ -771,6 +804,17 @@ k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
         }
       }
       // attribution pass: c4[v] += sum_w (L[w] - 1)
+      if (LANEROW)
+      for (int c0 = b; c0 < s; c0 += NT) {
+        u64 sv = 0;
+        const int G = group_stream(c0, [&](int w) {
+          if (P == 1 || part_of(w, P) == part) sv += hash_get(keys, vals, hlog, w) - 1;
+        });
+        for (int o = G / 2; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        const int row = threadIdx.x / G;
+        if ((threadIdx.x & (G - 1)) == 0 && c0 + row < s && sv) atomicAdd(c4 + ci[c0 + row], sv);
+      }
+      else
       for (int c0 = b; c0 < s; c0 += NT) {
         const int T = flatten(c0);
         int cr = -1;

@@ -42,6 +42,25 @@ __global__ void __cluster_dims__(8, 1, 1) k_dsmem(int iters, unsigned range, uns
   if (threadIdx.x == 0) out[blockIdx.x] = L[0];
 }
 
+// cluster of 2: every CTA adds into either half of the pair's combined
+// counters (its own or its partner's shared memory), like a dense tile split
+// over two SMs
+__global__ void __cluster_dims__(2, 1, 1) k_dsmem2(int iters, unsigned range, unsigned* out) {
+  extern __shared__ unsigned L[];
+  cg::cluster_group cl = cg::this_cluster();
+  for (unsigned i = threadIdx.x; i < range; i += blockDim.x) L[i] = 0;
+  cl.sync();
+  unsigned* mine = L;
+  unsigned* other = cl.map_shared_rank(L, cl.block_rank() ^ 1);
+  unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = 0; i < iters; ++i) {
+    s = hsh(s + i);
+    atomicAdd(((s & 1) ? other : mine) + ((s >> 1) % range), 1u);
+  }
+  cl.sync();
+  if (threadIdx.x == 0) out[blockIdx.x] = L[0];
+}
+
 __global__ void k_red(int iters, unsigned range, unsigned* arr) {
   unsigned s = blockIdx.x * blockDim.x + threadIdx.x;
   for (int i = 0; i < iters; ++i) {
@@ -88,6 +107,10 @@ int main() {
   cudaFuncSetAttribute(k_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, range * 4);
   double ops = (double)sms * threads * iters;
   time("smem atomicAdd (48K u32/CTA)", [&] { k_smem<<<sms, threads, range * 4>>>(iters, range, out); }, ops);
+  cudaFuncSetAttribute(k_dsmem2, cudaFuncAttributeMaxDynamicSharedMemorySize, range * 4);
+  time("dsmem atomicAdd (cluster 2, half remote)",
+       [&] { k_dsmem2<<<(sms / 2) * 2, threads, range * 4>>>(iters, range, out); },
+       (double)((sms / 2) * 2) * threads * iters);
   int g8 = (sms / 8) * 8;
   time("dsmem atomicAdd (cluster 8)", [&] { k_dsmem<<<g8, threads, range * 4>>>(iters, range, out); },
        (double)g8 * threads * iters);
