@@ -90,12 +90,17 @@ class Clocks:
     def stop(self):
         if not self.proc:
             return None
+        t1 = time.time()
+        time.sleep(0.15)  # one more sample: a timed region shorter than the period
         self.proc.terminate()
         self.reader.join(timeout=10)
         t0 = self.t0 or 0.0
+        inside = [ln for t, ln in self.lines if t0 <= t <= t1]
+        if not inside:  # region shorter than 100 ms: the samples bracketing it
+            inside = [ln for t, ln in self.lines if t0 - 0.15 <= t <= t1 + 0.15]
         sm, smax, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in (ln for t, ln in self.lines if t >= t0):
+        for line in inside:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 8:
                 continue

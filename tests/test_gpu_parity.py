@@ -157,6 +157,32 @@ def test_net_from_raw_corrupted(ctx):
     assert net[0, 14] == 0
 
 
+def test_net_from_raw_custom_matrix(ctx):
+    """net_from_raw honours the caller's ConversionMatrix (conversion.hpp:
+    14-37,49-51), not the built-in U16(s,s): a modified unit upper-triangular
+    U gives exactly the back substitution of that U (Python integers)."""
+    rp, ci = gu.er(40, 0.3, 77)
+    mask = FULL
+    raw, net16, _ = ctx.transform_host(rp, ci, mask)
+    U = ob.u16().astype(np.uint64)
+    np.testing.assert_array_equal(ctx.net_from_raw(raw, mask, U=U), net16)
+    U2 = U.copy()
+    U2[2, 4] = 1          # was 2
+    U2[5, 15] = 5         # was 6
+    got = ctx.net_from_raw(raw, mask, lenient=True, U=U2)
+    for v in range(raw.shape[0]):
+        x = [0] * 16
+        for r in range(15, -1, -1):
+            a = sum(int(U2[r, c]) * x[c] for c in range(r + 1, 16))
+            x[r] = max(int(raw[v, r]) - a, 0)
+        assert got[v].tolist() == x
+    bad = U2.copy()
+    bad[3, 1] = 1  # below the diagonal
+    with pytest.raises(_capi.TransformFailed) as ei:
+        ctx.net_from_raw(raw, mask, U=bad)
+    assert ei.value.code == 2
+
+
 def test_choose3_overflow_site(ctx):
     """choose3 (col 8) is the one checked site reachable with int32 CSR:
     a star with 2^22 leaves overflows d(d-1)/2*(d-2). Reference order: the
@@ -333,6 +359,28 @@ def test_stats_contract(ctx):
     _, _, st = ctx.transform_host(rp, ci)
     assert 0 < st["p2_row_touches"] <= st["p2_touch_bound"]
     assert st["p2_row_touches"] == st["W"] - len(ci)
+
+
+def test_per_call_scratch_and_phases(ctx):
+    """TransformStats are per call (the reference resets its MemoryTracker
+    each call, kernels.cpp:312): a small graph after a large one reports the
+    small graph's scratch and launches; the scratch report lists exactly the
+    counted buffers; phases carry CUDA-event times and the dense wedge units."""
+    big_rp, big_ci = graphs.rmat(14, 16, seed=2)
+    _, _, st_big = ctx.transform_host(big_rp, big_ci, timings=True)
+    rp, ci = gu.regular(400, 4, 11)
+    _, _, st = ctx.transform_host(rp, ci)
+    assert 0 < st["peak_aux_words"] < st_big["peak_aux_words"]
+    assert 0 < st["kernel_launches"] < 200
+    rep = ctx.scratch_report()
+    counted = sum(b for b, staging in rep.values() if not staging)
+    assert counted // 8 == st["peak_aux_words"]
+    assert st["largest_aux_alloc_words"] < (400 * 400) // 8
+    names = [p[0] for p in st_big["phases"]]
+    for must in ("prepare", "triangle pass", "four-cycle rows", "column fill"):
+        assert must in names
+    assert all(secs >= 0 for _, secs, _ in st_big["phases"])
+    assert ctx.smem_atomic_rate() > 1e11
 
 
 def test_sharded_stages_byte_identical(ctx):
