@@ -30,7 +30,7 @@ EXPORTS = [
     "fglt_ctx_scratch_report", "fglt_transform_multi",
 ]
 
-DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB, DEBUG_TRILIST = 1, 2, 3, 4, 5
+DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB, DEBUG_TRILIST, DEBUG_ROW_SORT = 1, 2, 3, 4, 5, 6
 
 
 class FgltError(ctypes.Structure):

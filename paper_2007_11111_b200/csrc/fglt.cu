@@ -59,8 +59,8 @@ constexpr int kWarpHashLog = 9;   // 512-slot table per warp (wc <= 256)
 constexpr int kWarpHashLog2 = 11; // 2048-slot table per warp (wc <= 1024)
 
 enum Buf {
-  B_RP_IN, B_CI_IN, B_KEYS, B_KEYS2, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
-  B_SPLIT, B_OUTDEG, B_ORP, B_MIR, B_CE_ROW, B_CE_POS, B_VEC, B_WORK, B_BINKEY, B_LISTS,
+  B_RP_IN, B_CI_IN, B_PERM, B_INV, B_NDEG, B_NRP, B_NCI, B_TMP,
+  B_SPLIT, B_MIR, B_VEC, B_WORK, B_BINKEY, B_LISTS,
   B_CUB, B_CURSOR, B_TBND, B_BIGROWS, B_HUB, B_HUBBASE, B_ROWOF, B_KEYSOUT, B_GBM, B_RAW, B_NET, B_DICT, B_SMALL, B_RLISTS, B_RKEY,
   B_ING_E, B_ING_K, B_ING_K2, B_ING_RP, B_ING_CI, B_SEND, B_SORTK, B_SORTV,
   B_API0, B_API1, B_API2, B_API3, B_API4, B_API5, B_TB, B_TLREC, B_TLPIECES, B_TLFAIL, B_TBS, B_TBNDS, B_CURSORS, B_TLCHUNKS,
@@ -68,8 +68,8 @@ enum Buf {
 };
 
 const char* const kBufName[] = {
-  "rp_in", "ci_in", "keys", "keys2", "perm", "inv", "ndeg", "nrp", "nci", "tmp_c3",
-  "split", "outdeg", "orp", "mir", "ce_row", "ce_pos", "vec", "work", "binkey", "lists",
+  "rp_in", "ci_in", "perm", "inv", "ndeg", "nrp", "nci", "tmp_c3",
+  "split", "mir", "vec", "work", "binkey", "lists",
   "cub", "cursor", "tbnd", "bigrows", "hub", "hubbase", "rowof", "keysout", "gbm", "raw", "net",
   "dict", "small", "rlists", "rkey",
   "ing_e", "ing_k", "ing_k2", "ing_rp", "ing_ci", "send", "sortk", "sortv",
@@ -80,6 +80,7 @@ static_assert(sizeof(kBufName) / sizeof(kBufName[0]) == B_COUNT, "buffer names")
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  size_t req = 0;     // bytes the current call asked for (<= cap: capacity is kept across calls)
   uint64_t call = 0;  // last call that used this buffer (per-call accounting)
 };
 
@@ -213,10 +214,7 @@ struct fglt_ctx {
   int* inv = nullptr;
   int* split = nullptr;
   int* send = nullptr;  // end of the active part of N+(u)
-  int* orp = nullptr;
   int* mir = nullptr;
-  int* ce_row = nullptr;
-  int* ce_pos = nullptr;
   u32* C3f = nullptr;
   u64* vec = nullptr;
   DictInfo* d_dict = nullptr;
@@ -234,6 +232,7 @@ struct fglt_ctx {
 
   // test hooks (fglt_ctx_set_debug): force one code path for every root
   int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1, force_hub = 0;
+  int force_row_sort = 0;  // 2: never take the in-register row sort (k_fill_sort)
   // triangle list (k_roots_block -> k_diamond_list); tl_mode: 0 auto, 1 off,
   // 2 a tiny pool (test hook: most roots fall back to the probing pass)
   int tl_mode = 0;
@@ -261,30 +260,35 @@ struct fglt_ctx {
     launches_at_call = launches;
   }
 
+  // Per-call accounting charges what the call asked for (plus the growth
+  // slack when this call allocated), not the capacity an earlier, larger
+  // graph left behind.
   template <class T>
   T* ensure(Buf b, size_t count) {
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
     DevBuf& d = buf[b];
-    const bool counted = d.call == call;
+    if (d.call != call) {
+      d.call = call;
+      d.req = 0;
+    }
     if (d.cap < bytes) {
       if (d.p) {
         CK(cudaFreeAsync(d.p, stream));
         scratch_bytes -= d.cap;
-        if (counted && !is_staging(b)) call_bytes -= d.cap;
       }
       size_t grow = bytes + bytes / 8;
       CK(cudaMallocAsync(&d.p, grow, stream));
       d.cap = grow;
       scratch_bytes += grow;
-      if (counted && !is_staging(b)) call_bytes += grow;
+      bytes = grow;
     }
-    if (!counted) {
-      d.call = call;
-      if (!is_staging(b)) call_bytes += d.cap;
+    if (bytes > d.req) {
+      if (!is_staging(b)) call_bytes += bytes - d.req;
+      d.req = bytes;
     }
     if (!is_staging(b)) {
       peak_scratch = std::max(peak_scratch, call_bytes);
-      largest = std::max(largest, d.cap);
+      largest = std::max(largest, d.req);
     }
     return reinterpret_cast<T*>(d.p);
   }
@@ -381,7 +385,7 @@ void launch_probe_work(fglt_ctx* c, u64* tw) {
 
 template <int G>
 void launch_c4_hashp(fglt_ctx* c, int g, int block, size_t sm, const int* roots, int nroots,
-                     const u64* wc, const u64* parts, int max_log, int* queue, u64* c4) {
+                     const u64* wc, const u32* parts, int max_log, int* queue, u64* c4) {
   set_smem(k_c4_hashp<G>, sm);
   k_c4_hashp<G><<<g, block, sm, c->stream>>>(c->rp, c->ci, c->split, c->mir, roots, nroots, wc,
                                              parts, max_log, queue, c4);
@@ -406,22 +410,43 @@ void launch_fill_rows(fglt_ctx* c, const int* rp, const int* ci, const int* perm
   c->launched();
 }
 
+// Low-degree graphs (d_max <= 4 G): rows relabelled, sorted and split by their
+// own lane group (k_fill_sort); K = elements per lane.
 template <int G>
-void launch_mirror(fglt_ctx* c, const int* split, const int* send, const int* orp, int n, int* mir,
-                   int* ce_row, int* ce_pos) {
-  k_mirror<G><<<c->grid((int64_t)n * G, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, send, orp,
-                                                                   n, mir, ce_row, ce_pos);
+void launch_fill_sort(fglt_ctx* c, const int* rp, const int* ci, const int* perm, const int* inv,
+                      const int* nrp, int n, int* out, int* split, int* send) {
+  const int K = (int)((c->dmax + G - 1) / G);
+  const int g = c->grid((int64_t)n * G, 256);
+  u64* nact_p = c->d_small + 4;
+  u64* maxout = c->d_small + 3;
+  if (K <= 1)
+    k_fill_sort<G, 1><<<g, 256, 0, c->stream>>>(rp, ci, perm, inv, nrp, n, nact_p, out, split, send, maxout);
+  else if (K == 2)
+    k_fill_sort<G, 2><<<g, 256, 0, c->stream>>>(rp, ci, perm, inv, nrp, n, nact_p, out, split, send, maxout);
+  else
+    k_fill_sort<G, 4><<<g, 256, 0, c->stream>>>(rp, ci, perm, inv, nrp, n, nact_p, out, split, send, maxout);
   check_launch();
   c->launched();
 }
 
 template <int G>
-void launch_canon(fglt_ctx* c, const int* split, const int* send, const int* orp, int n,
-                  int* ce_row, int* ce_pos) {
-  k_canon<G><<<c->grid((int64_t)n * G, 256), 256, 0, c->stream>>>(split, send, orp, n, ce_row,
-                                                                  ce_pos);
+void launch_mirror(fglt_ctx* c, const int* split, const int* send, int n, int* mir) {
+  k_mirror<G><<<c->grid((int64_t)n * G, 256), 256, 0, c->stream>>>(c->rp, c->ci, split, send, n,
+                                                                   mir);
   check_launch();
   c->launched();
+}
+
+// Graph totals of the INPUT row pointer (k_graph_stats): W, d_max, n_active.
+// Read once, early: d_max picks the relabel path; the device keeps working on
+// the degree sort while the host waits.
+void read_input_stats(fglt_ctx* c) {
+  u64 h[4];
+  CK(cudaMemcpyAsync(h, c->d_small + 1, 32, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->W = h[0];
+  c->dmax = h[1];
+  c->nact = h[3];
 }
 
 // ------------------------------------------------------------------ prepare
@@ -460,98 +485,110 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   if (!c->plan.enumerate || n == 0) return;
 
   // ---- degree relabel: rank by (degree, id) = stable sort of the ids by
-  // the degree key (k_degree_keys), over the key's live bits only
-  int* keys = c->ensure<int>(B_KEYS, 2 * (size_t)n);   // keys | ids
-  int* keys2 = c->ensure<int>(B_KEYS2, 2 * (size_t)n); // sorted keys | sorted ids
-  int key_bits = 1;
-  while (key_bits < 31 && ((int64_t)1 << key_bits) <= n + 1) ++key_bits;
-  k_degree_keys<<<c->grid(n, 256), 256, 0, c->stream>>>(d_rp, N, keys, keys + n);
-  check_launch();
-  c->launched();
-  size_t tmp_bytes = 0, t2 = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, keys + n, keys2 + n, N, 0,
-                                     key_bits, c->stream));
+  // the degree key (k_degree_keys), over the key's live bits only. Every sort
+  // here runs on cub::DoubleBuffer pairs of our own arrays: no hidden
+  // (keys + values)-sized temporary.
+  // The sort's four n-int arrays are buffers nothing has written yet: keys in
+  // (nrp, ndeg), ids in (split, perm); if the sorted ids land in perm itself,
+  // k_perm's copy is the identity.
   int* perm = c->ensure<int>(B_PERM, n);
   int* inv = c->ensure<int>(B_INV, n);
   int* ndeg = c->ensure<int>(B_NDEG, n + 1);
   int* nrp = c->ensure<int>(B_NRP, n + 1);
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, ndeg, nrp, N + 1, c->stream));
-  tmp_bytes = std::max(tmp_bytes, t2);
-  size_t t3 = 0;
+  int* split = c->ensure<int>(B_SPLIT, n);
+  int* send = c->ensure<int>(B_SEND, n);
+  int key_bits = 1;
+  while (key_bits < 31 && ((int64_t)1 << key_bits) <= n + 1) ++key_bits;
+  k_degree_keys<<<c->grid(n, 256), 256, 0, c->stream>>>(d_rp, N, nrp, split);
+  check_launch();
+  c->launched();
   int id_bits = 1;
   while (id_bits < 31 && ((int64_t)1 << id_bits) < n) ++id_bits;
-  int* tmp = c->ensure<int>(B_TMP, std::max<int64_t>(nnz, 1));
-  int* row_of = c->ensure<int>(B_ROWOF, std::max<int64_t>(nnz, 1));
-  int* keys_out = c->ensure<int>(B_KEYSOUT, std::max<int64_t>(nnz, 1));
-  int* nci = c->ensure<int>(B_NCI, std::max<int64_t>(nnz, 1) + 4);  // +4: 16-byte tail reads
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, tmp, keys_out, row_of, nci, (int)nnz, 0, id_bits,
-                                     c->stream));
-  tmp_bytes = std::max(tmp_bytes, t3);
+  size_t tmp_bytes = 0, t2 = 0, t3 = 0;
+  {
+    cub::DoubleBuffer<int> dk(nrp, ndeg), dv(split, perm);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, N, 0, key_bits, c->stream));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, ndeg, nrp, N + 1, c->stream));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, dk, dv, (int)std::max<int64_t>(nnz, 1), 0,
+                                       id_bits, c->stream));  // size query only
+  }
+  tmp_bytes = std::max(tmp_bytes, std::max(t2, t3));
   void* cub_tmp = c->ensure<unsigned char>(B_CUB, tmp_bytes);
   size_t tb = c->buf[B_CUB].cap;
-  CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, keys, keys2, keys + n, keys2 + n, N, 0, key_bits,
-                                     c->stream));
+  const int* sorted_ids = nullptr;
+  {
+    cub::DoubleBuffer<int> dk(nrp, ndeg), dv(split, perm);
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, dk, dv, N, 0, key_bits, c->stream));
+    sorted_ids = dv.Current();
+  }
   c->launched();
+  read_input_stats(c);  // overlaps the degree sort
   CK(cudaMemsetAsync(ndeg + n, 0, sizeof(int), c->stream));
-  k_perm<<<c->grid(n, 256), 256, 0, c->stream>>>(keys2 + n, d_rp, N, perm, inv, ndeg);
+  k_perm<<<c->grid(n, 256), 256, 0, c->stream>>>(sorted_ids, d_rp, N, perm, inv, ndeg);
   check_launch();
   c->launched();
   tb = c->buf[B_CUB].cap;
   CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, ndeg, nrp, N + 1, c->stream));
   c->launched();
   const int G = group_for((double)nnz / (double)std::max<int64_t>(n, 1));
-  DISPATCH_G(G, launch_fill_rows, c, d_rp, d_ci, perm, inv, nrp, N, tmp, row_of);
-  tb = c->buf[B_CUB].cap;
-  if (nnz > 0) {  // stable sort by neighbour id: rows come out sorted (see k_fill_rows)
-    CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, tmp, keys_out, row_of, nci, (int)nnz, 0,
-                                       id_bits, c->stream));
-    c->launched();
+  int* tmp = c->ensure<int>(B_TMP, std::max<int64_t>(nnz, 1));  // fill scratch, then C3
+  int* nci = c->ensure<int>(B_NCI, std::max<int64_t>(nnz, 1) + 4);  // +4: 16-byte tail reads
+  int* free_vals = nullptr;   // nnz-int arrays the row sort leaves free
+  int* free_keys = nullptr;
+  const bool row_sort = c->force_row_sort != 2 && (c->dmax <= (u64)(4 * G));
+  if (row_sort) {
+    DISPATCH_G(G, launch_fill_sort, c, d_rp, d_ci, perm, inv, nrp, N, nci, split, send);
+  } else {
+    int* row_of = c->ensure<int>(B_ROWOF, std::max<int64_t>(nnz, 1) + 4);
+    int* keys_out = c->ensure<int>(B_KEYSOUT, std::max<int64_t>(nnz, 1));
+    DISPATCH_G(G, launch_fill_rows, c, d_rp, d_ci, perm, inv, nrp, N, tmp, row_of);
+    if (nnz > 0) {  // stable sort by neighbour id: rows come out sorted (see k_fill_rows)
+      cub::DoubleBuffer<int> dk(tmp, keys_out), dv(row_of, nci);
+      tb = c->buf[B_CUB].cap;
+      CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, dk, dv, (int)nnz, 0, id_bits, c->stream));
+      c->launched();
+      if (dv.Current() != nci) std::swap(nci, row_of);  // the sorted rows may land in either
+    }
+    free_vals = row_of;
+    free_keys = keys_out;
   }
   c->perm = perm;
   c->inv = inv;
   c->rp = nrp;
   c->ci = nci;
 
-  // ---- split / mirror / canonical edge list
-  int* split = c->ensure<int>(B_SPLIT, n);
-  int* outdeg = c->ensure<int>(B_OUTDEG, n + 1);
-  int* orp = c->ensure<int>(B_ORP, n + 1);
-  CK(cudaMemsetAsync(outdeg + n, 0, sizeof(int), c->stream));
-  int* send = c->ensure<int>(B_SEND, n);
-  k_split<<<c->grid(n, 256), 256, 0, c->stream>>>(c->rp, c->ci, N, c->d_small + 4, split, send,
-                                                  outdeg, c->d_small + 3);
-  check_launch();
-  c->launched();
-  tb = c->buf[B_CUB].cap;
-  CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, outdeg, orp, N + 1, c->stream));
-  c->launched();
+  // ---- split / mirror
+  if (!row_sort) {
+    k_split<<<c->grid(n, 256), 256, 0, c->stream>>>(c->rp, c->ci, N, c->d_small + 4, split, send,
+                                                    c->d_small + 3);
+    check_launch();
+    c->launched();
+  }
   int* mir = c->ensure<int>(B_MIR, std::max<int64_t>(nnz, 1));
-  int* ce_row = c->ensure<int>(B_CE_ROW, std::max<int64_t>(c->m, 1));
-  int* ce_pos = c->ensure<int>(B_CE_POS, std::max<int64_t>(c->m, 1));
   const bool sort_mirror = nnz >= FGLT_MIRROR_SORT_DEG * n;  // else per-edge binary searches
   if (nnz > 0 && !sort_mirror) {
-    DISPATCH_G(G, launch_mirror, c, split, send, orp, N, mir, ce_row, ce_pos);
+    DISPATCH_G(G, launch_mirror, c, split, send, N, mir);
   } else if (nnz > 0) {
     // mirror positions by a second stable transpose: the sorted CSR read
     // r-major as (key = neighbour y, value = own position j) sorts into
     // y-major order with r ascending, i.e. the value landing at j' (the slot
-    // of (y, r)) is j, the slot of (r, y).
-    k_iota<<<c->grid(nnz, 256), 256, 0, c->stream>>>(row_of, nnz);
+    // of (y, r)) is j, the slot of (r, y). Keys: a copy of the column array
+    // (in the C3 buffer, zeroed later anyway).
+    if (!free_vals) free_vals = c->ensure<int>(B_ROWOF, std::max<int64_t>(nnz, 1) + 4);
+    if (!free_keys) free_keys = c->ensure<int>(B_KEYSOUT, std::max<int64_t>(nnz, 1));
+    k_iota_copy<<<c->grid(nnz, 256), 256, 0, c->stream>>>(free_vals, tmp, c->ci, nnz);
     check_launch();
     c->launched();
+    cub::DoubleBuffer<int> dk(tmp, free_keys), dv(free_vals, mir);
     tb = c->buf[B_CUB].cap;
-    CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, nci, keys_out, row_of, mir, (int)nnz, 0,
-                                       id_bits, c->stream));
+    CK(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, dk, dv, (int)nnz, 0, id_bits, c->stream));
     c->launched();
-    DISPATCH_G(G, launch_canon, c, split, send, orp, N, ce_row, ce_pos);
+    mir = dv.Current();
   }
   c->split = split;
   c->send = send;
-  c->orp = orp;
   c->mir = mir;
-  c->ce_row = ce_row;
-  c->ce_pos = ce_pos;
-  c->C3f = reinterpret_cast<u32*>(tmp);  // B_TMP is dead after the row sort
+  c->C3f = reinterpret_cast<u32*>(tmp);  // B_TMP is dead after the sorts
 }
 
 void read_graph_stats(fglt_ctx* c) {
@@ -579,8 +616,8 @@ void sweep_a(fglt_ctx* c) {
 void local_sweeps(fglt_ctx* c, bool mirror_c3 = false) {
   if (!c->plan.c3 || c->n == 0) return;
   if (mirror_c3 && c->m > 0) {
-    k_c3_mirror<<<c->grid(c->m, 256), 256, 0, c->stream>>>(c->ce_pos, c->mir, c->orp + c->n,
-                                                          c->C3f);
+    k_c3_mirror<<<c->grid((int64_t)c->nact * 8, 256), 256, 0, c->stream>>>(
+        c->split, c->send, c->mir, (int)c->nact, c->C3f);
     check_launch();
     c->launched();
   }
@@ -588,46 +625,65 @@ void local_sweeps(fglt_ctx* c, bool mirror_c3 = false) {
   DISPATCH_G(G, launch_sweep_bc, c);
 }
 
-// Bin roots [u0,u1) by key into up to 3 lists; returns counts (host sync).
-std::vector<int> bin_roots(fglt_ctx* c, const u64* key, int64_t u0, int64_t u1,
-                           const std::vector<u64>& thr, int** lists, int64_t* stride,
-                           Buf which = B_LISTS) {
+// Bin roots [u0,u1) by key into compact lists; returns the counts (host
+// sync). The kernel that wrote the keys tallied the bins into bin_counts(c)
+// (zeroed by bin_counts_reset before it ran).
+int* bin_counts(fglt_ctx* c) { return reinterpret_cast<int*>(c->d_small + 16); }
+
+void bin_counts_reset(fglt_ctx* c) {
+  CK(cudaMemsetAsync(bin_counts(c), 0, 10 * sizeof(int), c->stream));  // slots 16..20
+}
+
+std::vector<int> bin_roots(fglt_ctx* c, const u32* key, int64_t u0, int64_t u1,
+                           const std::vector<u64>& thr, int** lists, Buf which = B_LISTS) {
   const int nb = (int)thr.size() + 1;
   if (nb > 9) throw CudaFail{FGLT_E_CUDA, "internal: at most 9 root bins"};
-  const int64_t span = std::max<int64_t>(u1 - u0, 1);
-  int* lst = c->ensure<int>(which, (size_t)nb * span);
-  u64* d_thr = c->d_small + 8;
-  int* counts = reinterpret_cast<int*>(c->d_small + 16);
-  std::vector<u64> th(thr);
-  th.resize(8, ~0ull);
-  CK(cudaMemcpyAsync(d_thr, th.data(), 8 * sizeof(u64), cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemsetAsync(counts, 0, 10 * sizeof(int), c->stream));  // slots 16..20
-  if (u1 > u0) {
-    k_bin<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(key, (int)u0, (int)u1, d_thr, nb, counts,
-                                                       lst, span);
+  std::vector<int> h(9);
+  CK(cudaMemcpyAsync(h.data(), bin_counts(c), 9 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  h.resize(nb);
+  BinThr T;
+  BinBases B;
+  for (int b = 0; b < 8; ++b) T.thr[b] = b < (int)thr.size() ? thr[b] : ~0ull;
+  T.nbins = nb;
+  int64_t total = 0;
+  for (int b = 0; b < 9; ++b) {
+    B.base[b] = (int)total;
+    if (b < nb) total += h[b];
+  }
+  int* lst = c->ensure<int>(which, (size_t)std::max<int64_t>(total, 1));
+  for (int b = 0; b < nb; ++b) lists[b] = lst + B.base[b];
+  if (total > 0) {
+    int* cursors = reinterpret_cast<int*>(c->d_small + 44);  // slots 44..48
+    CK(cudaMemsetAsync(cursors, 0, 10 * sizeof(int), c->stream));
+    k_bin<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(key, (int)u0, (int)u1, T, B, cursors, lst);
     check_launch();
     c->launched();
   }
-  std::vector<int> h(9);
-  CK(cudaMemcpyAsync(h.data(), counts, 9 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  for (int b = 0; b < nb; ++b) lists[b] = lst + (int64_t)b * span;
-  *stride = span;
-  h.resize(nb);
   return h;
 }
 
 
 __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict__ split, int n,
-                             u64* __restrict__ key, u64 force_key) {
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
-    const int s = send[u] - split[u];
-    u64 k = s >= 2 ? (u64)s : 0ull;
-    // test hook: push roots into a larger bin (a bin's kernel handles any s
-    // below its cap, so forcing upward is always valid)
-    if (k && force_key && force_key > k) k = force_key;
-    key[u] = k;
+                             u32* __restrict__ key, u32 force_key, int u0, int u1, BinThr T,
+                             int* __restrict__ counts) {
+  int tally = 0;
+  const int lane = threadIdx.x & 31;
+  for (int ub = blockIdx.x * blockDim.x + threadIdx.x - lane; ub < n;
+       ub += gridDim.x * blockDim.x) {  // warp-uniform trip count (bin_tally votes)
+    const int u = ub + lane;
+    u32 k = 0;
+    if (u < n) {
+      const int s = send[u] - split[u];
+      k = s >= 2 ? (u32)s : 0u;
+      // test hook: push roots into a larger bin (a bin's kernel handles any s
+      // below its cap, so forcing upward is always valid)
+      if (k && force_key && force_key > k) k = force_key;
+      key[u] = k;
+    }
+    bin_tally(u >= u0 && u < u1 ? bin_of(k, T) : -1, T.nbins, tally);
   }
+  bin_tally_flush(tally, T.nbins, counts);
 }
 
 #ifndef FGLT_SPLIT_BIG
@@ -658,7 +714,8 @@ constexpr u64 kRootThr[] = {(u64)kRootsTiny, (u64)kSmallS, FGLT_BIN1, FGLT_BIN2,
                             (u64)kBlockS};
 constexpr int kFirstBlockBin = 2;
 
-__global__ void k_gather_keys(const int* __restrict__ list, int cnt, const u64* __restrict__ w,
+template <class T>
+__global__ void k_gather_keys(const int* __restrict__ list, int cnt, const T* __restrict__ w,
                               u64* __restrict__ keys) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
     keys[i] = w[list[i]];
@@ -666,12 +723,13 @@ __global__ void k_gather_keys(const int* __restrict__ list, int cnt, const u64* 
 
 // Order a root list by work, largest first (LPT for the dynamic queues).
 // Keys are < 2^bits (radix passes only over the live bits).
-void sort_by_work_desc(fglt_ctx* c, int* list, int cnt, const u64* w, int bits = 64) {
+template <class T>
+void sort_by_work_desc(fglt_ctx* c, int* list, int cnt, const T* w, int bits = 64) {
   if (cnt < 2) return;
   bits = std::max(1, std::min(bits, 64));
   u64* k = c->ensure<u64>(B_SORTK, 2 * (size_t)cnt);
   int* v = c->ensure<int>(B_SORTV, (size_t)cnt);
-  k_gather_keys<<<c->grid(cnt, 256), 256, 0, c->stream>>>(list, cnt, w, k);
+  k_gather_keys<T><<<c->grid(cnt, 256), 256, 0, c->stream>>>(list, cnt, w, k);
   check_launch();
   c->launched();
   size_t tb = 0;
@@ -726,15 +784,19 @@ void build_hubs(fglt_ctx* c) {
 void root_bins(fglt_ctx* c, int64_t u0, int64_t u1) {
   build_hubs(c);
   if (c->rb_u0 == u0 && c->rb_u1 == u1 && !c->rb_cnt.empty()) return;
-  u64* key = c->ensure<u64>(B_RKEY, (size_t)std::max<int64_t>(c->n, 1));
-  static const u64 kForceKey[] = {0, 33, 129, 257, 513, 1025};
-  const u64 fk = (c->force_roots_bin > 0 && c->force_roots_bin < 6) ? kForceKey[c->force_roots_bin] : 0;
-  k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->send, c->split, (int)c->n, key, fk);
+  u32* key = c->ensure<u32>(B_RKEY, (size_t)std::max<int64_t>(c->n, 1));
+  static const u32 kForceKey[] = {0, 33, 129, 257, 513, 1025};
+  const u32 fk = (c->force_roots_bin > 0 && c->force_roots_bin < 6) ? kForceKey[c->force_roots_bin] : 0;
+  const std::vector<u64> thr(std::begin(kRootThr), std::end(kRootThr));
+  BinThr T;
+  for (int b = 0; b < 8; ++b) T.thr[b] = b < (int)thr.size() ? thr[b] : ~0ull;
+  T.nbins = (int)thr.size() + 1;
+  bin_counts_reset(c);
+  k_outdeg_key<<<c->grid(c->n, 256), 256, 0, c->stream>>>(c->send, c->split, (int)c->n, key, fk,
+                                                         (int)u0, (int)u1, T, bin_counts(c));
   check_launch();
   c->launched();
-  int64_t stride = 0;
-  c->rb_cnt = bin_roots(c, key, u0, u1, std::vector<u64>(std::begin(kRootThr), std::end(kRootThr)),
-                        c->rb_lists, &stride, B_RLISTS);
+  c->rb_cnt = bin_roots(c, key, u0, u1, thr, c->rb_lists, B_RLISTS);
   // keys are |N+(u)| <= max out-degree (or a forced bin key <= 1025)
   const int kbits = 64 - __builtin_clzll(std::max<u64>(std::max<u64>(c->maxout, 1025), 1));
   for (int b = kFirstBlockBin; b < (int)c->rb_cnt.size(); ++b)
@@ -921,12 +983,11 @@ void triangles(fglt_ctx* c, int64_t u0, int64_t u1) {
 void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
   const Plan& P = c->plan;
   if (c->n == 0 || !(P.c4 || P.d13)) return;
-  u64* work = c->ensure<u64>(B_WORK, 3 * (size_t)c->n);
+  u64* work = c->ensure<u64>(B_WORK, 2 * (size_t)c->n);  // wc (u64) | class, parts (u32 each)
   u64* wc = work;
-  u64* cls = work + c->n;
-  u64* parts = work + 2 * c->n;
+  u32* cls = reinterpret_cast<u32*>(work + c->n);
+  u32* parts = cls + c->n;
   int* lists[9];
-  int64_t stride = 0;
   if (P.c4) {
     const int G = group_for((double)c->nnz / (double)c->n);
     DISPATCH_G(G, launch_root_work, c, wc);
@@ -947,12 +1008,13 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     c->unit_slots.push_back({"c4 dense", c->d_small + 32});
     c->unit_slots.push_back({"c4 classes", c->d_small + 33});
     c->mark("c4 classes:start");
+    bin_counts_reset(c);
     k_c4_class<<<c->grid(u1 - u0, 256), 256, 0, c->stream>>>(
         c->rp, c->split, wc, (int)u0, (int)u1, bands[0], bands[1], bands[2], cls, parts,
-        c->force_c4_class, c->force_c4_parts, cw);
+        c->force_c4_class, c->force_c4_parts, cw, bin_counts(c));
     check_launch();
     c->launched();
-    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6, 7, 8}, lists, &stride);
+    std::vector<int> cnt = bin_roots(c, cls, u0, u1, {1, 2, 3, 4, 5, 6, 7, 8}, lists);
     // wc(u) <= W = sum of squared degrees
     const int wbits = 64 - __builtin_clzll(std::max<u64>(c->W, 1));
     for (int bb = 3; bb <= 6; ++bb) sort_by_work_desc(c, lists[bb], cnt[bb], wc, wbits);
@@ -1318,7 +1380,7 @@ int fglt_ctx_scratch_report(const fglt_ctx* c, char* out, int len) {
   std::string r;
   for (int b = 0; b < B_COUNT; ++b)
     if (c->buf[b].p && c->buf[b].call == c->call)
-      r += std::string(kBufName[b]) + " " + std::to_string(c->buf[b].cap) +
+      r += std::string(kBufName[b]) + " " + std::to_string(c->buf[b].req) +
            (is_staging(b) ? " staging\n" : "\n");
   std::snprintf(out, (size_t)len, "%s", r.c_str());
   return FGLT_OK;
@@ -1488,6 +1550,7 @@ int fglt_ctx_set_debug(fglt_ctx* c, int key, int value) {
     case FGLT_DEBUG_ROOTS_BIN: c->force_roots_bin = value; return FGLT_OK;
     case FGLT_DEBUG_HUB: c->force_hub = value; c->hub_built = false; return FGLT_OK;
     case FGLT_DEBUG_TRILIST: c->tl_mode = value; return FGLT_OK;
+    case FGLT_DEBUG_ROW_SORT: c->force_row_sort = value; return FGLT_OK;
     default: return FGLT_E_PARSE;
   }
 }

@@ -139,6 +139,36 @@ __device__ __forceinline__ u64 seg_sum_runs(int row, u64 v, bool* tail) {
   return v;
 }
 
+// ---------------------------------------------------------------- root bins
+struct BinThr {
+  u64 thr[8];
+  int nbins;
+};
+struct BinBases {
+  int base[9];
+};
+
+__device__ __forceinline__ int bin_of(u64 x, const BinThr& T) {
+  if (x == 0) return -1;  // key 0 roots are dropped
+  int b = 0;
+  while (b + 1 < T.nbins && x > T.thr[b]) ++b;
+  return b;
+}
+
+// all 32 lanes call it (b = -1: nothing to count)
+__device__ __forceinline__ void bin_tally(int b, int nbins, int& acc) {
+  const int lane = threadIdx.x & 31;
+  for (int q = 0; q < nbins; ++q) {
+    const unsigned m = __ballot_sync(0xffffffffu, b == q);
+    if (lane == q) acc += __popc(m);
+  }
+}
+
+__device__ __forceinline__ void bin_tally_flush(int acc, int nbins, int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  if (lane < nbins && acc) atomicAdd(counts + lane, acc);
+}
+
 // ------------------------------------------------------------ preprocessing
 
 // key = degree << 32 | id : sorting these gives the relabelling order.
@@ -158,8 +188,10 @@ __global__ void k_degree_keys(const int* __restrict__ rp, int n, int* __restrict
   }
 }
 
-__global__ void k_perm(const int* __restrict__ sorted_ids, const int* __restrict__ rp, int n,
-                       int* __restrict__ perm, int* __restrict__ inv, int* __restrict__ ndeg) {
+// sorted_ids may BE perm (the degree sort's id buffers are (split, perm)): no
+// __restrict__ on the two; each thread reads its entry before writing it.
+__global__ void k_perm(const int* sorted_ids, const int* __restrict__ rp, int n, int* perm,
+                       int* __restrict__ inv, int* __restrict__ ndeg) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     const int old = sorted_ids[r];
     perm[r] = old;
@@ -216,12 +248,10 @@ __global__ void k_fill_rows(const int* __restrict__ rp, const int* __restrict__ 
   }
 }
 
-// split[r] = first position of row r holding a neighbour > r; row_of for the
-// canonical (upper) positions is written as a compact edge list.
+// split[r] = first position of row r holding a neighbour > r.
 __global__ void k_split(const int* __restrict__ rp, const int* __restrict__ ci, int n,
                         const unsigned long long* __restrict__ nact_p, int* __restrict__ split,
-                        int* __restrict__ send, int* __restrict__ outdeg,
-                        unsigned long long* __restrict__ maxout) {
+                        int* __restrict__ send, unsigned long long* __restrict__ maxout) {
   // split[r]: first neighbour > r; send[r]: first neighbour >= n_active (the
   // pendant/isolated tail). N+(r) restricted to active vertices is
   // [split[r], send[r]); vertices >= n_active are never enumeration roots.
@@ -232,7 +262,6 @@ __global__ void k_split(const int* __restrict__ rp, const int* __restrict__ ci, 
     const int e = r < nact ? lower_bound_i32(ci, s, rp[r + 1], nact) : s;
     split[r] = s;
     send[r] = e;
-    outdeg[r] = e - s;
     mo = max(mo, (unsigned long long)(e - s));
   }
   // one atomic per warp: every thread hitting the same word serialises
@@ -241,47 +270,114 @@ __global__ void k_split(const int* __restrict__ rp, const int* __restrict__ ci, 
   if ((threadIdx.x & 31) == 0 && mo) atomicMax(maxout, mo);
 }
 
-// Low-degree graphs (binary searches are short): warp per row; for each
+// Low-degree graphs (binary searches are short): G lanes per row; for each
 // canonical position p (row r, v = ci[p] > r) find the mirror position q of
-// r in row v (a prefix entry) and record both; also emit the compact
-// canonical edge list (row, position), index e = orp[r] + offset.
+// r in row v (a prefix entry) and record both.
 template <int G>  // lanes per row (from the mean degree)
 __global__ void k_mirror(const int* __restrict__ rp, const int* __restrict__ ci,
-                         const int* __restrict__ split, const int* __restrict__ send,
-                         const int* __restrict__ orp, int n, int* __restrict__ mir,
-                         int* __restrict__ ce_row, int* __restrict__ ce_pos) {
+                         const int* __restrict__ split, const int* __restrict__ send, int n,
+                         int* __restrict__ mir) {
   // canonical edges between active vertices only: edges to the pendant tail
   // carry no triangles (their C3 stays 0 in both slots)
   const int lane = threadIdx.x & (G - 1);
   const int groups = (gridDim.x * blockDim.x) / G;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) / G; r < n; r += groups) {
-    const int s = split[r], e = send[r], base = orp[r];
+    const int s = split[r], e = send[r];
     for (int p = s + lane; p < e; p += G) {
       const int v = ci[p];
       const int q = lower_bound_i32(ci, rp[v], split[v], r);
       mir[p] = q;
       mir[q] = p;
-      ce_row[base + (p - s)] = r;
-      ce_pos[base + (p - s)] = p;
     }
   }
 }
 
-// Compact canonical edge list of the active-active upper entries: for row r,
-// positions [split[r], send[r]) go to e = orp[r] + offset as (row, position).
-// (The mirror positions come from a second stable transpose sort, prepare().)
-template <int G>  // lanes per row (from the mean degree)
-__global__ void k_canon(const int* __restrict__ split, const int* __restrict__ send,
-                        const int* __restrict__ orp, int n, int* __restrict__ ce_row,
-                        int* __restrict__ ce_pos) {
+// Low-degree graphs (d_max <= G * K): the relabelled row r is built AND sorted
+// by its own G lanes in registers — K elements per lane, each element's rank
+// = the number of row elements below it (ties by position, so a malformed
+// row with repeats still lands in distinct slots) — and written straight to
+// its sorted slot: one read of the input row, one write of the new row, no
+// global sort and no (row, key) scratch arrays. The same lanes count the
+// neighbours below r and below n_active: split[r], send[r] and max |N+(r)|
+// (k_split's outputs).
+template <int G, int K>
+__global__ void __launch_bounds__(256)
+k_fill_sort(const int* __restrict__ rp, const int* __restrict__ ci, const int* __restrict__ perm,
+            const int* __restrict__ inv, const int* __restrict__ nrp, int n,
+            const unsigned long long* __restrict__ nact_p, int* __restrict__ out,
+            int* __restrict__ split, int* __restrict__ send,
+            unsigned long long* __restrict__ maxout) {
+  const int nact = (int)*nact_p;
   const int lane = threadIdx.x & (G - 1);
+  const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
   const int groups = (gridDim.x * blockDim.x) / G;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) / G; r < n; r += groups) {
-    const int s = split[r], e = send[r], base = orp[r];
-    for (int p = s + lane; p < e; p += G) {
-      ce_row[base + (p - s)] = r;
-      ce_pos[base + (p - s)] = p;
+  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int rounds = (n + groups - 1) / groups;
+  unsigned long long mo = 0;
+  for (int it = 0; it < rounds; ++it) {  // warp-uniform trip count (group shuffles)
+    const int r = g0 + it * groups;
+    int d = 0, b = 0, w = 0;
+    if (r < n) {
+      const int o = perm[r];
+      b = rp[o];
+      d = rp[o + 1] - b;
+      w = nrp[r];
     }
+    int x[K], rank[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int i = lane + k * G;
+      x[k] = i < d ? inv[__ldg(ci + b + i)] : 0x7fffffff;
+      rank[k] = 0;
+    }
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      if (kk * G < d) {  // group-uniform
+#pragma unroll
+        for (int l = 0; l < G; ++l) {
+          const int y = __shfl_sync(gmask, x[kk], l, G);
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            rank[k] += (y < x[k]) || (y == x[k] && (kk < k || (kk == k && l < lane)));
+        }
+      }
+    }
+    int below = 0, act = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (lane + k * G < d) {
+        out[w + rank[k]] = x[k];
+        below += x[k] < r;
+        act += x[k] < nact;
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      below += __shfl_xor_sync(gmask, below, o, G);
+      act += __shfl_xor_sync(gmask, act, o, G);
+    }
+    if (r < n && lane == 0) {
+      const int s = w + below;
+      const int e = r < nact ? w + act : s;
+      split[r] = s;
+      send[r] = e;
+      mo = max(mo, (unsigned long long)(e - s));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mo = max(mo, __shfl_xor_sync(0xffffffffu, mo, o));
+  if ((threadIdx.x & 31) == 0 && mo) atomicMax(maxout, mo);
+}
+
+// a[i] = i and k[i] = src[i]: the (key, value) input of the mirror transpose
+// sort (the sort consumes its key buffer, so the graph's column array is
+// copied, not handed over).
+__global__ void k_iota_copy(int* __restrict__ a, int* __restrict__ k, const int* __restrict__ src,
+                            long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    a[i] = (int)i;
+    k[i] = src[i];
   }
 }
 
@@ -382,15 +478,14 @@ struct SweepA {
 // The triangle pass (per-edge C3, and 4-cliques) is root-centric: see
 // k_roots_warp / k_roots_block<kC3=true> in fglt_roots.cuh.
 
-// Copy canonical C3 values into their mirror slots so rows read contiguously.
-__global__ void k_c3_mirror(const int* __restrict__ ce_pos, const int* __restrict__ mir,
-                            const int* __restrict__ m_active, u32* __restrict__ C3f) {
-  // m_active = orp[n]: the canonical list holds active-active edges only
-  const int m = *m_active;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < m; e += gridDim.x * blockDim.x) {
-    const int p = ce_pos[e];
-    C3f[mir[p]] = C3f[p];
-  }
+// Copy canonical C3 values into their mirror slots so rows read contiguously
+// (per-kernel API only): row r's canonical slots are [split[r], send[r]).
+__global__ void k_c3_mirror(const int* __restrict__ split, const int* __restrict__ send,
+                            const int* __restrict__ mir, int nact, u32* __restrict__ C3f) {
+  const int lane = threadIdx.x & 7;
+  const int groups = (gridDim.x * blockDim.x) >> 3;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 3; r < nact; r += groups)
+    for (int p = split[r] + lane; p < send[r]; p += 8) C3f[mir[p]] = C3f[p];
 }
 
 // c3 = sum C3 / 2; d14 = sum C(C3,2); d10 = sum C3 * (d_j - 2)+;

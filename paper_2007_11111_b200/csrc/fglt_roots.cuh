@@ -410,14 +410,20 @@ __host__ __device__ inline void dense_span(u64 u, u64 b4, u64 b8, u64 b16, u64 t
 
 __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ split,
                            const u64* __restrict__ wc, int u0, int u1, int b4, int b8, int b16,
-                           u64* __restrict__ cls, u64* __restrict__ parts, int force_cls,
-                           int force_parts, unsigned long long* __restrict__ class_wedges) {
+                           u32* __restrict__ cls, u32* __restrict__ parts, int force_cls,
+                           int force_parts, unsigned long long* __restrict__ class_wedges,
+                           int* __restrict__ bin_counts) {
   // class_wedges[0] += wedges of the dense-tile roots (classes 5/6/7),
-  // class_wedges[1] += all wedges (the 4-cycle phases' work units)
+  // class_wedges[1] += all wedges (the 4-cycle phases' work units);
+  // bin_counts[c - 1] += roots of class c (k_bin's list sizes)
   unsigned long long dense_w = 0, all_w = 0;
-  for (int u = u0 + blockIdx.x * blockDim.x + threadIdx.x; u < u1;
-       u += gridDim.x * blockDim.x) {
-    const u64 w = wc[u];
+  int tally = 0;
+  const int lane_ = threadIdx.x & 31;
+  for (int ub = u0 + blockIdx.x * blockDim.x + threadIdx.x - lane_; ub < u1;
+       ub += gridDim.x * blockDim.x) {
+    const int u = ub + lane_;
+    const bool valid = u < u1;  // warp-uniform trip count: idle lanes still vote below
+    const u64 w = valid ? wc[u] : 0;
     u64 c = 0, P = 1;
     if (w == 0) {
       c = 0;
@@ -464,11 +470,15 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
         if (force_parts > 0) P = (u64)force_parts;
       }
     }
-    cls[u] = c;
-    parts[u] = P;
+    if (valid) {
+      cls[u] = (u32)c;
+      parts[u] = (u32)P;  // P <= wc / 12288 + 1 < 2^32 (wc < 2^45: nnz < 2^31 rows of < 2^31)
+    }
     all_w += w;
     if (c >= 5 && c <= 7) dense_w += w;
+    bin_tally((int)c - 1, 9, tally);
   }
+  bin_tally_flush(tally, 9, bin_counts);
   dense_w = warp_sum_u64(dense_w);
   all_w = warp_sum_u64(all_w);
   if ((threadIdx.x & 31) == 0) {
@@ -492,7 +502,7 @@ __global__ void
 k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, const u64* __restrict__ wcv,
-           const u64* __restrict__ parts, int max_log, int* __restrict__ next_root,
+           const u32* __restrict__ parts, int max_log, int* __restrict__ next_root,
            u64* __restrict__ c4) {
   // roots are sorted by work (largest first) and handed out dynamically
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -509,7 +519,7 @@ k_c4_hashp(const int* __restrict__ rp, const int* __restrict__ ci,
     const int k = s_root;
     if (k >= nroots) break;
     const int u = roots[k];
-    const u32 P = (u32)parts[u];
+    const u32 P = parts[u];
     const u64 per_pass = (wcv[u] + P - 1) / P;
     int hlog = 6;
     while (hlog < max_log && ((u64)1 << hlog) < 2 * per_pass) ++hlog;
@@ -669,7 +679,7 @@ __global__ void __launch_bounds__(NT)
 k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
            const int* __restrict__ split, const int* __restrict__ mir,
            const int* __restrict__ roots, int nroots, const u64* __restrict__ wcv,
-           const u64* __restrict__ parts, int max_log, int* __restrict__ next_root,
+           const u32* __restrict__ parts, int max_log, int* __restrict__ next_root,
            u64* __restrict__ c4) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -691,7 +701,7 @@ k_c4_block(const int* __restrict__ rp, const int* __restrict__ ci,
     const int k = s_root;
     if (k >= nroots) break;
     const int u = roots[k];
-    const u32 P = (u32)parts[u];
+    const u32 P = parts[u];
     const u64 per_pass = (wcv[u] + P - 1) / P;
     int hlog = 6;
     while (hlog < max_log && ((u64)1 << hlog) < 2 * per_pass) ++hlog;
@@ -2826,33 +2836,28 @@ __global__ void k_graph_stats(const int* __restrict__ rp, int n, u64* __restrict
   }
 }
 
-// Bin roots into work lists: lists[b] gets the roots whose key falls in bin b
-// (key <= thresholds[b]); key 0 roots are dropped.
-__global__ void k_bin(const u64* __restrict__ key, int u0, int u1, const u64* __restrict__ thr,
-                      int nbins, int* __restrict__ counts, int* __restrict__ lists,
-                      long long list_stride) {
+// Bin roots into compact work lists. The kernel that computes the keys also
+// tallies the bins (bin_tally: lane q of a warp accumulates bin q, one atomic
+// per warp and bin at the end), so the lists are sized exactly: one array of
+// (#binned roots) ints per binning instead of one n-int list per bin.
+// lists[base[b] ..] gets the roots of bin b (order within a bin is arbitrary)
+__global__ void k_bin(const u32* __restrict__ key, int u0, int u1, BinThr T, BinBases B,
+                      int* __restrict__ cursors, int* __restrict__ list) {
   // warp-aggregated: one atomic per (warp, bin) instead of one per root
   const int lane = threadIdx.x & 31;
   const int span = u1 - u0;
   const int stride = gridDim.x * blockDim.x;
   for (int i0 = (blockIdx.x * blockDim.x + threadIdx.x) - lane; i0 < span; i0 += stride) {
     const int i = i0 + lane;
-    int b = -1;
-    if (i < span) {
-      const u64 x = key[u0 + i];
-      if (x != 0) {
-        b = 0;
-        while (b + 1 < nbins && x > thr[b]) ++b;
-      }
-    }
+    const int b = i < span ? bin_of(key[u0 + i], T) : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, b);
     if (b >= 0) {
       const int leader = __ffs(peers) - 1;
       int base = 0;
-      if (lane == leader) base = atomicAdd(counts + b, __popc(peers));
+      if (lane == leader) base = atomicAdd(cursors + b, __popc(peers));
       base = __shfl_sync(peers, base, leader);
       const int rank = __popc(peers & ((1u << lane) - 1));
-      lists[(long long)b * list_stride + base + rank] = u0 + i;
+      list[B.base[b] + base + rank] = u0 + i;
     }
   }
 }

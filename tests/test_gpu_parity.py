@@ -264,6 +264,26 @@ def test_forced_code_paths(label, key, value, parts):
     c.close()
 
 
+def test_relabel_paths_agree():
+    """Low-degree graphs build their relabelled rows with the in-register row
+    sort (k_fill_sort: every lanes-per-row / elements-per-lane shape below);
+    forcing the global transpose sort must give the same bits."""
+    cases = [gu.regular(400, 4, 11), gu.er(2000, 0.004, 1), gu.er(500, 0.02, 3),
+             gu.er(300, 0.06, 5), graphs.sbm(64, 64, 0.3, 3.0, 9), gu.er(200, 0.3, 2),
+             gu.star(70), gu.complete(40), gu.demo()]
+    c = _capi.Context(0)
+    f = _capi.Context(0)
+    f.set_debug(_capi.DEBUG_ROW_SORT, 2)
+    for rp, ci in cases:
+        check_same(c, rp, ci, d15_mode=1)
+        a = c.transform_host(rp, ci)
+        b = f.transform_host(rp, ci)
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+    c.close()
+    f.close()
+
+
 @pytest.mark.parametrize("hub", [1, 2])
 @pytest.mark.parametrize("rbin", [0, 1, 3, 5])
 def test_hub_rows_paths(hub, rbin):
