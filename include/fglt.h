@@ -236,6 +236,7 @@ int fglt_ctx_scratch_report(const fglt_ctx* ctx, char* out, int len);
 #define FGLT_DEBUG_HUB 4       /* 0 auto, 1 no hub rows, 2 hub rows for every hub member */
 #define FGLT_DEBUG_TRILIST 5   /* 0 auto, 1 no triangle list, 2 tiny list pool (fallbacks) */
 #define FGLT_DEBUG_ROW_SORT 6  /* 0 auto (in-register row sort when d_max is small), 2 always the global transpose sort */
+#define FGLT_DEBUG_FLAT_DMAX 7 /* d_max up to which active vertices keep the caller's order (0: always degree order; <= 255) */
 int fglt_ctx_set_debug(fglt_ctx* ctx, int key, int value);
 
 /* Measured random-address shared-memory atomicAdd rate (ops/s) of this

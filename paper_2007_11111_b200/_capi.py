@@ -31,6 +31,7 @@ EXPORTS = [
 ]
 
 DEBUG_C4_CLASS, DEBUG_C4_PARTS, DEBUG_ROOTS_BIN, DEBUG_HUB, DEBUG_TRILIST, DEBUG_ROW_SORT = 1, 2, 3, 4, 5, 6
+DEBUG_FLAT_DMAX = 7
 
 
 class FgltError(ctypes.Structure):

@@ -38,6 +38,10 @@ namespace {
 #ifndef FGLT_TL_MEM_FRAC
 #define FGLT_TL_MEM_FRAC 0.70  // triangle-list pool: at most this share of the free HBM
 #endif
+#ifndef FGLT_FLAT_DMAX
+#define FGLT_FLAT_DMAX 0  // graphs with d_max up to this are not relabelled by degree (<= 255); 0 = off:
+                          // measured on the SBM (64: DRAM 41 -> 28 GB/step but the 4-cycle classes get uneven roots, 24.4 -> 25.0 ms)
+#endif
 #ifndef FGLT_TINY_DMAX
 #define FGLT_TINY_DMAX 64  // graphs with d_max up to this run tiny roots thread-per-root
 #endif
@@ -233,6 +237,10 @@ struct fglt_ctx {
   // test hooks (fglt_ctx_set_debug): force one code path for every root
   int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1, force_hub = 0;
   int force_row_sort = 0;  // 2: never take the in-register row sort (k_fill_sort)
+  // graphs with d_max up to this keep the caller's vertex order among active
+  // vertices (k_degree_keys); at most 255 (the dense 4-cycle bands below)
+  int flat_dmax = FGLT_FLAT_DMAX;
+  bool flat_order() const { return dmax <= (u64)flat_dmax; }
   // triangle list (k_roots_block -> k_diamond_list); tl_mode: 0 auto, 1 off,
   // 2 a tiny pool (test hook: most roots fall back to the probing pass)
   int tl_mode = 0;
@@ -499,7 +507,8 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   int* send = c->ensure<int>(B_SEND, n);
   int key_bits = 1;
   while (key_bits < 31 && ((int64_t)1 << key_bits) <= n + 1) ++key_bits;
-  k_degree_keys<<<c->grid(n, 256), 256, 0, c->stream>>>(d_rp, N, nrp, split);
+  k_degree_keys<<<c->grid(n, 256), 256, 0, c->stream>>>(d_rp, N, nrp, split, c->d_small + 1,
+                                                        (u64)c->flat_dmax);
   check_launch();
   c->launched();
   int id_bits = 1;
@@ -995,6 +1004,9 @@ void roots(fglt_ctx* c, int64_t u0, int64_t u1) {
     int bands[3] = {0, 0, 0};
     if (c->nact > 0 && c->dmax <= 15) {  // every active id in the 4-bit band: no readback
       bands[0] = bands[1] = bands[2] = (int)c->nact;
+    } else if (c->nact > 0 && c->flat_order()) {  // ids not in degree order: one 8-bit band
+      bands[0] = 0;
+      bands[1] = bands[2] = (int)c->nact;
     } else if (c->nact > 0) {
       int* d_b = reinterpret_cast<int*>(c->d_small + 41);
       k_degree_bands<<<1, 32, 0, c->stream>>>(c->rp, (int)c->nact, d_b);
@@ -1551,6 +1563,7 @@ int fglt_ctx_set_debug(fglt_ctx* c, int key, int value) {
     case FGLT_DEBUG_HUB: c->force_hub = value; c->hub_built = false; return FGLT_OK;
     case FGLT_DEBUG_TRILIST: c->tl_mode = value; return FGLT_OK;
     case FGLT_DEBUG_ROW_SORT: c->force_row_sort = value; return FGLT_OK;
+    case FGLT_DEBUG_FLAT_DMAX: c->flat_dmax = value < 0 ? 0 : value > 255 ? 255 : value; return FGLT_OK;
     default: return FGLT_E_PARSE;
   }
 }

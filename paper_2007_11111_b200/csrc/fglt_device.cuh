@@ -179,11 +179,19 @@ __device__ __forceinline__ void bin_tally_flush(int acc, int nbins, int* __restr
 // (degree 0 before 1), ties by id. As a STABLE sort of the ids by one int key
 // (CUB radix sort is stable): key = d for d >= 2, n + d below (d <= n - 1,
 // so every leaf key is above every active one).
+// Low-skew graphs (d_max <= flat_dmax, read from the device-side graph stats:
+// no host round trip): every active vertex gets the same key, so the active
+// ids keep the caller's order (and whatever locality it has: the SBM's
+// communities are contiguous) and only the leaves move to the end. With
+// degrees this small the orientation by id costs about the same enumeration
+// work as the orientation by degree.
 __global__ void k_degree_keys(const int* __restrict__ rp, int n, int* __restrict__ keys,
-                              int* __restrict__ ids) {
+                              int* __restrict__ ids, const u64* __restrict__ stats,
+                              u64 flat_dmax) {
+  const bool flat = stats[1] <= flat_dmax;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int d = rp[i + 1] - rp[i];
-    keys[i] = d >= 2 ? d : n + d;
+    keys[i] = d >= 2 ? (flat ? 2 : d) : n + d;
     ids[i] = i;
   }
 }

@@ -384,6 +384,9 @@ constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many w
 #ifndef FGLT_BATCH_G
 #define FGLT_BATCH_G 2  // lanes per row in lane-row batches (1, 2, 4, 8)
 #endif
+#ifndef FGLT_BATCH_MASKED
+#define FGLT_BATCH_MASKED 0  // lane-row batches over aligned quads with masked ends: every load of a round issued up front
+#endif
 constexpr int kBatchG = FGLT_BATCH_LANE_ROW ? FGLT_BATCH_G : 1;
 constexpr int kBatchRows = 32 / kBatchG;
 constexpr int kQuadsInFlight = FGLT_QUADS;          // 16-byte loads in flight per lane (dense batches)
@@ -886,7 +889,7 @@ __global__ void k_degree_bands(const int* __restrict__ rp, int nact, int* __rest
 // by the last block. Phases: 0 zero, 1 count work, 2 count barrier, 3 sweep,
 // 4 attribution work, 5 attribution barrier, 6 root setup.
 #ifdef FGLT_DENSE_PROF
-__device__ unsigned long long g_dense_prof[8];
+__device__ unsigned long long g_dense_prof[16];
 __device__ unsigned int g_dense_done;
 #define DPROF_MARK(k)                                                       \
   do {                                                                      \
@@ -1027,6 +1030,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         if (lane == 0) segend[q] = se;
         warp_for_each(ci, st, se, [&](int w) { inc(w - lo); });
       }
+      DPROF_MARK(7);
       for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
         if (split_kt) {  // segment from the tile boundaries
@@ -1042,6 +1046,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
           inc(w - lo);
         }
       }
+      DPROF_MARK(8);
       while (true) {
         int bt = 0;
         if (lane == 0) bt = atomicAdd(next_batch, 1);
@@ -1072,6 +1077,34 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         // lane per row: the batch's rows are consecutive in N-(u), so their
         // degrees (and tile segments) are similar; each lane streams its own
         // segment with 16-byte loads, no flattening bookkeeping per quad
+#if FGLT_BATCH_MASKED
+        if (se > st) {
+          // aligned quads [st >> 2, (se + 3) >> 2) at stride kBatchG; elements
+          // outside [st, se) masked; a round's loads are all issued before use
+          const int sub = lane & (kBatchG - 1);
+          const int4* q4 = reinterpret_cast<const int4*>(ci);
+          const int qe = (se + 3) >> 2;
+          const u32 len = (u32)(se - st);
+          for (int k = (st >> 2) + sub; k < qe; k += kBatchG * kQuadsInFlight) {
+            int4 x[kQuadsInFlight];
+#pragma unroll
+            for (int j = 0; j < kQuadsInFlight; ++j)
+              if (k + j * kBatchG < qe) x[j] = __ldg(q4 + k + j * kBatchG);
+#pragma unroll
+            for (int j = 0; j < kQuadsInFlight; ++j) {
+              const int kj = k + j * kBatchG;
+              if (kj < qe) {
+                const int d = (kj << 2) - st;  // segment position of the quad's first element
+                if ((u32)d < len) inc(x[j].x - lo);
+                if ((u32)(d + 1) < len) inc(x[j].y - lo);
+                if ((u32)(d + 2) < len) inc(x[j].z - lo);
+                if ((u32)(d + 3) < len) inc(x[j].w - lo);
+              }
+            }
+          }
+        }
+        continue;
+#endif
         if (se > st) {
           const int sub = lane & (kBatchG - 1);
           const int a0 = min(se, (st + 3) & ~3), a1 = max(a0, se & ~3);
@@ -1189,6 +1222,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
           cur[q] = se;
         }
       }
+      DPROF_MARK(9);
       for (int q = threadIdx.x; q < qs; q += blockDim.x) {
         const int end = mir[b + q];
         u64 sv = 0;
@@ -1208,6 +1242,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
         }
         if (sv) atomicAdd(c4 + ci[b + q], sv);
       }
+      DPROF_MARK(10);
       while (true) {
         int bt = 0;
         if (lane == 0) bt = atomicAdd(next_batch + 1, 1);
@@ -1223,6 +1258,31 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
           const int sub = lane & (kBatchG - 1);
           u64 sv = 0;
           typename std::conditional<PACK, u32, u64>::type ps = 0;
+#if FGLT_BATCH_MASKED
+          if (se > st) {
+            const int4* q4 = reinterpret_cast<const int4*>(ci);
+            const int qe = (se + 3) >> 2;
+            const u32 len = (u32)(se - st);
+            for (int k = (st >> 2) + sub; k < qe; k += kBatchG * kQuadsInFlight) {
+              int4 x[kQuadsInFlight];
+#pragma unroll
+              for (int j = 0; j < kQuadsInFlight; ++j)
+                if (k + j * kBatchG < qe) x[j] = __ldg(q4 + k + j * kBatchG);
+#pragma unroll
+              for (int j = 0; j < kQuadsInFlight; ++j) {
+                const int kj = k + j * kBatchG;
+                if (kj < qe) {
+                  const int d = (kj << 2) - st;
+                  if ((u32)d < len) ps += get(x[j].x - lo) - 1;
+                  if ((u32)(d + 1) < len) ps += get(x[j].y - lo) - 1;
+                  if ((u32)(d + 2) < len) ps += get(x[j].z - lo) - 1;
+                  if ((u32)(d + 3) < len) ps += get(x[j].w - lo) - 1;
+                }
+              }
+              if (PACK) { sv += ps; ps = 0; }
+            }
+          }
+#else
           if (se > st) {
             const int a0 = min(se, (st + 3) & ~3), a1 = max(a0, se & ~3);
             for (int p = st + sub; p < a0; p += kBatchG) ps += get(__ldg(ci + p) - lo) - 1;
@@ -1240,6 +1300,7 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
             }
             for (int pt = a1 + sub; pt < se; pt += kBatchG) ps += get(__ldg(ci + pt) - lo) - 1;
           }
+#endif
           sv += ps;
 #pragma unroll
           for (int o = kBatchG / 2; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
@@ -1318,12 +1379,13 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
   __syncthreads();
   if (threadIdx.x == 0 && atomicAdd(&g_dense_done, 1u) == gridDim.x - 1) {
     unsigned long long t = 0;
-    for (int k = 0; k < 7; ++k) t += g_dense_prof[k];
-    printf("dense phases (warp-cycles %%): zero %.1f count %.1f cbar %.1f sweep %.1f attr %.1f abar %.1f setup %.1f\n",
-           100.0 * g_dense_prof[0] / t, 100.0 * g_dense_prof[1] / t, 100.0 * g_dense_prof[2] / t,
-           100.0 * g_dense_prof[3] / t, 100.0 * g_dense_prof[4] / t, 100.0 * g_dense_prof[5] / t,
-           100.0 * g_dense_prof[6] / t);
-    for (int k = 0; k < 8; ++k) g_dense_prof[k] = 0;
+    for (int k = 0; k < 11; ++k) t += g_dense_prof[k];
+    printf("dense phases (warp-cycles %%): zero %.1f | count: giant %.1f short %.1f batch %.1f bar %.1f | sweep %.1f | attr: giant %.1f short %.1f batch %.1f bar %.1f | setup %.1f\n",
+           100.0 * g_dense_prof[0] / t, 100.0 * g_dense_prof[7] / t, 100.0 * g_dense_prof[8] / t,
+           100.0 * g_dense_prof[1] / t, 100.0 * g_dense_prof[2] / t, 100.0 * g_dense_prof[3] / t,
+           100.0 * g_dense_prof[9] / t, 100.0 * g_dense_prof[10] / t, 100.0 * g_dense_prof[4] / t,
+           100.0 * g_dense_prof[5] / t, 100.0 * g_dense_prof[6] / t);
+    for (int k = 0; k < 16; ++k) g_dense_prof[k] = 0;
     g_dense_done = 0;
   }
 #endif

@@ -284,6 +284,24 @@ def test_relabel_paths_agree():
     f.close()
 
 
+@pytest.mark.parametrize("flat", [0, 64, 255])
+@pytest.mark.parametrize("c4class", [0, 2, 3, 4, 5])
+def test_vertex_order_paths_agree(flat, c4class):
+    """Graphs with d_max <= the flat threshold keep the caller's vertex order
+    among active vertices (k_degree_keys; dense 4-cycle counters then use one
+    8-bit band); threshold 0 always relabels by degree. Same bits either way,
+    under every forced 4-cycle class."""
+    c = _capi.Context(0)
+    c.set_debug(_capi.DEBUG_FLAT_DMAX, flat)
+    c.set_debug(_capi.DEBUG_C4_CLASS, c4class)
+    cases = [gu.regular(400, 4, 11), gu.er(2000, 0.004, 1), gu.er(300, 0.06, 5),
+             graphs.sbm(64, 64, 0.3, 3.0, 9), gu.er(200, 0.3, 2), gu.star(70),
+             gu.complete(40), gu.complete(17), graphs.rmat(11, 8, seed=3), gu.demo()]
+    for rp, ci in cases:
+        check_same(c, rp, ci, d15_mode=1)
+    c.close()
+
+
 @pytest.mark.parametrize("hub", [1, 2])
 @pytest.mark.parametrize("rbin", [0, 1, 3, 5])
 def test_hub_rows_paths(hub, rbin):

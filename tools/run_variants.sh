@@ -12,5 +12,6 @@ sh=[l for l in L if l.startswith('sha')]
 try:
   st=json.loads(L[-1]); ph={k:round(v*1e3,2) for k,v in st['kernel_times'] if v}
 except Exception as e: ph=L[-3:]
-print('$v', it[-1] if it else 'FAIL', sh, ph)"
+print('$v', it[-1] if it else 'FAIL', sh, ph)
+for l in [l for l in L if l.startswith('dense phases')][-4:]: print('   ', l)"
 done
