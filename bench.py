@@ -133,6 +133,16 @@ def ncu_summary(cfg: int):
         return json.load(f)
 
 
+def onchip_summary(cfg: int):
+    """The committed on-chip digest of the dominant kernel's `ncu --set full`
+    capture (tools/make_onchip_summary.py), if any."""
+    p = os.path.join(ROOT, "profiles", f"ncu_config{cfg}_dense_onchip.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
 def compulsory_bytes(n: int, nnz: int) -> int:
     """Algorithm-specific lower bound on HBM bytes of one transform step
     (DESIGN.md §6): read the int32 CSR (4n + 4nnz), write + read the
@@ -487,6 +497,17 @@ def main():
                 "peak_kind": "measured live (fglt_probe_smem_atomics: 96 KB tiles, 2 x 512 "
                              "threads per SM)",
                 "frac": ach / rate if rate else None}
+        oc = onchip_summary(args.config) if dom_name == "c4 dense" else None
+        if oc:
+            # the binding on-chip unit of the same build's --set full capture
+            # (profiles/): % of peak sustained over the launch, per unit
+            dominant.setdefault("onchip", {})["ncu"] = {
+                "bound": oc["bound"], "frac": oc["frac"], "pct_of_peak": oc["pct_of_peak"],
+                "capture_ms": oc["duration_ms"], "l2_hit_rate_pct": oc["l2_hit_rate_pct"],
+                "shared_bank_conflict_share": (oc["shared_bank_conflict_wavefronts"] /
+                                               oc["shared_wavefronts"])
+                if oc.get("shared_wavefronts") else None,
+                "source": oc["source"]}
         if summ:
             for kk in summ.get("kernels", []):
                 if kk["name"].startswith("void fglt::k_c4_dense") and dom_name == "c4 dense":

@@ -166,9 +166,13 @@ int fglt_csr_fetch(fglt_ctx* ctx, int32_t* row_ptr, int32_t* col_idx, uint32_t f
  *   fglt_stage_bounds       root ranges balanced by exact work
  *   fglt_stage_triangles    partial per-edge triangle counts for own roots
  *   -- all-reduce(sum) of the uint32 edge-count buffer --
- *   fglt_stage_local        vertex sweeps over the full graph (replicated)
+ *   fglt_stage_local_part   phase 0: sweep B on my rows (r = rank mod world)
+ *   -- all-reduce(sum) of the uint64 c3 vector (n) --
+ *   fglt_stage_local_part   phase 1: sweep C on my rows
  *   fglt_stage_roots        partial c4/d13/d15 for own roots
- *   -- all-reduce(sum) of the uint64 3n vector buffer --
+ *   -- all-reduce(sum) of the uint64 vector buffer (7n: d14 d10 p3 d9 c4 d13 d15) --
+ *   (fglt_stage_local = both sweeps over every row, replicated; fglt_stage_roots
+ *    then hands out the 3n c4/d13/d15 block)
  *   fglt_stage_epilogue     raw/net rows [r0, r1) in original-id order
  * Buffers handed to the caller are device pointers owned by the context. */
 int fglt_stage_prepare(fglt_ctx* ctx, const int32_t* d_row_ptr,
@@ -180,6 +184,10 @@ int fglt_stage_triangles(fglt_ctx* ctx, int64_t u0, int64_t u1,
                          uint32_t** d_edge_counts, int64_t* count,
                          fglt_error* err);
 int fglt_stage_local(fglt_ctx* ctx, fglt_error* err);
+/* rows r = part (mod nparts); phase 0 returns the c3 vector to sum (count = n,
+ * or 0 when nparts == 1 / no triangle columns), phase 1 returns count 0 */
+int fglt_stage_local_part(fglt_ctx* ctx, int part, int nparts, int phase,
+                          uint64_t** d_c3, int64_t* count, fglt_error* err);
 int fglt_stage_roots(fglt_ctx* ctx, int64_t u0, int64_t u1,
                      uint64_t** d_vectors, int64_t* count, fglt_error* err);
 /* Rows are ORIGINAL vertex ids [v0, v1); outputs are device pointers of

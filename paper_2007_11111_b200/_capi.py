@@ -23,7 +23,7 @@ CODES = {0: "ok", 1: "parse", 2: "structural", 3: "overflow", 4: "inconsistency"
 EXPORTS = [
     "fglt_ctx_create", "fglt_ctx_destroy", "fglt_ctx_release_workspace", "fglt_ctx_transform", "fglt_transform_csr32",
     "fglt_net_from_raw", "fglt_net_from_raw_matrix", "fglt_stage_prepare", "fglt_stage_bounds", "fglt_stage_triangles",
-    "fglt_stage_local", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
+    "fglt_stage_local", "fglt_stage_local_part", "fglt_stage_roots", "fglt_stage_epilogue", "fglt_version",
     "fglt_device_count", "fglt_ctx_kernel_launches", "fglt_ctx_set_debug", "fglt_build_csr",
     "fglt_csr_fetch", "fglt_kernel_p2", "fglt_kernel_c3", "fglt_kernel_p3", "fglt_kernel_d7",
     "fglt_kernel_d8", "fglt_kernel_d9_d10_d11", "fglt_kernel_d13", "fglt_probe_smem_atomics",
@@ -114,6 +114,11 @@ def lib():
                                            ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(FgltError)]
         L.fglt_stage_local.restype = ctypes.c_int
         L.fglt_stage_local.argtypes = [vp, ctypes.POINTER(FgltError)]
+        L.fglt_stage_local_part.restype = ctypes.c_int
+        L.fglt_stage_local_part.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.POINTER(ctypes.c_void_p),
+                                            ctypes.POINTER(ctypes.c_int64),
+                                            ctypes.POINTER(FgltError)]
         L.fglt_stage_roots.restype = ctypes.c_int
         L.fglt_stage_roots.argtypes = [vp, ctypes.c_int64, ctypes.c_int64,
                                        ctypes.POINTER(ctypes.c_void_p),
@@ -361,6 +366,18 @@ class Context:
         rc = self._L.fglt_stage_local(self._h, ctypes.byref(err))
         if rc:
             _raise(rc, err)
+
+    def stage_local_part(self, part: int, nparts: int, phase: int):
+        """Row-partitioned vertex sweeps; phase 0 returns (device pointer, n)
+        of the c3 vector to sum over ranks (count 0: nothing to sum)."""
+        err = FgltError()
+        p = ctypes.c_void_p()
+        cnt = ctypes.c_int64()
+        rc = self._L.fglt_stage_local_part(self._h, part, nparts, phase, ctypes.byref(p),
+                                           ctypes.byref(cnt), ctypes.byref(err))
+        if rc:
+            _raise(rc, err)
+        return p.value or 0, cnt.value
 
     def stage_roots(self, u0: int, u1: int):
         p, cnt, err = ctypes.c_void_p(), ctypes.c_int64(), FgltError()

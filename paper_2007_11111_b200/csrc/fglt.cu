@@ -236,6 +236,10 @@ struct fglt_ctx {
 
   // test hooks (fglt_ctx_set_debug): force one code path for every root
   int force_c4_class = 0, force_c4_parts = 0, force_roots_bin = -1, force_hub = 0;
+  // vertex sweeps B/C of a multi-GPU rank: rows r = rows_part (mod rows_parts)
+  // only (fglt_stage_local_part); 0 / 1 = every row
+  int rows_part = 0, rows_parts = 1;
+  bool local_partial = false;  // this call's sweeps B/C were row-partitioned
   int force_row_sort = 0;  // 2: never take the in-register row sort (k_fill_sort)
   // graphs with d_max up to this keep the caller's vertex order among active
   // vertices (k_degree_keys); at most 255 (the dense 4-cycle bands below)
@@ -348,11 +352,13 @@ void list_big_rows(fglt_ctx* c) {
 template <int G, class F>
 void run_rows(fglt_ctx* c, const F& f) {
   list_big_rows(c);
-  k_rows_group<G, F><<<c->grid(c->n * G, 256), 256, 0, c->stream>>>(f, c->rp, (int)c->n);
+  const int r0 = c->rows_part, rs = std::max(c->rows_parts, 1);
+  k_rows_group<G, F><<<c->grid((c->n + rs - 1) / rs * G, 256), 256, 0, c->stream>>>(
+      f, c->rp, (int)c->n, r0, rs);
   check_launch();
   c->launched();
   k_rows_block<F><<<c->sms * 4, kSweepBlock, 0, c->stream>>>(
-      f, c->rp, c->big_rows, reinterpret_cast<const int*>(c->d_small + 5));
+      f, c->rp, c->big_rows, reinterpret_cast<const int*>(c->d_small + 5), r0, rs);
   check_launch();
   c->launched();
 }
@@ -370,14 +376,17 @@ void launch_sweep_a(fglt_ctx* c) {
   run_rows<G>(c, f);
 }
 
+// phases: 1 = sweep B, 2 = sweep C (needs every row's c3), 3 = both
 template <int G>
-void launch_sweep_bc(fglt_ctx* c) {
-  SweepB fb{c->rp, c->ci, c->C3f, c->mir, (int)c->nact, c->plan.p3 ? c->V(V_P2) : nullptr,
-            c->V(V_C3),
-            c->plan.d14 ? c->V(V_D14) : nullptr, c->plan.d10 ? c->V(V_D10) : nullptr,
-            c->plan.p3 ? c->V(V_P3) : nullptr};
-  run_rows<G>(c, fb);
-  if (c->plan.d9) {
+void launch_sweep_bc(fglt_ctx* c, int phases) {
+  if (phases & 1) {
+    SweepB fb{c->rp, c->ci, c->C3f, c->mir, (int)c->nact, c->plan.p3 ? c->V(V_P2) : nullptr,
+              c->V(V_C3),
+              c->plan.d14 ? c->V(V_D14) : nullptr, c->plan.d10 ? c->V(V_D10) : nullptr,
+              c->plan.p3 ? c->V(V_P3) : nullptr};
+    run_rows<G>(c, fb);
+  }
+  if ((phases & 2) && c->plan.d9) {
     SweepC fc{c->ci, c->V(V_C3), c->V(V_D9)};
     run_rows<G>(c, fc);
   }
@@ -478,6 +487,9 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   c->vec = c->ensure<u64>(B_VEC, (size_t)V_COUNT * std::max<int64_t>(n, 1));
   CK(cudaMemsetAsync(c->vec, 0, (size_t)V_COUNT * std::max<int64_t>(n, 1) * 8, c->stream));
   c->perm = c->inv = nullptr;
+  c->rows_part = 0;
+  c->rows_parts = 1;
+  c->local_partial = false;
   c->rb_u0 = c->rb_u1 = -1;  // graph changed: root bins are stale
   c->hub_built = false;
   c->big_rows_listed = false;
@@ -622,7 +634,7 @@ void sweep_a(fglt_ctx* c) {
 // Vertex sweeps over the per-edge triangle counts. The counts stay at the
 // canonical slots (SweepB reads lower neighbours through mir); the per-kernel
 // API, which hands C3 out in CSR order, mirrors them first.
-void local_sweeps(fglt_ctx* c, bool mirror_c3 = false) {
+void local_sweeps(fglt_ctx* c, bool mirror_c3 = false, int phases = 3) {
   if (!c->plan.c3 || c->n == 0) return;
   if (mirror_c3 && c->m > 0) {
     k_c3_mirror<<<c->grid((int64_t)c->nact * 8, 256), 256, 0, c->stream>>>(
@@ -631,7 +643,7 @@ void local_sweeps(fglt_ctx* c, bool mirror_c3 = false) {
     c->launched();
   }
   const int G = group_for((double)c->nnz / (double)c->n);
-  DISPATCH_G(G, launch_sweep_bc, c);
+  DISPATCH_G(G, launch_sweep_bc, c, phases);
 }
 
 // Bin roots [u0,u1) by key into compact lists; returns the counts (host
@@ -1937,6 +1949,38 @@ int fglt_stage_local(fglt_ctx* c, fglt_error* err) {
   }
 }
 
+// Row-partitioned vertex sweeps of rank `part` of `nparts` (rows r = part mod
+// nparts). phase 0: sweep B (c3, d14, d10, p3 of my rows; the other rows stay
+// 0) and *d_c3 / *count = the c3 vector to sum over ranks before phase 1;
+// phase 1: sweep C (d9 of my rows, reads every row's c3). fglt_stage_roots
+// then hands out d14..d15 (7 n values) instead of c4..d15 for the final sum.
+int fglt_stage_local_part(fglt_ctx* c, int part, int nparts, int phase, uint64_t** d_c3,
+                          int64_t* count, fglt_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (nparts < 1 || part < 0 || part >= nparts || (phase != 0 && phase != 1)) {
+    set_err(err, FGLT_E_PARSE, -1, -1, "fglt_stage_local_part: bad part / phase");
+    return FGLT_E_PARSE;
+  }
+  try {
+    CK(cudaSetDevice(c->device));
+    c->rows_part = part;
+    c->rows_parts = nparts;
+    c->local_partial = nparts > 1;
+    local_sweeps(c, false, phase == 0 ? 1 : 2);
+    c->rows_part = 0;
+    c->rows_parts = 1;
+    if (d_c3) *d_c3 = reinterpret_cast<uint64_t*>(c->V(V_C3));
+    if (count) *count = (phase == 0 && c->plan.c3 && nparts > 1) ? c->n : 0;
+    if (phase == 0) CK(cudaStreamSynchronize(c->stream));
+    return FGLT_OK;
+  } catch (const CudaFail& f) {
+    c->rows_part = 0;
+    c->rows_parts = 1;
+    set_err(err, f.code, -1, -1, "%s", f.msg.c_str());
+    return f.code;
+  }
+}
+
 int fglt_stage_roots(fglt_ctx* c, int64_t u0, int64_t u1, uint64_t** d_vectors, int64_t* count,
                      fglt_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
@@ -1944,9 +1988,10 @@ int fglt_stage_roots(fglt_ctx* c, int64_t u0, int64_t u1, uint64_t** d_vectors, 
     CK(cudaSetDevice(c->device));
     roots(c, u0, u1);
     CK(cudaStreamSynchronize(c->stream));
-    // c4, d13, d15 are contiguous in B_VEC
-    *d_vectors = reinterpret_cast<uint64_t*>(c->V(V_C4));
-    *count = 3 * c->n;
+    // d14, d10, p3, d9, c4, d13, d15 are contiguous in B_VEC; after
+    // row-partitioned sweeps the first four are partial too
+    *d_vectors = reinterpret_cast<uint64_t*>(c->V(c->local_partial ? V_D14 : V_C4));
+    *count = (c->local_partial ? 7 : 3) * c->n;
     return FGLT_OK;
   } catch (const CudaFail& f) {
     set_err(err, f.code, -1, -1, "%s", f.msg.c_str());

@@ -409,14 +409,18 @@ __global__ void k_list_big_rows(const int* __restrict__ rp, int n, int* __restri
     if (rp[r + 1] - rp[r] > kSweepBig) list[atomicAdd(count, 1)] = r;
 }
 
+// Rows r = r0 + i * rstep (multi-GPU: rank `r0` of `rstep` takes every
+// rstep-th row, an even share of every degree range; 0 / 1 = all rows).
 template <int G, class F>
-__global__ void k_rows_group(F f, const int* __restrict__ rp, int n) {
+__global__ void k_rows_group(F f, const int* __restrict__ rp, int n, int r0, int rstep) {
   const int lane = threadIdx.x & (G - 1);
   const int groups = (gridDim.x * blockDim.x) / G;
   const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int rounds = (n + groups - 1) / groups;
+  const int mine_n = n > r0 ? (n - r0 + rstep - 1) / rstep : 0;
+  const int rounds = (mine_n + groups - 1) / groups;
   for (int it = 0; it < rounds; ++it) {  // warp-uniform trip count (group shuffles)
-    const int r = g0 + it * groups;
+    const int i = g0 + it * groups;
+    const int r = i < mine_n ? r0 + i * rstep : n;
     u64 acc[F::NV] = {};
     bool mine = false;
     if (r < n) {
@@ -434,12 +438,13 @@ __global__ void k_rows_group(F f, const int* __restrict__ rp, int n) {
 template <class F>
 __global__ void __launch_bounds__(kSweepBlock)
 k_rows_block(F f, const int* __restrict__ rp, const int* __restrict__ list,
-             const int* __restrict__ count) {
+             const int* __restrict__ count, int r0, int rstep) {
   __shared__ u64 part[F::NV][kSweepBlock / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nb = *count;
   for (int i = blockIdx.x; i < nb; i += gridDim.x) {
     const int r = list[i];
+    if (rstep > 1 && r % rstep != r0) continue;  // block-uniform
     u64 acc[F::NV] = {};
     for (int p = rp[r] + threadIdx.x; p < rp[r + 1]; p += kSweepBlock) f.elem(r, p, acc);
 #pragma unroll

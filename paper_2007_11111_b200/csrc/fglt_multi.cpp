@@ -7,8 +7,10 @@
 //   stage_prepare (replicated: degree relabel + split/mirror)
 //   stage_bounds  (contiguous root blocks of equal exact work)
 //   stage_triangles(own roots) -> ncclAllReduce(sum) of the uint32 per-edge C3
-//   stage_local   (vertex sweeps)
-//   stage_roots(own roots)     -> ncclAllReduce(sum) of the 3n uint64 c4/d13/d15
+//   stage_local_part(rows r = rank mod world): sweep B -> ncclAllReduce(sum) of
+//                 the n uint64 c3 -> sweep C
+//   stage_roots(own roots)     -> ncclAllReduce(sum) of the 7n uint64
+//                 d14/d10/p3/d9 (my rows) + c4/d13/d15 (my roots)
 //   stage_epilogue(own block of ORIGINAL ids) -> rows straight to the caller's
 //                  tables (D2H, or a peer copy to devices[0])
 //
@@ -270,10 +272,17 @@ void rank_nccl(Group* g, int r, const Job* jp, Outcome* o) {
     stage_check(fglt_stage_triangles(R.ctx, u0, u1, &c3, &cnt, &e), e, o);
     if (cnt && g->ranks.size() > 1)
       NCK(nccl().AllReduce(c3, c3, (size_t)cnt, ncclUint32, ncclSum, R.comm, R.stream));
-    stage_check(fglt_stage_local(R.ctx, &e), e, o);
+    // vertex sweeps on my rows (r = rank mod world); sweep C reads every
+    // row's c3, so that vector is summed in between
+    const int world = (int)g->ranks.size();
+    uint64_t* c3v = nullptr;
+    stage_check(fglt_stage_local_part(R.ctx, r, world, 0, &c3v, &cnt, &e), e, o);
+    if (cnt && world > 1)
+      NCK(nccl().AllReduce(c3v, c3v, (size_t)cnt, ncclUint64, ncclSum, R.comm, R.stream));
+    stage_check(fglt_stage_local_part(R.ctx, r, world, 1, nullptr, nullptr, &e), e, o);
     uint64_t* vec = nullptr;
     stage_check(fglt_stage_roots(R.ctx, u0, u1, &vec, &cnt, &e), e, o);
-    if (cnt && g->ranks.size() > 1)
+    if (cnt && world > 1)
       NCK(nccl().AllReduce(vec, vec, (size_t)cnt, ncclUint64, ncclSum, R.comm, R.stream));
     rank_epilogue(g, r, j, o);
   } catch (const Fail& f) {
@@ -324,7 +333,16 @@ void run_emulated(Group* g, const Job& j, std::vector<Outcome>* outs) {
   if (cnt && world > 1) host_sum(ptrs, cnt, 4);
   for (int r = 0; r < world; ++r) {
     Rank& R = *g->ranks[(size_t)r];
-    stage_check(fglt_stage_local(R.ctx, &e), e, &(*outs)[(size_t)r]);
+    uint64_t* c3v = nullptr;
+    stage_check(fglt_stage_local_part(R.ctx, r, world, 0, &c3v, &cnt, &e), e,
+                &(*outs)[(size_t)r]);
+    ptrs[(size_t)r] = c3v;
+  }
+  if (cnt && world > 1) host_sum(ptrs, cnt, 8);
+  for (int r = 0; r < world; ++r) {
+    Rank& R = *g->ranks[(size_t)r];
+    stage_check(fglt_stage_local_part(R.ctx, r, world, 1, nullptr, nullptr, &e), e,
+                &(*outs)[(size_t)r]);
     uint64_t* vec = nullptr;
     stage_check(fglt_stage_roots(R.ctx, b[(size_t)r][(size_t)r], b[(size_t)r][(size_t)r + 1], &vec,
                                  &cnt, &e), e, &(*outs)[(size_t)r]);

@@ -68,6 +68,10 @@ class CudaStages:
     def local(self):
         self.ctx.stage_local()
 
+    def local_part(self, part: int, nparts: int, phase: int) -> torch.Tensor:
+        ptr, count = self.ctx.stage_local_part(part, nparts, phase)
+        return device_view(ptr, count, torch.int64, self.device)
+
     def roots(self, u0: int, u1: int) -> torch.Tensor:
         ptr, count = self.ctx.stage_roots(u0, u1)
         return device_view(ptr, count, torch.int64, self.device)
@@ -104,8 +108,14 @@ def sharded_transform(stages, rp: torch.Tensor | None, ci: torch.Tensor | None, 
     c3 = stages.triangles(u0, u1)
     if c3.numel() and world > 1:
         dist.all_reduce(c3, op=dist.ReduceOp.SUM, group=group)
-    stages.local()
-    # exchange 2: per-vertex 4-cycle / diamond / 4-clique partials
+    # vertex sweeps on my rows (r = rank mod world) only; sweep C reads every
+    # row's c3, so the c3 vector is summed in between (exchange 1b, n values)
+    c3v = stages.local_part(rank, world, 0)
+    if c3v.numel() and world > 1:
+        dist.all_reduce(c3v, op=dist.ReduceOp.SUM, group=group)
+    stages.local_part(rank, world, 1)
+    # exchange 2: per-vertex partials (world > 1: d14 d10 p3 d9 of my rows and
+    # c4 d13 d15 of my roots, 7n values; world 1: nothing to sum)
     vec = stages.roots(u0, u1)
     if vec.numel() and world > 1:
         dist.all_reduce(vec, op=dist.ReduceOp.SUM, group=group)

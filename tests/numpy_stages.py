@@ -61,6 +61,33 @@ class NumpyStages:
                 self.c3full[(r, v)] = int(c[self._canon(r, v)])
         self.C3vals = c
 
+    def local_part(self, part, nparts, phase):
+        """Row-partitioned sweeps (rows r = part mod nparts). Phase 0: c3, d14,
+        d10, p3 of my rows, returns the c3 vector to sum over ranks; phase 1:
+        d9 of my rows from the summed c3."""
+        n = self.n
+        sat = lambda a, b: a - b if a > b else 0  # noqa: E731
+        deg = [len(a) for a in self.adj]
+        if phase == 0:
+            self.local()
+            self.partial = nparts > 1
+            self.c3v = torch.zeros(n, dtype=torch.int64)
+            self.loc = np.zeros((4, n), np.int64)  # d14, d10, p3, d9
+            p2 = [sat(sum(deg[v] for v in self.adj[r]), deg[r]) for r in range(n)]
+            for r in range(part, n, nparts):
+                cc = [self.c3full[(r, x)] for x in self.adj[r]]
+                c3 = sum(cc) // 2
+                self.c3v[r] = c3
+                self.loc[0, r] = sum(c * (c - 1) // 2 for c in cc)
+                self.loc[1, r] = sum(c * sat(deg[x], 2) for c, x in zip(cc, self.adj[r]))
+                self.loc[2, r] = sat(sum(p2[x] for x in self.adj[r]),
+                                     deg[r] * sat(deg[r], 1) + 2 * c3)
+            return self.c3v if nparts > 1 else torch.zeros(0, dtype=torch.int64)
+        c3 = self.c3v.numpy()
+        for r in range(part, n, nparts):
+            self.loc[3, r] = sat(sum(int(c3[x]) for x in self.adj[r]), 2 * int(c3[r]))
+        return torch.zeros(0, dtype=torch.int64)
+
     def roots(self, u0, u1):
         n = self.n
         c4 = np.zeros(n, np.int64)
@@ -91,12 +118,19 @@ class NumpyStages:
                 if b in self.adjs[a] and x in self.adjs[a] and x in self.adjs[b]:
                     for y in (u, a, b, x):
                         d15[y] += 1
-        self.vec = torch.from_numpy(np.concatenate([c4, d13, d15]))
+        if getattr(self, "partial", False):  # 7n: d14 d10 p3 d9 | c4 d13 d15
+            self.vec = torch.from_numpy(np.concatenate([self.loc.reshape(-1), c4, d13, d15]))
+        else:
+            self.vec = torch.from_numpy(np.concatenate([c4, d13, d15]))
         return self.vec
 
     def epilogue(self, v0, v1, raw, net):
         n = self.n
         vec = self.vec.numpy()
+        loc = getattr(self, "loc", None)
+        if getattr(self, "partial", False):  # the summed row-partitioned vectors
+            loc = vec[: 4 * n].reshape(4, n)
+            vec = vec[4 * n:]
         c4, d13, d15 = vec[:n], vec[n:2 * n], vec[2 * n:]
         deg = np.array([len(a) for a in self.adj], np.int64)
         ids = [i for i in range(16) if self.mask >> i & 1]
@@ -122,6 +156,10 @@ class NumpyStages:
             col[11] = sat(d, 2) * int(c3[r])
             col[12], col[13] = int(c4[r]), int(d13[r])
             col[14] = sum(c * (c - 1) // 2 for c in cc)
+            if loc is not None:  # what the staged sweeps produced must agree
+                assert int(getattr(self, "c3v")[r]) == col[4]
+                assert (int(loc[0, r]), int(loc[1, r]), int(loc[2, r]), int(loc[3, r])) == \
+                    (col[14], col[10], col[5], col[9]), (r, loc[:, r], col)
             col[15] = int(d15[r])
             rows.append([col[i] for i in ids])
         rows = np.array(rows, dtype=np.uint64).reshape(v1 - v0, len(ids))
