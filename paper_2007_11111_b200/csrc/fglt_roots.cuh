@@ -362,6 +362,10 @@ constexpr int kC4Long = FGLT_C4_LONG;       // rows at least this long: flattene
 #define FGLT_GIANT 512
 #endif
 constexpr int kC4GiantPerTile = FGLT_GIANT;  // rows expected to put this many wedges in a tile: warp per row
+#ifndef FGLT_GIANT_BIG
+#define FGLT_GIANT_BIG FGLT_GIANT  // the same for the big-tile (1024-thread) kernel
+#endif
+constexpr int kC4GiantPerTileBig = FGLT_GIANT_BIG;
 #ifndef FGLT_PROBE_NOCUT
 #define FGLT_PROBE_NOCUT 0  // probe lists up to this long are probed whole (no cut search)
 #endif
@@ -975,7 +979,8 @@ k_c4_dense(const int* __restrict__ rp, const int* __restrict__ ci,
     // giant rows: expected >= 512 elements per tile -> warp per row
     int ntiles = 0;
     while (tb[ntiles] < u) ++ntiles;
-    const int giant_deg = max(kC4Long, kC4GiantPerTile * ntiles);
+    const int giant_deg =
+        max(kC4Long, (NT == kC4DenseThreadsS ? kC4GiantPerTile : kC4GiantPerTileBig) * ntiles);
     hi_q = nq;
     while (lo_q < hi_q) {
       const int mid = (lo_q + hi_q) >> 1;
