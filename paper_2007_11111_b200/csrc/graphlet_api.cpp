@@ -65,20 +65,29 @@ std::vector<int> ids_of_mask(std::uint32_t m) {
   return out;
 }
 
+// Blanks (spaces only, as in the reference grammar) off both ends.
 std::string_view trim_blanks(std::string_view s) {
-  while (!s.empty() && s.front() == ' ') s.remove_prefix(1);
-  while (!s.empty() && s.back() == ' ') s.remove_suffix(1);
-  return s;
+  const std::size_t b = s.find_first_not_of(' ');
+  if (b == std::string_view::npos) return {};
+  return s.substr(b, s.find_last_not_of(' ') - b + 1);
 }
 
-// One graphlet id token (decimal, whole token).
+// One graphlet id token: an optionally signed decimal filling the whole token
+// (what std::from_chars<int> accepts: '-' allowed, '+' not).
 int parse_id(std::string_view tok) {
-  int v = 0;
-  const auto [end, ec] = std::from_chars(tok.data(), tok.data() + tok.size(), v);
-  if (ec != std::errc{} || end != tok.data() + tok.size())
-    throw ParseError("malformed graphlet id '" + std::string(tok) + "'");
-  if (v < 0 || v >= kNumGraphlets) id_out_of_range(v);
-  return v;
+  const bool neg = !tok.empty() && tok.front() == '-';
+  const std::string_view digits = tok.substr(neg ? 1 : 0);
+  long long v = 0;
+  bool ok = !digits.empty();
+  for (char ch : digits) {
+    ok = ok && ch >= '0' && ch <= '9' && v <= (1ll << 31);
+    if (ok) v = v * 10 + (ch - '0');
+  }
+  if (ok && !neg && v > 0x7fffffffll) ok = false;          // int overflow: from_chars fails too
+  if (ok && neg && v > 0x80000000ll) ok = false;
+  if (!ok) throw ParseError("malformed graphlet id '" + std::string(tok) + "'");
+  if (neg ? v != 0 : v >= kNumGraphlets) id_out_of_range(neg ? -v : v);
+  return static_cast<int>(v);
 }
 
 // Ids named by one comma-separated item: "k" or "lo-hi" (inclusive).
@@ -247,35 +256,36 @@ const Csr32& SparseAdjacency::csr32() const {
 
 namespace {
 
-std::vector<std::string_view> tokens(std::string_view s) {
-  std::vector<std::string_view> out;
-  std::size_t i = 0;
-  while (i < s.size()) {
-    while (i < s.size() && std::isspace(static_cast<unsigned char>(s[i]))) ++i;
-    std::size_t j = i;
-    while (j < s.size() && !std::isspace(static_cast<unsigned char>(s[j]))) ++j;
-    if (j > i) out.push_back(s.substr(i, j - i));
-    i = j;
+inline bool is_blank(char c) { return std::isspace(static_cast<unsigned char>(c)) != 0; }
+
+// The whitespace-separated fields of one line, scanned in place: the first
+// kKeep are kept, all are counted (the grammars need at most five).
+struct Fields {
+  static constexpr std::size_t kKeep = 8;
+  std::array<std::string_view, kKeep> at{};
+  std::size_t count = 0;
+  explicit Fields(std::string_view line) {
+    const char* p = line.data();
+    const char* const e = p + line.size();
+    for (;;) {
+      p = std::find_if_not(p, e, is_blank);
+      if (p == e) break;
+      const char* q = std::find_if(p, e, is_blank);
+      if (count < kKeep) at[count] = std::string_view(p, static_cast<std::size_t>(q - p));
+      ++count;
+      p = q;
+    }
   }
-  return out;
-}
+  std::string_view operator[](std::size_t k) const { return at[k]; }
+};
 
-std::int64_t to_int(std::string_view t, std::size_t line, const char* what) {
-  std::int64_t v = 0;
-  const char* end = t.data() + t.size();
-  auto r = std::from_chars(t.data(), end, v);
-  if (r.ec != std::errc{} || r.ptr != end)
-    throw ParseError("line " + std::to_string(line) + ": malformed " + what + " '" +
-                     std::string(t) + "'");
-  return v;
-}
-
-std::string lower(std::string_view s) {
-  std::string o(s);
-  for (char& c : o) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+// ASCII case folding for the Matrix Market keywords.
+std::string folded(std::string_view s) {
+  std::string o(s.size(), '\0');
+  std::transform(s.begin(), s.end(), o.begin(),
+                 [](unsigned char c) { return static_cast<char>(std::tolower(c)); });
   return o;
 }
-
 
 }  // namespace
 
@@ -300,10 +310,11 @@ std::string slurp(std::istream& in) {
   return buf;
 }
 
-std::string_view trim_ws(std::string_view s) {
-  while (!s.empty() && std::isspace(static_cast<unsigned char>(s.front()))) s.remove_prefix(1);
-  while (!s.empty() && std::isspace(static_cast<unsigned char>(s.back()))) s.remove_suffix(1);
-  return s;
+std::string_view strip(std::string_view s) {
+  const char* b = std::find_if_not(s.data(), s.data() + s.size(), is_blank);
+  const char* e = s.data() + s.size();
+  while (e > b && is_blank(e[-1])) --e;
+  return std::string_view(b, static_cast<std::size_t>(e - b));
 }
 
 // Next line of buf starting at *pos (without the '\n'); false at the end.
@@ -360,7 +371,7 @@ std::vector<ParsedChunk> parse_chunks(std::string_view buf, std::size_t from, F 
       ++c.lines;
       if (c.failed) continue;  // keep counting lines only
       std::string suffix;
-      if (!entry(trim_ws(line), &c, &suffix)) {
+      if (!entry(strip(line), &c, &suffix)) {
         c.failed = true;
         c.fail_line = c.lines;
         c.entries_before = c.edges.size();
@@ -386,9 +397,9 @@ EdgeCollection parse_edge_list(std::istream& in) {
   const std::string buf = slurp(in);
   auto chunks = parse_chunks(buf, 0, [](std::string_view body, ParsedChunk* c, std::string* err) {
     if (body.empty() || body.front() == '#' || body.front() == '%') return true;
-    auto t = tokens(body);
-    if (t.size() != 2) {
-      *err = ": expected 'u v', got " + std::to_string(t.size()) + " tokens";
+    const Fields t(body);
+    if (t.count != 2) {
+      *err = ": expected 'u v', got " + std::to_string(t.count) + " tokens";
       return false;
     }
     std::int64_t u = 0, v = 0;
@@ -417,12 +428,12 @@ EdgeCollection parse_matrix_market(std::istream& in) {
   std::string_view line;
   if (!next_line(buf, &pos, &line)) throw ParseError("empty Matrix Market stream");
   ++ln;
-  auto banner = tokens(line);
-  if (banner.size() < 5 || lower(banner[0]) != "%%matrixmarket" || lower(banner[1]) != "matrix")
+  const Fields banner(line);
+  if (banner.count < 5 || folded(banner[0]) != "%%matrixmarket" || folded(banner[1]) != "matrix")
     throw ParseError("line 1: missing %%MatrixMarket matrix banner");
-  if (lower(banner[2]) != "coordinate")
-    throw ParseError("line 1: only coordinate format is supported, got '" + lower(banner[2]) + "'");
-  const std::string field = lower(banner[3]), sym = lower(banner[4]);
+  const std::string format = folded(banner[2]), field = folded(banner[3]), sym = folded(banner[4]);
+  if (format != "coordinate")
+    throw ParseError("line 1: only coordinate format is supported, got '" + format + "'");
   if (field != "pattern" && field != "real" && field != "integer")
     throw ParseError("line 1: unsupported field '" + field + "'");
   if (sym != "general" && sym != "symmetric")
@@ -433,13 +444,16 @@ EdgeCollection parse_matrix_market(std::istream& in) {
   for (;;) {
     if (!next_line(buf, &pos, &line)) throw ParseError("unexpected end of stream before size line");
     ++ln;
-    const std::string_view body = trim_ws(line);
+    const std::string_view body = strip(line);
     if (body.empty() || body.front() == '%') continue;
-    auto t = tokens(body);
-    if (t.size() != 3) throw ParseError("line " + std::to_string(ln) + ": expected 'rows cols nnz'");
-    rows = to_int(t[0], ln, "row count");
-    cols = to_int(t[1], ln, "column count");
-    nnz = to_int(t[2], ln, "entry count");
+    const Fields t(body);
+    if (t.count != 3) throw ParseError("line " + std::to_string(ln) + ": expected 'rows cols nnz'");
+    const char* const what[3] = {"row count", "column count", "entry count"};
+    std::int64_t* const dst[3] = {&rows, &cols, &nnz};
+    for (int k = 0; k < 3; ++k)
+      if (!parse_i64(t[k], dst[k]))
+        throw ParseError("line " + std::to_string(ln) + ": malformed " + what[k] + " '" +
+                         std::string(t[k]) + "'");
     break;
   }
   if (rows != cols)
@@ -448,8 +462,8 @@ EdgeCollection parse_matrix_market(std::istream& in) {
   if (rows < 0 || nnz < 0) throw ParseError("negative size header");
   auto chunks = parse_chunks(buf, pos, [&](std::string_view body, ParsedChunk* c, std::string* err) {
     if (body.empty() || body.front() == '%') return true;
-    auto t = tokens(body);
-    if (t.size() != per_entry) {
+    const Fields t(body);
+    if (t.count != per_entry) {
       *err = ": expected " + std::to_string(per_entry) + " tokens per entry";
       return false;
     }
