@@ -260,6 +260,10 @@ def reference_arm(args):
             times.append(secs)
             if time.time() - t_start > 150:  # keep the arm within a few minutes
                 break
+        single = None
+        if cfg in (1, 2):  # also one worker thread on the small configs
+            _, _, s1, _ = ob.ref_transform(rp, ci, mask, False, 1)
+            single = {"threads": 1, "ms_per_step": s1 * 1e3, "value": m / s1, "unit": UNIT}
         d15 = None
         if big:
             t = _capped_ref_d15(tmp, REF_D15_CAP_S)
@@ -285,7 +289,7 @@ def reference_arm(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "kernel_times": stats.get("kernel_times") if stats else None,
-            "d15": d15, "host": _host_facts(),
+            "d15": d15, "single_thread": single, "host": _host_facts(),
             "note": "value is an upper bound on the reference's full-Σ16 rate where d15 is "
                     "excluded" if big else "full Σ16"}
     print(json.dumps(line))

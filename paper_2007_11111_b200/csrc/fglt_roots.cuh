@@ -2303,6 +2303,10 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
 
 // Diamonds from the triangle list (the kD13 terms of k_roots_block, see
 // above): block per piece, per-member partial sums in shared memory.
+#ifndef FGLT_DLIST_UNROLL
+#define FGLT_DLIST_UNROLL 1  // measured at R-MAT 20 (diamond rows, ms): 1: 2.5, 2: 2.5, 4: 2.9, 8: 3.4 (L2 gather rate, not latency)
+#endif
+constexpr int kDlistUnroll = FGLT_DLIST_UNROLL;
 template <int NT>
 __global__ void __launch_bounds__(NT)
 k_diamond_list(const TriPiece* __restrict__ pieces, const unsigned* __restrict__ npieces,
@@ -2334,17 +2338,35 @@ k_diamond_list(const TriPiece* __restrict__ pieces, const unsigned* __restrict__
     const bool narrow = (u64)s * (u64)(rp[u + 1] - rp[u]) < (1ull << 32);
     u64 tu = 0;
     const uint2* r = rec + pc.start;
-    for (unsigned i = threadIdx.x; i < pc.count; i += NT) {
-      const uint2 x = r[i];
-      const int a = (int)(x.x & 0xffffu), b = (int)(x.x >> 16);
-      const u32 ca = __ldg(C3f + s0 + a), cb = __ldg(C3f + s0 + b), cp = __ldg(C3f + x.y);
-      tu += (u64)cp - 1;
-      if (narrow) {
-        atomicAdd(reinterpret_cast<u32*>(sD + a), cb - 1);
-        atomicAdd(reinterpret_cast<u32*>(sD + b), ca - 1);
-      } else {
-        smem_add_u64(sD + a, (u64)cb - 1);
-        smem_add_u64(sD + b, (u64)ca - 1);
+    // kDlistUnroll records per thread and round: the records, then their three
+    // count gathers, are all issued before the first shared add
+    for (unsigned i0 = threadIdx.x; i0 < pc.count; i0 += kDlistUnroll * NT) {
+      uint2 x[kDlistUnroll];
+      u32 ca[kDlistUnroll], cb[kDlistUnroll], cp[kDlistUnroll];
+#pragma unroll
+      for (int j = 0; j < kDlistUnroll; ++j) {
+        const unsigned i = i0 + j * NT;
+        x[j] = i < pc.count ? r[i] : make_uint2(0xffffffffu, 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < kDlistUnroll; ++j) {
+        if (x[j].x == 0xffffffffu) continue;  // a == b == 0xffff never occurs (a < b)
+        ca[j] = __ldg(C3f + s0 + (int)(x[j].x & 0xffffu));
+        cb[j] = __ldg(C3f + s0 + (int)(x[j].x >> 16));
+        cp[j] = __ldg(C3f + x[j].y);
+      }
+#pragma unroll
+      for (int j = 0; j < kDlistUnroll; ++j) {
+        if (x[j].x == 0xffffffffu) continue;
+        const int a = (int)(x[j].x & 0xffffu), b = (int)(x[j].x >> 16);
+        tu += (u64)cp[j] - 1;
+        if (narrow) {
+          atomicAdd(reinterpret_cast<u32*>(sD + a), cb[j] - 1);
+          atomicAdd(reinterpret_cast<u32*>(sD + b), ca[j] - 1);
+        } else {
+          smem_add_u64(sD + a, (u64)cb[j] - 1);
+          smem_add_u64(sD + b, (u64)ca[j] - 1);
+        }
       }
     }
     __syncthreads();

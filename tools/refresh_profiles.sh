@@ -9,9 +9,9 @@ timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/p
 echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 for c in 3 2 5 4; do
   python tools/profile_step.py $c > /dev/null 2>&1 && \
-  timeout 900 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none --csv --log-file gpurun_out/launches$c.csv python tools/profile_step.py $c > gpurun_out/ncu$c.log 2>&1
+  timeout 900 ncu --nvtx --nvtx-include "step/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors.sum,lts__t_sectors_lookup_hit.sum --cache-control none --clock-control none --csv --log-file gpurun_out/launches$c.csv python tools/profile_step.py $c > gpurun_out/ncu$c.log 2>&1
   echo "ncu $c rc=$?"
-  python tools/make_ncu_summary.py gpurun_out/launches$c.csv $c "ncu --nvtx --nvtx-include step/ --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none of tools/profile_step.py $c"
+  python tools/make_ncu_summary.py gpurun_out/launches$c.csv $c "ncu --nvtx --nvtx-include step/ --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors.sum,lts__t_sectors_lookup_hit.sum --cache-control none --clock-control none of tools/profile_step.py $c"
 done
 # dominant kernel: one --set full capture (after the plain run above exited 0)
 bash tools/gpu_full.sh k_c4_dense 3 1 dense
