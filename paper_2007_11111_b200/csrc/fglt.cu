@@ -224,6 +224,7 @@ struct fglt_ctx {
   DictInfo* d_dict = nullptr;
   u64* d_small = nullptr;  // [0] err key, [1] W, [2] d_max, [3..] bin counts
   bool have_stats = false;
+  bool dmax_valid = false;  // dmax is this graph's (set by the stats readbacks)
   uint64_t W = 0, dmax = 0, maxout = 0, nact = 0;
 
   // last ingest result (fglt_build_csr), on the device
@@ -351,12 +352,15 @@ void list_big_rows(fglt_ctx* c) {
 
 template <int G, class F>
 void run_rows(fglt_ctx* c, const F& f) {
-  list_big_rows(c);
+  // no row longer than kSweepBig (known d_max): no list, no block-per-row launch
+  const bool no_big = c->dmax_valid && c->dmax <= (u64)kSweepBig;
+  if (!no_big) list_big_rows(c);
   const int r0 = c->rows_part, rs = std::max(c->rows_parts, 1);
   k_rows_group<G, F><<<c->grid((c->n + rs - 1) / rs * G, 256), 256, 0, c->stream>>>(
       f, c->rp, (int)c->n, r0, rs);
   check_launch();
   c->launched();
+  if (no_big) return;
   k_rows_block<F><<<c->sms * 4, kSweepBlock, 0, c->stream>>>(
       f, c->rp, c->big_rows, reinterpret_cast<const int*>(c->d_small + 5), r0, rs);
   check_launch();
@@ -463,6 +467,7 @@ void read_input_stats(fglt_ctx* c) {
   CK(cudaStreamSynchronize(c->stream));
   c->W = h[0];
   c->dmax = h[1];
+  c->dmax_valid = true;
   c->nact = h[3];
 }
 
@@ -497,6 +502,7 @@ void prepare(fglt_ctx* c, const int* d_rp, const int* d_ci, int64_t n, int64_t n
   c->rp = d_rp;
   c->ci = d_ci;
   c->have_stats = false;
+  c->dmax_valid = false;
   if (n > 0) {
     k_graph_stats<<<c->grid(n, 256, 4), 256, 0, c->stream>>>(d_rp, N, c->d_small + 1);
     check_launch();
@@ -618,6 +624,7 @@ void read_graph_stats(fglt_ctx* c) {
   CK(cudaStreamSynchronize(c->stream));
   c->W = h[0];
   c->dmax = h[1];
+  c->dmax_valid = true;
   c->maxout = h[2];
   c->nact = h[3];
   c->have_stats = true;
