@@ -1,13 +1,18 @@
 mkdir -p gpurun_out
-timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench3.json 2> gpurun_out/bench3.err; echo "bench3 rc=$?"
-timeout 300 python bench.py --config 1 --no-cpu-baseline > gpurun_out/bench1.json 2> gpurun_out/bench1.err; echo "bench1 rc=$?"
-timeout 300 python bench.py --config 2 --no-cpu-baseline > gpurun_out/bench2.json 2> gpurun_out/bench2.err; echo "bench2 rc=$?"
-timeout 300 python bench.py --config 5 --no-cpu-baseline > gpurun_out/bench5.json 2> gpurun_out/bench5.err; echo "bench5 rc=$?"
-timeout 600 python bench.py --config 4 --no-cpu-baseline --steps 3 > gpurun_out/bench4.json 2> gpurun_out/bench4.err; echo "bench4 rc=$?"
-python -c "
-import json
-for c in (1,2,3,4,5):
-    d=json.load(open('gpurun_out/bench%d.json'%c)); print(c, round(d['ms_per_step'],3), round(d['e2e']['ms_per_step'],3), d['gpu_launches'], d['roofline']['frac'])
-"
+export FGLT_LIB_OVERRIDE=$PWD/variants/checked/libfglt.so
+OUT=gpurun_out/bounds_checked_runs.txt
+echo "# FGLT_DEBUG_BOUNDS build (tools/build_variant.sh checked -DFGLT_DEBUG_BOUNDS) of the final round-2 source: sanitize workload + full configs" > $OUT
+run() { # name, command...
+  n=$1; shift
+  timeout 900 "$@" > gpurun_out/$n.log 2>&1
+  echo "== $n: $(grep -c 'FGLT bounds' gpurun_out/$n.log) bounds violations (rc $?)" >> $OUT
+  grep -v 'FGLT bounds' gpurun_out/$n.log | tail -3 >> $OUT
+}
+run bounds_cases python tools/sanitize_cases.py
+run bounds_cfg3 python tools/run_case.py cfg 3
+run bounds_cfg5 python tools/run_case.py cfg 5
+run bounds_cfg2 python tools/run_case.py cfg 2
+run bounds_cfg1 python tools/run_case.py cfg 1 check
+run bounds_cfg4 python tools/run_case.py cfg 4
+run bounds_rmat16_check python tools/run_case.py rmat 16 check
+cat $OUT
