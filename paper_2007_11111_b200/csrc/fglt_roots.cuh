@@ -320,7 +320,14 @@ __device__ __forceinline__ u64 block_sum_u64(u64 v, u64* red) {
 #define FGLT_C4B_THREADS 1024
 #endif
 #ifndef FGLT_HASH_WEIGHT
-#define FGLT_HASH_WEIGHT 1
+// hash-pass cost vs the big-tile dense cost. Measured after the dense kernel's
+// lane-row rewrite (four-cycle phase, ms; R-MAT 20 / R-MAT 23): 1: 17.6 / 357,
+// 2: 16.3 / 357, 4: 16.1 / 351, 8: 16.2 / 360, 16: 16.5 / 383, never hash:
+// 16.2 / 383
+#define FGLT_HASH_WEIGHT 4
+#endif
+#ifndef FGLT_HASH_WEIGHT_S
+#define FGLT_HASH_WEIGHT_S FGLT_HASH_WEIGHT  // ... vs the small-tile dense cost
 #endif
 #ifndef FGLT_TILE_FIXED
 #define FGLT_TILE_FIXED 2048  // per-tile fixed cost (barriers, setup) in the cost model
@@ -447,7 +454,9 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
     } else {
       const u64 nq = (u64)(split[u] - rp[u]);
       P = (w + kC4HashFill - 1) / kC4HashFill;
-      const u64 cost_hash = FGLT_HASH_WEIGHT * (P * (w + (1ull << kC4HashLog)) + w);
+      const u64 cost_base = P * (w + (1ull << kC4HashLog)) + w;
+      const u64 cost_hash = FGLT_HASH_WEIGHT * cost_base;
+      const u64 cost_hash_s = FGLT_HASH_WEIGHT_S * cost_base;
       const bool pack = u <= b16;  // no 32-bit band below u
       u64 tiles, bytes, tiles_s, bytes_s;
       dense_span((u64)u, (u64)b4, (u64)b8, (u64)b16, kC4TileBytes, &tiles, &bytes);
@@ -462,7 +471,7 @@ __global__ void k_c4_class(const int* __restrict__ rp, const int* __restrict__ s
               ? ~0ull
               : (bytes_s / 8 + tiles_s * (FGLT_TILE_FIXED / 2 + FGLT_ROW_TILE * nq) + 2 * w) *
                     FGLT_SMALL_EFF / 100;
-      if (cost_hash <= cost_dense && (!pack || cost_hash <= cost_small)) c = 4;
+      if (cost_hash <= cost_dense && (!pack || cost_hash_s <= cost_small)) c = 4;
       else if (!pack) c = 6;
       else c = cost_small < cost_dense ? 7 : 5;
     }
