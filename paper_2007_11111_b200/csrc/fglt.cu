@@ -38,6 +38,13 @@ namespace {
 #ifndef FGLT_TL_MEM_FRAC
 #define FGLT_TL_MEM_FRAC 0.70  // triangle-list pool: at most this share of the free HBM
 #endif
+#ifndef FGLT_BIG512_MAXOUT
+// graphs with max |N+(u)| above this run the 257..1024 root bins on 512
+// threads. Always, since the triangle kernel fits 64 registers
+// (FGLT_ROOTS_QUADS 1): R-MAT 20 triangles 12.1 -> 11.7 ms (it was +12 % at 80
+// registers)
+#define FGLT_BIG512_MAXOUT 0
+#endif
 #ifndef FGLT_FLAT_DMAX
 #define FGLT_FLAT_DMAX 0  // graphs with d_max up to this are not relabelled by degree (<= 255); 0 = off:
                           // measured on the SBM (64: DRAM 41 -> 28 GB/step but the 4-cycle classes get uneven roots, 24.4 -> 25.0 ms)
@@ -718,10 +725,10 @@ __global__ void k_outdeg_key(const int* __restrict__ send, const int* __restrict
 #define FGLT_SPLIT_BIG 0  // big-tile packed roots as (root, tile) items too
 #endif
 #ifndef FGLT_SLAB_BLOCKS_PER_SM
-#define FGLT_SLAB_BLOCKS_PER_SM 2  // resident global-slab root blocks per SM (|S| > 1024)
+#define FGLT_SLAB_BLOCKS_PER_SM 1  // resident global-slab root blocks per SM (|S| > 1024)
 #endif
 #ifndef FGLT_SLAB_THREADS
-#define FGLT_SLAB_THREADS 256  // block threads of the global-slab root bin (|S| > 1024)
+#define FGLT_SLAB_THREADS 1024  // block threads of the global-slab root bin (|S| > 1024); R-MAT 23 triangles: 2 x 256: 216, 2 x 512: 210, 1 x 1024: 206 ms
 #endif
 constexpr int kSlabThreads = FGLT_SLAB_THREADS;
 #ifndef FGLT_DLIST_NT
@@ -876,7 +883,7 @@ void roots_pass(fglt_ctx* c) {
     // graphs with roots beyond the shared-memory bins have long probe lists:
     // their 257..1024 bins take 512-thread blocks (R-MAT 23 -7 %; R-MAT 20,
     // max |S| 777, keeps 256: +12 % otherwise)
-    const int big_nt = c->maxout > (u64)kBlockS ? 512 : kRootsThreads;
+    const int big_nt = c->maxout > (u64)FGLT_BIG512_MAXOUT ? 512 : kRootsThreads;
     const int nt = global ? kSlabThreads
                           : (b == kFirstBlockBin ? FGLT_BIN1_NT
                                                  : b == kFirstBlockBin + 1 ? FGLT_BIN2_NT : big_nt);

@@ -401,6 +401,10 @@ constexpr int kC4GiantPerTileBig = FGLT_GIANT_BIG;
 constexpr int kBatchG = FGLT_BATCH_LANE_ROW ? FGLT_BATCH_G : 1;
 constexpr int kBatchRows = 32 / kBatchG;
 constexpr int kQuadsInFlight = FGLT_QUADS;          // 16-byte loads in flight per lane (dense batches)
+#ifndef FGLT_ROOTS_QUADS
+#define FGLT_ROOTS_QUADS 1  // the same for the triangle pass (k_roots_block): 1 keeps it at 64 registers (2: 80), R-MAT 23 triangles 234 -> 215 ms
+#endif
+constexpr int kRootsQuads = FGLT_ROOTS_QUADS;
 constexpr int kC4BlockThreads = FGLT_C4B_THREADS;  // class-4 block (one 128 KB table per SM)
 
 // Dense tiles use counters as narrow as the target's degree allows: L[w] <=
@@ -2094,11 +2098,11 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
         const int k0 = wid * per, k1 = min(T, k0 + per);
         if (k0 + lane < k1) {
           int r = upper_row(f_off, k0 + lane, NT);
-          for (int kk = k0 + lane; kk < k1; kk += 32 * kQuadsInFlight) {
-            int4 v[kQuadsInFlight];
-            int lt[kQuadsInFlight], ht[kQuadsInFlight], rr[kQuadsInFlight], e0[kQuadsInFlight];
+          for (int kk = k0 + lane; kk < k1; kk += 32 * kRootsQuads) {
+            int4 v[kRootsQuads];
+            int lt[kRootsQuads], ht[kRootsQuads], rr[kRootsQuads], e0[kRootsQuads];
 #pragma unroll
-            for (int j = 0; j < kQuadsInFlight; ++j) {
+            for (int j = 0; j < kRootsQuads; ++j) {
               const int kj = kk + 32 * j;
               lt[j] = 4;
               ht[j] = 0;
@@ -2114,7 +2118,7 @@ k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
               }
             }
 #pragma unroll
-            for (int j = 0; j < kQuadsInFlight; ++j) {
+            for (int j = 0; j < kRootsQuads; ++j) {
               if (ht[j] <= 0) break;
               to_row(c0, rr[j]);
               const int a = c0 + rr[j];
