@@ -1885,11 +1885,12 @@ constexpr int kRootsThreads = FGLT_ROOTS_THREADS;  // block threads for |S| > 25
 #endif
 constexpr int kPairsInFlight = FGLT_PAIRS_IN_FLIGHT;  // hub-row words in flight per lane
 
-#ifndef FGLT_ROOTS_SMALL_TPS
-#define FGLT_ROOTS_SMALL_TPS 0  // resident threads per SM the 64/128-thread root bins are compiled for (0: no cap = 64 registers; 1280/1536/2048 cap at 48/40/32 with spills: R-MAT 20 triangles 11.7 -> 14.3/15.2/16.0 ms)
-#endif
+// (Measured and dropped: a minimum-blocks launch bound capping the 64/128-
+// thread bins at 48/40/32 registers spills, R-MAT 20 triangles 11.7 -> 14.3/
+// 15.2/16.0 ms; even a bound of (NT, 1) changes the allocation to 86
+// registers and loses the 64-register occupancy: keep plain (NT).)
 template <bool kC3, bool kD13, bool kD15, bool kGlobal, int NT>
-__global__ void __launch_bounds__(NT, (NT <= 128 && FGLT_ROOTS_SMALL_TPS) ? FGLT_ROOTS_SMALL_TPS / NT : 1)
+__global__ void __launch_bounds__(NT)
 k_roots_block(const int* __restrict__ rp, const int* __restrict__ ci,
               const int* __restrict__ split, const int* __restrict__ send,
               u32* __restrict__ C3f,
