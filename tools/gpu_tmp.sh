@@ -1,2 +1,2 @@
-bash tools/run_variants.sh 3 pin
-bash tools/run_variants.sh 4 pin
+bash tools/run_variants.sh 5
+bash tools/run_variants.sh 2
